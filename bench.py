@@ -1,0 +1,415 @@
+#!/usr/bin/env python3
+"""bench.py — T-product throughput (effective fp64 GFLOP/s) on B200.
+
+Workload: BASELINE.json configs[4], the 1/2/4/8-GPU scaling case
+(m = n = s = 2048, p = 32, components U[-1,1) from the reference generator),
+override with --config {1..5}.  One step = one full T-product C = A *_T B
+(K1 tube FFT of A and B -> K2 paired-frequency DMMA GEMM -> K3 inverse tube
+FFT) over inputs already resident in HBM.  With N ranks (torchrun) the rows
+of A and C are sharded in slabs of ceil(m/N) and B is broadcast from rank 0
+with NCCL inside the timed step (strong scaling: total work fixed).
+
+metric value = F_eff / step time, F_eff = 32 m n s p + 10 (mn + ns + ms) p log2 p
+(SURVEY §8(d)).  e2e = the same metric through the host-buffer C-ABI call
+qt_tprod_f64_host (pinned host in/out, H2D + D2H inside the timed region).
+
+--impl reference times the reference's own CPU tprod_fast (oracle/_ref, built
+from /root/reference's sources) on the host cores over bounded tiles of the
+same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAK_FP64_DMMA_TFLOPS = 37.1  # measured burst, profiles/r01_fp64_peak.txt (tools/microbench/fp64_peak.cu)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self._t.join(timeout=2)
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------- CPU reference
+def reference_tiles(cfg, tile: int, count: int, seed: int = 7):
+    """`count` (row-slab x column-slab) tiles of the workload, spread over C."""
+    rng = np.random.default_rng(seed)
+    tr, tc = min(tile, cfg.m), min(tile, cfg.s)
+    nr, nc = -(-cfg.m // tr), -(-cfg.s // tc)
+    picks = rng.choice(nr * nc, size=min(count, nr * nc), replace=False)
+    out = []
+    for k in picks:
+        r0, c0 = (int(k) // nc) * tr, (int(k) % nc) * tc
+        out.append((r0, min(cfg.m, r0 + tr), c0, min(cfg.s, c0 + tc)))
+    return out, nr * nc
+
+
+def time_reference(cfg, a, b, tile: int, threads: int):
+    """Run the UNMODIFIED reference tprod_fast (oracle/_ref) on `threads`
+    tiles in parallel, one host thread each (ctypes releases the GIL).  Each
+    tile is bitwise the matching block of the reference's full result (rows
+    of C depend only on rows of A, columns only on columns of B), so
+    (tile fraction of F_eff) / wall time is the reference's throughput on the
+    workload with all host cores busy."""
+    import oracle as O
+    tiles, total = reference_tiles(cfg, tile, threads)
+    jobs = []
+    for (r0, r1, c0, c1) in tiles:
+        at = (np.ascontiguousarray(a.t1[:, r0:r1, :]), np.ascontiguousarray(a.t2[:, r0:r1, :]))
+        bt = (np.ascontiguousarray(b.t1[:, :, c0:c1]), np.ascontiguousarray(b.t2[:, :, c0:c1]))
+        jobs.append((at, bt))
+    th = [threading.Thread(target=O.ref_tprod_fast, args=j) for j in jobs]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    frac = sum((r1 - r0) * (c1 - c0) for (r0, r1, c0, c1) in tiles) / float(cfg.m * cfg.s)
+    gflops = frac * cfg.flops_eff / wall / 1e9
+    sample = (f"{len(tiles)} tiles of {tiles[0][1] - tiles[0][0]} rows x {tiles[0][3] - tiles[0][2]} cols "
+              f"({frac * 100:.3f}% of C), one tile per thread, reference tprod_fast unmodified")
+    return gflops, wall, sample
+
+
+def auto_tile(cfg):
+    # ~10-25 s of single-thread reference work per tile on a ~3 GHz Xeon
+    return {1: 32, 2: 128, 3: 16, 4: 64, 5: 128}.get(cfg.idx, 64)
+
+
+def host_inputs(cfg, pinned: bool):
+    """Seeded host inputs (reference generator / SURVEY §8(d) distributions)."""
+    import torch
+
+    import paper_2212_14318_b200 as qt
+    sa, sb = cfg.seeds()
+    shp_a, shp_b = (cfg.p, cfg.m, cfg.n), (cfg.p, cfg.n, cfg.s)
+
+    def alloc(shape):
+        t = torch.empty(shape + (2,), dtype=torch.float64, pin_memory=pinned)
+        return t
+
+    bufs = {k: alloc(shp_a if k.startswith("a") else shp_b) for k in ("a1", "a2", "b1", "b2")}
+    a = qt.CdTensor3(cfg.m, cfg.n, cfg.p, bufs["a1"].numpy().view(np.complex128)[..., 0],
+                     bufs["a2"].numpy().view(np.complex128)[..., 0])
+    b = qt.CdTensor3(cfg.n, cfg.s, cfg.p, bufs["b1"].numpy().view(np.complex128)[..., 0],
+                     bufs["b2"].numpy().view(np.complex128)[..., 0])
+    # CdTensor3 keeps views of the pinned buffers (no copy): generate in place
+    assert a.t1.ctypes.data == bufs["a1"].data_ptr()
+    qt.gen_tensor(cfg.m, cfg.n, cfg.p, sa, cfg.dist_a, cfg.scale_a, out=a)
+    qt.gen_tensor(cfg.n, cfg.s, cfg.p, sb, cfg.dist_b, cfg.scale_b, out=b)
+    return a, b, bufs
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqtref.so not built "
+                          "(make -C oracle ref needs /root/reference)"}))
+        return 0
+    a, b, _ = host_inputs(cfg, pinned=False)
+    threads = os.cpu_count() or 1
+    tile = args.cpu_tile or auto_tile(cfg)
+    for _ in range(args.warmup):
+        time_reference(cfg, a, b, max(8, tile // 4), threads)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        g, w, sample = time_reference(cfg, a, b, tile, threads)
+        vals.append(g)
+        walls.append(w)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference",
+        "metric": "T-product throughput (effective fp64 GFLOP/s)",
+        "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, reference generator)",
+        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
+                   "parallelism": f"{threads} host threads, tile-parallel"},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2212_14318_b200 as qt
+    from paper_2212_14318_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = qt._native.lib()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    lo, hi = shard.row_slab(cfg.m, world, rank)
+    rows = hi - lo
+    a, b, _ = host_inputs(cfg, pinned=True)
+    # device-resident inputs (slab of A on every rank; B on rank 0, broadcast per step)
+    da1 = torch.from_numpy(a.t1[:, lo:hi].view(np.float64)).to(dev).contiguous()
+    da2 = torch.from_numpy(a.t2[:, lo:hi].view(np.float64)).to(dev).contiguous()
+    if rank == 0:
+        db1 = torch.from_numpy(b.t1.view(np.float64)).to(dev)
+        db2 = torch.from_numpy(b.t2.view(np.float64)).to(dev)
+    else:
+        db1 = torch.empty((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
+        db2 = torch.empty_like(db1)
+    dc1 = torch.empty((cfg.p, rows, 2 * cfg.s), dtype=torch.float64, device=dev)
+    dc2 = torch.empty_like(dc1)
+    l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    big = (cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s)) > 2 * 126e6
+
+    def step():
+        if world > 1:
+            dist.broadcast(db1, 0)
+            dist.broadcast(db2, 0)
+        rc = L.qt_tprod_f64_device(da1.data_ptr(), da2.data_ptr(), db1.data_ptr(), db2.data_ptr(), dc1.data_ptr(),
+                                   dc2.data_ptr(), rows, cfg.n, cfg.s, cfg.p, sh)
+        qt._native.check(rc, "tprod_fast")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.qt_kernel_launches()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if not big:
+                l2_flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = L.qt_kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cfg.flops_eff / (ms * 1e-3) / 1e9  # whole-job GFLOP/s (all ranks' rows)
+
+    # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
+    ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
+    bh = torch.empty((2, cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
+    qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
+                                                rows, cfg.n, cfg.p, sh), "qfft3")
+    qt._native.check(L.qt_qfft3_conj_f64_device(db1.data_ptr(), db2.data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(),
+                                                cfg.n, cfg.s, cfg.p, sh), "qfft3")
+
+    def timed(fn, reps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for s0, e0 in evs:
+            if not big:
+                l2_flush.zero_()
+            s0.record(stream)
+            fn()
+            e0.record(stream)
+        torch.cuda.synchronize()
+        return sum(s0.elapsed_time(e0) for s0, e0 in evs) / reps
+
+    gemm_ms = timed(lambda: L.qt_spectral_product_f64_device(ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(),
+                                                             bh[1].data_ptr(), dc1.data_ptr(), dc2.data_ptr(), rows,
+                                                             cfg.n, cfg.s, cfg.p, sh), max(2, args.steps))
+    fftA_ms = timed(lambda: L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(),
+                                                       ah[1].data_ptr(), rows, cfg.n, cfg.p, sh), max(3, args.steps))
+    ifft_ms = timed(lambda: L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
+                                                        dc2.data_ptr(), rows, cfg.s, cfg.p, sh), max(3, args.steps))
+    del ah, bh
+    peaks, peak_src = load_peaks()
+    gemm_tf = 32.0 * rows * cfg.n * cfg.s * cfg.p / (gemm_ms * 1e-3) / 1e12
+    fftA_gbs = 2 * cfg.bytes_tensor(rows, cfg.n) / (fftA_ms * 1e-3) / 1e9
+    ifft_gbs = 2 * cfg.bytes_tensor(rows, cfg.s) / (ifft_ms * 1e-3) / 1e9
+    gemm_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s) + cfg.bytes_tensor(rows, cfg.s)
+    gemm_ai = 32.0 * rows * cfg.n * cfg.s * cfg.p / gemm_bytes
+    ridge = PEAK_FP64_DMMA_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if gemm_ai >= ridge:
+        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": gemm_tf,
+                "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": gemm_tf / PEAK_FP64_DMMA_TFLOPS,
+                "peak_source": "measured fp64 DMMA burst (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no fp64",
+                "algorithmic": "32*m*n*s*p flops per launch", "kernel_ms": gemm_ms, "share_of_step": gemm_ms / ms,
+                "traffic": None}
+    else:
+        gb = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "hbm", "achieved": gb,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"],
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "kernel_ms": gemm_ms, "share_of_step": gemm_ms / ms,
+                "traffic": None}
+    stages = {
+        "K1_fft_A": {"ms": fftA_ms, "GB_s": fftA_gbs, "frac_hbm": fftA_gbs / peaks["hbm_gbs"]},
+        "K2_gemm": {"ms": gemm_ms, "TFLOP_s": gemm_tf, "frac_fp64": gemm_tf / PEAK_FP64_DMMA_TFLOPS},
+        "K3_ifft_C": {"ms": ifft_ms, "GB_s": ifft_gbs, "frac_hbm": ifft_gbs / peaks["hbm_gbs"]},
+    }
+
+    # ---- end to end through the host-buffer C-ABI call ----
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        c1p = torch.empty((cfg.p, cfg.m, 2 * cfg.s), dtype=torch.float64, pin_memory=True)
+        c2p = torch.empty_like(c1p, pin_memory=True)
+
+        def e2e_step():
+            rc = L.qt_tprod_f64_host(a.t1.ctypes.data, a.t2.ctypes.data, b.t1.ctypes.data, b.t2.ctypes.data,
+                                     c1p.data_ptr(), c2p.data_ptr(), cfg.m, cfg.n, cfg.s, cfg.p, local)
+            qt._native.check(rc, "tprod_fast(host)")
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
+               "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
+               "api": "qt_tprod_f64_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        if O.ref_available():
+            threads = os.cpu_count() or 1
+            g, w, sample = time_reference(cfg, a, b, args.cpu_tile or auto_tile(cfg), threads)
+            cpu = {"value": g, "unit": "GFLOP/s", "cores": threads, "kind": "reference", "sample": sample,
+                   "wall_s": w}
+
+    if rank == 0:
+        line = {
+            "metric": "T-product throughput (effective fp64 GFLOP/s)",
+            "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
+            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
+                       "parallelism": f"rows{world}" + ("+bcastB" if world > 1 else ""),
+                       "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
+                       "flops_eff_per_step": cfg.flops_eff},
+            "roofline": roof,
+            "stages": stages,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    from paper_2212_14318_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

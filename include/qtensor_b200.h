@@ -1,0 +1,146 @@
+/*
+ * qtensor_b200.h — C-ABI of the B200-native quaternion-tensor T-product.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   qtensor::tprod_fast(a, b[, ws])      /root/reference/proj/include/qtensor/tproduct.hpp:45-46
+ *                                        /root/reference/proj/src/tproduct.cpp:75-111
+ * and for the two tube transforms it is built from
+ *   qtensor::qfft3_conj(q)               transform.hpp:56-60, transform.cpp:151-158
+ *   qtensor::qifft3_conj(qhat)           transform.hpp:62-64, transform.cpp:160-167
+ *
+ * Only plain pointers, sizes and status codes cross this boundary (no C++ or
+ * torch types).  A quaternion tensor Q = t1 + t2*j of shape m x n x p is passed
+ * as its two Cayley-Dickson planes t1, t2 (algebra.hpp:61-68), each an array of
+ * m*n*p complex doubles stored as interleaved (re, im) pairs, slice-major:
+ *     element (i, j, r) lives at complex index (r*m + i)*n + j
+ * which is exactly CdTensor3's layout (transform.hpp:35-37), so
+ * reinterpret_cast<const double*>(t.t1.data()) can be handed over unchanged.
+ *
+ * Error behaviour mirrors the reference: a shape the reference rejects with
+ * std::invalid_argument returns QT_EINVAL (p == 0, transform.cpp:152); CUDA
+ * failures return QT_ECUDA, allocation failures QT_ENOMEM, NCCL failures
+ * QT_ENCCL.  qt_last_error() returns the calling thread's last message.
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point fails with QT_ENODEV.
+ *
+ * All compute entry points are reentrant (per-call stream-ordered workspace,
+ * per-thread error state) and deterministic: identical inputs give bitwise
+ * identical outputs, independent of the number of GPUs the rows are sharded
+ * over.
+ */
+#ifndef QTENSOR_B200_H
+#define QTENSOR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QT_B200_ABI_VERSION 1
+
+enum qt_status {
+  QT_OK = 0,
+  QT_EINVAL = 1, /* reference throws std::invalid_argument            */
+  QT_ECUDA = 2,  /* CUDA runtime / launch error                       */
+  QT_ENOMEM = 3, /* device or pinned-host allocation failed            */
+  QT_ENCCL = 4,  /* NCCL unavailable or failed (multi-GPU driver)      */
+  QT_ENODEV = 5  /* no usable sm_100 device                            */
+};
+
+/* ---- library ---------------------------------------------------------- */
+
+/* ABI version (QT_B200_ABI_VERSION). */
+int qt_abi_version(void);
+
+/* Last error message of the calling thread ("" if none). */
+const char* qt_last_error(void);
+
+/* Number of CUDA kernels this library has launched in the process so far
+ * (all devices).  Used by bench.py to report gpu_launches. */
+uint64_t qt_kernel_launches(void);
+
+/* ---- device-resident entry points (all pointers are device pointers) ---
+ * stream is a cudaStream_t (NULL = legacy default stream).  Work is enqueued
+ * on the stream; the call returns without synchronising.                  */
+
+/* C = A *_T B (T-product).  A: m x n x p, B: n x s x p, C: m x s x p.
+ * Replaces tprod_fast(a, b) / tprod_fast(a, b, ws), tproduct.hpp:45-46.
+ * c1/c2 must not alias the inputs. */
+int qt_tprod_f64_device(const double* a1, const double* a2,
+                        const double* b1, const double* b2,
+                        double* c1, double* c2,
+                        uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                        void* stream);
+
+/* Forward conjugate-fused tube transform, qfft3_conj (transform.hpp:56-60):
+ *   y1 = fft_3(conj(x1)),  y2 = -fft_3(x2).  In-place (y == x) is allowed. */
+int qt_qfft3_conj_f64_device(const double* x1, const double* x2,
+                             double* y1, double* y2,
+                             uint64_t m, uint64_t n, uint64_t p, void* stream);
+
+/* Inverse, qifft3_conj (transform.hpp:62-64):
+ *   y1 = conj(ifft_3(x1)),  y2 = -ifft_3(x2).  In-place is allowed. */
+int qt_qifft3_conj_f64_device(const double* x1, const double* x2,
+                              double* y1, double* y2,
+                              uint64_t m, uint64_t n, uint64_t p, void* stream);
+
+/* Stage 2 alone (the paired-frequency quaternion block GEMM, tproduct.cpp:90-104)
+ * on already transformed operands: chat = ahat (.) bhat per frequency pair
+ * (k, p-k).  Exposed for profiling and for callers that keep operands in the
+ * transformed domain. */
+int qt_spectral_product_f64_device(const double* ahat1, const double* ahat2,
+                                   const double* bhat1, const double* bhat2,
+                                   double* chat1, double* chat2,
+                                   uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                   void* stream);
+
+/* ---- host-buffer entry points (what the C++ drop-in calls) ------------
+ * All pointers are host pointers (pageable or pinned).  The call copies to
+ * device `device`, computes, copies back and synchronises. */
+
+int qt_tprod_f64_host(const double* a1, const double* a2,
+                      const double* b1, const double* b2,
+                      double* c1, double* c2,
+                      uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device);
+
+int qt_qfft3_conj_f64_host(const double* x1, const double* x2,
+                           double* y1, double* y2,
+                           uint64_t m, uint64_t n, uint64_t p, int device);
+
+int qt_qifft3_conj_f64_host(const double* x1, const double* x2,
+                            double* y1, double* y2,
+                            uint64_t m, uint64_t n, uint64_t p, int device);
+
+/* ---- single-process multi-GPU driver -----------------------------------
+ * Host buffers in, host buffers out.  Rows of A and C are sharded in
+ * contiguous slabs of ceil(m/ndev) rows over devices[0..ndev); B is copied
+ * to devices[0] once and broadcast to the others with NCCL over NVLink.
+ * ndev == 1 runs without NCCL.  Output is bitwise identical for every ndev. */
+int qt_tprod_f64_multi(const double* a1, const double* a2,
+                       const double* b1, const double* b2,
+                       double* c1, double* c2,
+                       uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                       const int* devices, int ndev);
+
+/* ---- seeded synthetic inputs (host) -----------------------------------
+ * dist: QT_DIST_UNIFORM_SYM    all four components U[-1,1) — bitwise equal to
+ *                              the reference's gen_random_tensor (rng.cpp:21-33)
+ *       QT_DIST_NORMAL         all four components N(0, scale^2), Box-Muller
+ *                              over the same mt19937_64 top-53 uniforms
+ *       QT_DIST_PURE_UNIT      w = 0, (x, y, z) = U[0,1) (colour-video cfg4 A)
+ * t1/t2 are host arrays of 2*m*n*p doubles. */
+enum qt_dist { QT_DIST_UNIFORM_SYM = 0, QT_DIST_NORMAL = 1, QT_DIST_PURE_UNIT = 2 };
+
+int qt_gen_tensor_f64(int dist, uint64_t m, uint64_t n, uint64_t p, uint64_t seed,
+                      double scale, double* t1, double* t2);
+
+/* derive_seed(base, stream) of rng.cpp:15-19 (splitmix64 chain). */
+uint64_t qt_derive_seed(uint64_t base, uint64_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QTENSOR_B200_H */

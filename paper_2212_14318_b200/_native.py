@@ -1,0 +1,77 @@
+"""ctypes binding of the product library ``libqtensor_b200.so`` (C-ABI in
+``include/qtensor_b200.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` / ``make``.  There
+is deliberately no fallback: if the shared object is missing or cannot be
+loaded, :func:`lib` raises, and every compute call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqtensor_b200.so")
+
+QT_OK, QT_EINVAL, QT_ECUDA, QT_ENOMEM, QT_ENCCL, QT_ENODEV = 0, 1, 2, 3, 4, 5
+QT_DIST_UNIFORM_SYM, QT_DIST_NORMAL, QT_DIST_PURE_UNIT = 0, 1, 2
+
+# Every symbol include/qtensor_b200.h declares: name -> (restype, argtypes)
+_u64 = ctypes.c_uint64
+_dp = ctypes.c_void_p  # double* (host or device), passed as raw addresses
+_vp = ctypes.c_void_p
+SIGNATURES = {
+    "qt_abi_version": (ctypes.c_int, []),
+    "qt_last_error": (ctypes.c_char_p, []),
+    "qt_kernel_launches": (_u64, []),
+    "qt_tprod_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
+    "qt_qfft3_conj_f64_device": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),
+    "qt_qifft3_conj_f64_device": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),
+    "qt_spectral_product_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
+    "qt_tprod_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),
+    "qt_qfft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
+    "qt_qifft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
+    "qt_tprod_f64_multi": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
+    "qt_gen_tensor_f64": (ctypes.c_int, [ctypes.c_int] + [_u64] * 4 + [ctypes.c_double, _dp, _dp]),
+    "qt_derive_seed": (_u64, [_u64, _u64]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class QtError(RuntimeError):
+    """A non-EINVAL failure reported by the C-ABI (CUDA, NCCL, memory, device)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"qtensor_b200 error {code}: {msg}")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the product library; raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                    "there is no CPU fallback")
+            handle = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+        return _lib
+
+
+def check(rc: int, who: str) -> None:
+    """Map a C-ABI status to the reference's exception kinds."""
+    if rc == QT_OK:
+        return
+    msg = (lib().qt_last_error() or b"").decode(errors="replace")
+    if rc == QT_EINVAL:
+        raise ValueError(f"{who}: {msg}")  # std::invalid_argument in the reference
+    raise QtError(rc, f"{who}: {msg}")

@@ -1,0 +1,344 @@
+// qt_fft.cu — K1/K3: batched mode-3 tube FFT over the CD planes (sm_100a).
+//
+// Replaces transform_tubes/fft_rec (/root/reference/proj/src/transform.cpp:12-68,
+// 116-147).  The reference gathers each stride-m*n tube into a heap vector and
+// runs a recursive smallest-prime-factor DIT with per-call twiddles; here a CTA
+// owns T consecutive tubes of one CD plane, reads the p x T tile with coalesced
+// 16-byte loads (consecutive tubes are consecutive in memory), runs a
+// mixed-radix Stockham FFT in shared memory (radix-8/4/2 register butterflies,
+// generic direct-DFT stages for odd prime factors — the same O(p^2) fallback the
+// reference takes for prime lengths, transform.cpp:48) and writes the tile back
+// with the conj/negate/scale of the TubeOp fused into the store.
+//
+// Bytes per tube element: 16 B read + 16 B written per CD plane — the kernel is
+// HBM-bound (roofline of K1/K3).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "qt_internal.cuh"
+
+namespace qtb {
+
+// ------------------------------------------------------------------ planning
+FftPlan make_fft_plan(int p) {
+  FftPlan pl{};
+  pl.p = p;
+  int rest = p, ns = 0;
+  while (rest % 8 == 0 && ns < kMaxStages) { pl.radix[ns++] = 8; rest /= 8; }
+  while (rest % 4 == 0 && ns < kMaxStages) { pl.radix[ns++] = 4; rest /= 4; }
+  while (rest % 2 == 0 && ns < kMaxStages) { pl.radix[ns++] = 2; rest /= 2; }
+  for (int f = 3; rest > 1 && ns < kMaxStages;) {
+    if ((long long)f * f > rest) { pl.radix[ns++] = rest; rest = 1; break; }
+    if (rest % f == 0) { pl.radix[ns++] = f; rest /= f; }
+    else f += 2;
+  }
+  pl.nstages = ns;
+  return pl;
+}
+
+// ------------------------------------------------------------------ twiddles
+namespace {
+std::mutex g_tw_mu;
+std::map<std::pair<int, int>, double2*> g_tw;  // (device, p) -> table
+}  // namespace
+
+const double2* twiddles_for(int device, int p, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  auto key = std::make_pair(device, p);
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) return it->second;
+  // exp(-2 pi i k/p) evaluated in x87 long double (64-bit mantissa) and
+  // rounded once to double.
+  std::vector<double2> h(p);
+  const long double two_pi = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < p; ++k) {
+    long double ang = two_pi * (long double)k / (long double)p;
+    h[k].x = (double)cosl(ang);
+    h[k].y = (double)(-sinl(ang));
+  }
+  // exact values at the quarter points
+  h[0] = make_double2(1.0, 0.0);
+  if (p % 2 == 0) h[p / 2] = make_double2(-1.0, 0.0);
+  if (p % 4 == 0) { h[p / 4] = make_double2(0.0, -1.0); h[3 * p / 4] = make_double2(0.0, 1.0); }
+  double2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double2) * p) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), sizeof(double2) * p, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  (void)stream;
+  g_tw[key] = d;
+  return d;
+}
+
+// ------------------------------------------------------------- complex math
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * (-i)
+__device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+template <int R>
+__device__ __forceinline__ void dft_reg(double2 (&v)[R]);
+
+template <>
+__device__ __forceinline__ void dft_reg<2>(double2 (&v)[2]) {
+  double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+template <>
+__device__ __forceinline__ void dft_reg<4>(double2 (&v)[4]) {
+  double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+  double2 t2 = cadd(v[1], v[3]), t3 = cmul_mi(csub(v[1], v[3]));
+  v[0] = cadd(t0, t2);
+  v[2] = csub(t0, t2);
+  v[1] = cadd(t1, t3);
+  v[3] = csub(t1, t3);
+}
+
+template <>
+__device__ __forceinline__ void dft_reg<8>(double2 (&v)[8]) {
+  const double c = 0.70710678118654752440084436210484903928;  // 1/sqrt(2)
+  double2 e[4] = {v[0], v[2], v[4], v[6]};
+  double2 o[4] = {v[1], v[3], v[5], v[7]};
+  dft_reg<4>(e);
+  dft_reg<4>(o);
+  // o[k] *= W8^k
+  double2 o1 = make_double2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));
+  double2 o2 = cmul_mi(o[2]);
+  double2 o3 = make_double2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));
+  v[0] = cadd(e[0], o[0]);
+  v[4] = csub(e[0], o[0]);
+  v[1] = cadd(e[1], o1);
+  v[5] = csub(e[1], o1);
+  v[2] = cadd(e[2], o2);
+  v[6] = csub(e[2], o2);
+  v[3] = cadd(e[3], o3);
+  v[7] = csub(e[3], o3);
+}
+
+// One Stockham stage of radix R over a p x T smem tile (tube index fastest).
+// src/dst element (r, t) at [r*T + t].  Ns = product of earlier radices.
+template <int R>
+__device__ __forceinline__ void stage_reg(const double2* __restrict__ src, double2* __restrict__ dst,
+                                          const double2* __restrict__ tw, int p, int logT, int Ns) {
+  const int T = 1 << logT;
+  const int pR = p / R;
+  const int twmul = p / (Ns * R);
+  for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
+    const int j = b >> logT, t = b & (T - 1);
+    const int jm = j % Ns;
+    const int step = jm * twmul;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[((j + r * pR) << logT) + t];
+    if (step != 0) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * step]));
+    }
+    dft_reg<R>(v);
+    const int idxD = (j - jm) * R + jm;
+#pragma unroll
+    for (int k = 0; k < R; ++k) dst[((idxD + k * Ns) << logT) + t] = v[k];
+  }
+}
+
+// Generic radix-R stage: one output per thread iteration, direct R-point DFT
+// folded with the stage twiddle into one table lookup.
+__device__ __forceinline__ void stage_generic(const double2* __restrict__ src, double2* __restrict__ dst,
+                                              const double2* __restrict__ tw, int p, int logT, int Ns,
+                                              int R) {
+  const int T = 1 << logT;
+  const int pR = p / R;
+  const int twmul = p / (Ns * R);
+  for (int b = threadIdx.x; b < (p << logT); b += blockDim.x) {
+    const int o = b >> logT, t = b & (T - 1);
+    const int j = o / R, k = o - j * R;
+    const int jm = j % Ns;
+    const int base = jm * twmul + k * pR;  // < p
+    double2 acc = src[(j << logT) + t];
+    int e = 0;
+    for (int r = 1; r < R; ++r) {
+      e += base;
+      if (e >= p) e -= p;
+      const double2 x = src[((j + r * pR) << logT) + t];
+      const double2 w = __ldg(&tw[e]);
+      acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
+      acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
+    }
+    const int idxD = (j - jm) * R + jm;
+    dst[((idxD + k * Ns) << logT) + t] = acc;
+  }
+}
+
+// K1 / K3 kernel: grid (tiles, njobs), T = 1 << logT tubes per CTA.
+__global__ void __launch_bounds__(256) tube_fft_smem_kernel(TubeBatch batch, FftPlan plan,
+                                                            const double2* __restrict__ tw, int logT) {
+  extern __shared__ double2 sm[];
+  const TubeJob job = batch.job[blockIdx.y];
+  const int T = 1 << logT;
+  const uint64_t t0 = (uint64_t)blockIdx.x << logT;
+  if (t0 >= job.ntubes) return;
+  const int p = plan.p;
+  const int tcount = (int)min((uint64_t)T, job.ntubes - t0);
+  double2* src = sm;
+  double2* dst = sm + ((size_t)p << logT);
+
+  // coalesced tile load, conj fused
+  const double2* __restrict__ in = job.in + t0;
+  for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+    const int r = idx >> logT, t = idx & (T - 1);
+    double2 v = make_double2(0.0, 0.0);
+    if (t < tcount) v = __ldg(&in[(uint64_t)r * job.ntubes + t]);
+    if (job.conj_in) v.y = -v.y;
+    src[idx] = v;
+  }
+  __syncthreads();
+
+  int Ns = 1;
+  for (int s = 0; s < plan.nstages; ++s) {
+    const int R = plan.radix[s];
+    if (R == 8) stage_reg<8>(src, dst, tw, p, logT, Ns);
+    else if (R == 4) stage_reg<4>(src, dst, tw, p, logT, Ns);
+    else if (R == 2) stage_reg<2>(src, dst, tw, p, logT, Ns);
+    else stage_generic(src, dst, tw, p, logT, Ns, R);
+    __syncthreads();
+    double2* tmp = src; src = dst; dst = tmp;
+    Ns *= R;
+  }
+
+  // store with conj/scale fused
+  double2* __restrict__ out = job.out + t0;
+  const double sc = job.scale;
+  const double sci = job.conj_out ? -sc : sc;
+  for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+    const int r = idx >> logT, t = idx & (T - 1);
+    if (t < tcount) {
+      const double2 v = src[idx];
+      out[(uint64_t)r * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
+    }
+  }
+}
+
+// Large-p fallback: one Stockham stage per launch over global memory
+// (element (r, tube) at [r*ntubes + tube]).  Generic direct-DFT butterflies.
+__global__ void tube_fft_global_stage_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                                             uint64_t ntubes, int p, int Ns, int R,
+                                             const double2* __restrict__ tw, int conj_in, int conj_out,
+                                             double scale) {
+  const uint64_t total = (uint64_t)p * ntubes;
+  const int pR = p / R;
+  const int twmul = p / (Ns * R);
+  const double sci = conj_out ? -scale : scale;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < total;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t o = b / ntubes, t = b - o * ntubes;
+    const int j = (int)(o / R), k = (int)(o - (uint64_t)j * R);
+    const int jm = j % Ns;
+    const int base = jm * twmul + k * pR;
+    double2 acc = src[(uint64_t)j * ntubes + t];
+    if (conj_in) acc.y = -acc.y;
+    int e = 0;
+    for (int r = 1; r < R; ++r) {
+      e += base;
+      if (e >= p) e -= p;
+      double2 x = src[(uint64_t)(j + r * pR) * ntubes + t];
+      if (conj_in) x.y = -x.y;
+      const double2 w = __ldg(&tw[e]);
+      acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
+      acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
+    }
+    const int idxD = (j - jm) * R + jm;
+    dst[(uint64_t)(idxD + k * Ns) * ntubes + t] = make_double2(acc.x * scale, acc.y * sci);
+  }
+}
+
+// ------------------------------------------------------------------ launch
+namespace {
+constexpr int kFftThreads = 256;
+constexpr size_t kSmemBudget = 96 * 1024;   // two CTAs per SM
+constexpr size_t kSmemMax = 224 * 1024;     // one CTA per SM
+}  // namespace
+
+cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device) {
+  if (batch.njobs == 0) return cudaSuccess;
+  uint64_t maxtubes = 0;
+  for (int i = 0; i < batch.njobs; ++i) maxtubes = batch.job[i].ntubes > maxtubes ? batch.job[i].ntubes : maxtubes;
+  if (maxtubes == 0) return cudaSuccess;
+  const double2* tw = twiddles_for(device, p, stream);
+  if (!tw) return cudaErrorMemoryAllocation;
+  const FftPlan plan = make_fft_plan(p);
+
+  const size_t per_tube = 2 * sizeof(double2) * (size_t)p;  // ping-pong
+  if (per_tube <= kSmemMax) {
+    int logT = 0;
+    while (logT < 6 && (per_tube << (logT + 1)) <= kSmemBudget && (uint64_t(1) << logT) < maxtubes) ++logT;
+    // small problems: trade tile width for CTA count (keep >= 8 tubes = 128 B rows)
+    while (logT > 3 && (maxtubes >> logT) * (uint64_t)batch.njobs < 296) --logT;
+    const size_t smem = per_tube << logT;
+    {
+      static std::mutex mu;
+      static bool attr_set[64] = {};
+      std::lock_guard<std::mutex> lk(mu);
+      if (device >= 0 && device < 64 && !attr_set[device]) {
+        cudaError_t e = cudaFuncSetAttribute(tube_fft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmemMax);
+        if (e != cudaSuccess) return e;
+        attr_set[device] = true;
+      }
+    }
+    const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
+    dim3 grid((unsigned)tiles, batch.njobs);
+    tube_fft_smem_kernel<<<grid, kFftThreads, smem, stream>>>(batch, plan, tw, logT);
+    count_launches(1);
+    return cudaGetLastError();
+  }
+
+  // global multi-pass path (p > ~7000): one launch per stage per job
+  for (int i = 0; i < batch.njobs; ++i) {
+    const TubeJob& J = batch.job[i];
+    if (J.ntubes == 0) continue;
+    const size_t bytes = sizeof(double2) * (size_t)p * J.ntubes;
+    double2* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, 2 * bytes, stream);
+    if (e != cudaSuccess) return e;
+    double2* bufs[2] = {scratch, scratch + (size_t)p * J.ntubes};
+    const double2* src = J.in;
+    int Ns = 1;
+    for (int s = 0; s < plan.nstages; ++s) {
+      const bool first = s == 0, last = s == plan.nstages - 1;
+      // a single in-place stage must not write the buffer it is reading
+      const bool bounce = last && first && J.in == J.out;
+      double2* dst = (last && !bounce) ? J.out : bufs[s & 1];
+      const uint64_t total = (uint64_t)p * J.ntubes;
+      const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+      tube_fft_global_stage_kernel<<<blocks, 256, 0, stream>>>(src, dst, J.ntubes, p, Ns, plan.radix[s], tw,
+                                                               first ? J.conj_in : 0, last ? J.conj_out : 0,
+                                                               last ? J.scale : 1.0);
+      count_launches(1);
+      if (bounce) {
+        cudaError_t ce = cudaMemcpyAsync(J.out, dst, bytes, cudaMemcpyDeviceToDevice, stream);
+        if (ce != cudaSuccess) return ce;
+      }
+      src = dst;
+      Ns *= plan.radix[s];
+    }
+    if (plan.nstages == 0) {  // p == 1 cannot reach here; kept for completeness
+      cudaFreeAsync(scratch, stream);
+      continue;
+    }
+    e = cudaFreeAsync(scratch, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace qtb

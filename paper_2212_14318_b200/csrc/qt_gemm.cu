@@ -1,0 +1,296 @@
+// qt_gemm.cu — K2: paired-frequency quaternion block GEMM on FP64 DMMA (sm_100a).
+//
+// Replaces the slice loop of tprod_fast (/root/reference/proj/src/tproduct.cpp:90-104),
+// which for every frequency i (ri = slice_reflect(i, p) = (p - i) % p) runs
+//     C1_i = Â1_i·B̂1_i − conj(Â2_ri)·B̂2_i
+//     C2_i = conj(Â1_ri)·B̂2_i + Â2_i·B̂1_i
+// as four i-k-j complex MAC loops (slice_gemm_acc, tproduct.cpp:57-71).
+//
+// Here one CTA owns a BM x BN tile of the output for the frequency PAIR
+// (k, σk), σk = (p - k) % p.  The four Â slices Â1_k, Â2_k, Â1_σk, Â2_σk are
+// staged once per K-step and feed both frequencies:
+//     C1_k  = Â1_k ·B̂1_k  − conj(Â2_σk)·B̂2_k      C2_k  = conj(Â1_σk)·B̂2_k  + Â2_k ·B̂1_k
+//     C1_σk = Â1_σk·B̂1_σk − conj(Â2_k) ·B̂2_σk     C2_σk = conj(Â1_k) ·B̂2_σk + Â2_σk·B̂1_σk
+// Self-paired frequencies (k = 0 and k = p/2 for even p) run the SELF variant
+// that computes one frequency.  Each complex product is four real products
+// issued as `mma.sync.m8n8k4.f64` (SASS DMMA.8x8x4, the FP64 tensor pipe —
+// tcgen05 has no f64 kind); conjugation and the minus signs are sign-bit XORs
+// on the B fragments (ALU pipe), so the FP64 pipe only ever sees DMMA.
+//
+// Determinism: no split-K, no atomics; each accumulator adds its four terms in
+// a fixed order for K-steps 0..n-1, independent of the M/N tiling, so results
+// are bitwise reproducible and identical across row shardings.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "qt_internal.cuh"
+
+namespace qtb {
+
+namespace {
+
+constexpr int BM = 64;       // rows of C per CTA
+constexpr int BN = 16;       // columns of C per CTA
+constexpr int BK = 8;        // complex K per pipeline stage
+constexpr int STAGES = 2;    // cp.async ring depth
+constexpr int NTHREADS = 256;  // 8 warps: 4 (M) x 2 (N), warp tile 16 x 8
+
+// smem tile geometry (double2 units); XOR swizzles make every fragment load a
+// conflict-free LDS.128 without padding:
+//   A plane: [BM][BK], element (i, c) at i*BK + (c ^ ((i & 1) << 2))
+//   B plane: [BK][BN], element (k, j) at k*BN + (j ^ ((k & 3) << 1))
+constexpr int A_PLANE = BM * BK;
+constexpr int B_PLANE = BK * BN;
+constexpr int STAGE_ELEMS = 4 * A_PLANE + 4 * B_PLANE;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;  // zero-fill out-of-range chunks
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ double dneg(double x) {
+  // sign flip on the integer pipe (keeps the FP64 pipe for DMMA only)
+  long long b = __double_as_longlong(x) ^ (long long)0x8000000000000000ULL;
+  return __longlong_as_double(b);
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct PairArgs {
+  const double2* a[4];  // Â1_k, Â2_k, Â1_σ, Â2_σ   (m x n each)
+  const double2* b[4];  // B̂1_k, B̂2_k, B̂1_σ, B̂2_σ   (n x s each)
+  double2* c[4];        // Ĉ1_k, Ĉ2_k, Ĉ1_σ, Ĉ2_σ   (m x s each)
+};
+
+template <bool SELF>
+__device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int kt, int row0, int col0, int m,
+                                           int n, int s) {
+  constexpr int NP = SELF ? 2 : 4;
+  const int tid = threadIdx.x;
+  const int k0 = kt * BK;
+  // A: NP planes x BM rows x BK chunks (plane index static -> no local-memory indexing)
+#pragma unroll
+  for (int pl = 0; pl < NP; ++pl) {
+#pragma unroll
+    for (int it = 0; it < A_PLANE / NTHREADS; ++it) {
+      const int id = tid + it * NTHREADS;
+      const int c = id & (BK - 1);
+      const int i = id / BK;
+      const int gr = row0 + i, gc = k0 + c;
+      const bool ok = gr < m && gc < n;
+      const double2* src = P.a[pl] + (ok ? (size_t)gr * n + gc : 0);
+      double2* dst = st + pl * A_PLANE + i * BK + (c ^ ((i & 1) << 2));
+      cp_async16(smem_u32(dst), src, ok);
+    }
+  }
+  // B: NP planes x BK rows x BN chunks; two planes per pass of 256 threads
+  static_assert(2 * B_PLANE == NTHREADS, "B tile mapping assumes 2 planes per pass");
+  double2* sb = st + 4 * A_PLANE;
+#pragma unroll
+  for (int it = 0; it < NP / 2; ++it) {
+    const int hi = tid >= B_PLANE;
+    const int id = tid - hi * B_PLANE;
+    const int j = id & (BN - 1);
+    const int k = id / BN;
+    const int gk = k0 + k, gj = col0 + j;
+    const bool ok = gk < n && gj < s;
+    const double2* plane = hi ? P.b[2 * it + 1] : P.b[2 * it];
+    const double2* src = plane + (ok ? (size_t)gk * s + gj : 0);
+    double2* dst = sb + (2 * it + hi) * B_PLANE + k * BN + (j ^ ((k & 3) << 1));
+    cp_async16(smem_u32(dst), src, ok);
+  }
+}
+
+template <bool SELF>
+__device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0, int m, int n, int s) {
+  extern __shared__ double2 smem[];
+  constexpr int NC = SELF ? 4 : 8;  // accumulated real components
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;
+
+  double acc[NC][2][2];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) acc[c][rb][0] = acc[c][rb][1] = 0.0;
+
+  const int ktiles = (n + BK - 1) / BK;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < ktiles) load_stage<SELF>(smem + st * STAGE_ELEMS, P, st, row0, col0, m, n, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) load_stage<SELF>(smem + (nk % STAGES) * STAGE_ELEMS, P, nk, row0, col0, m, n, s);
+      cp_async_commit();
+    }
+    const double2* sa = smem + (kt % STAGES) * STAGE_ELEMS;
+    const double2* sb = sa + 4 * A_PLANE;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      // B fragments: element (k = ks*4 + q, j = wn*8 + g); swizzle j ^ (q << 1)
+      const int kb = ks * 4 + q;
+      const int jb = (wn * 8 + g) ^ (q << 1);
+      double br[4], bi[4];
+#pragma unroll
+      for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
+        const double2 v = sb[pl * B_PLANE + kb * BN + jb];
+        br[pl] = v.x;
+        bi[pl] = v.y;
+      }
+      const double nb1k_i = dneg(bi[0]);
+      const double nb2k_r = dneg(br[1]);
+      const double nb2k_i = dneg(bi[1]);
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        const int i = wm * 16 + rb * 8 + g;
+        const int ca = (ks * 4 + q) ^ ((i & 1) << 2);
+        double ar[4], ai[4];
+#pragma unroll
+        for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
+          const double2 v = sa[pl * A_PLANE + i * BK + ca];
+          ar[pl] = v.x;
+          ai[pl] = v.y;
+        }
+        if (SELF) {
+          // A1s = A1k, A2s = A2k
+          ar[2] = ar[0]; ai[2] = ai[0]; ar[3] = ar[1]; ai[3] = ai[1];
+        }
+        // C1_k
+        dmma(acc[0][rb], ar[0], br[0]);
+        dmma(acc[0][rb], ai[0], nb1k_i);
+        dmma(acc[0][rb], ar[3], nb2k_r);
+        dmma(acc[0][rb], ai[3], nb2k_i);
+        dmma(acc[1][rb], ar[0], bi[0]);
+        dmma(acc[1][rb], ai[0], br[0]);
+        dmma(acc[1][rb], ar[3], nb2k_i);
+        dmma(acc[1][rb], ai[3], br[1]);
+        // C2_k
+        dmma(acc[2][rb], ar[2], br[1]);
+        dmma(acc[2][rb], ai[2], bi[1]);
+        dmma(acc[2][rb], ar[1], br[0]);
+        dmma(acc[2][rb], ai[1], nb1k_i);
+        dmma(acc[3][rb], ar[2], bi[1]);
+        dmma(acc[3][rb], ai[2], nb2k_r);
+        dmma(acc[3][rb], ar[1], bi[0]);
+        dmma(acc[3][rb], ai[1], br[0]);
+        if (!SELF) {
+          const double nb1s_i = dneg(bi[2]);
+          const double nb2s_r = dneg(br[3]);
+          const double nb2s_i = dneg(bi[3]);
+          // C1_σ
+          dmma(acc[4 % NC][rb], ar[2], br[2]);
+          dmma(acc[4 % NC][rb], ai[2], nb1s_i);
+          dmma(acc[4 % NC][rb], ar[1], nb2s_r);
+          dmma(acc[4 % NC][rb], ai[1], nb2s_i);
+          dmma(acc[5 % NC][rb], ar[2], bi[2]);
+          dmma(acc[5 % NC][rb], ai[2], br[2]);
+          dmma(acc[5 % NC][rb], ar[1], nb2s_i);
+          dmma(acc[5 % NC][rb], ai[1], br[3]);
+          // C2_σ
+          dmma(acc[6 % NC][rb], ar[0], br[3]);
+          dmma(acc[6 % NC][rb], ai[0], bi[3]);
+          dmma(acc[6 % NC][rb], ar[3], br[2]);
+          dmma(acc[6 % NC][rb], ai[3], nb1s_i);
+          dmma(acc[7 % NC][rb], ar[0], bi[3]);
+          dmma(acc[7 % NC][rb], ai[0], nb2s_r);
+          dmma(acc[7 % NC][rb], ar[3], bi[2]);
+          dmma(acc[7 % NC][rb], ai[3], br[2]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: (re, im) pairs of C[row][col], col = 2q, 2q+1 of the 8-wide block
+  const int col = col0 + wn * 8 + 2 * q;
+#pragma unroll
+  for (int f = 0; f < (SELF ? 1 : 2); ++f) {
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      double2* C = P.c[f * 2 + part];
+      const int cr = f * 4 + part * 2;
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        const int row = row0 + wm * 16 + rb * 8 + g;
+        if (row < m) {
+          double2* dst = C + (size_t)row * s + col;
+          if (col < s) dst[0] = make_double2(acc[cr % NC][rb][0], acc[(cr + 1) % NC][rb][0]);
+          if (col + 1 < s) dst[1] = make_double2(acc[cr % NC][rb][1], acc[(cr + 1) % NC][rb][1]);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 2)
+    paired_spectral_gemm_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
+                                const double2* __restrict__ bh1, const double2* __restrict__ bh2,
+                                double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s,
+                                int p) {
+  const int k = blockIdx.z;
+  const int sg = (p - k) % p;
+  const size_t amn = (size_t)m * n, bns = (size_t)n * s, cms = (size_t)m * s;
+  PairArgs P;
+  P.a[0] = ah1 + k * amn;
+  P.a[1] = ah2 + k * amn;
+  P.a[2] = ah1 + sg * amn;
+  P.a[3] = ah2 + sg * amn;
+  P.b[0] = bh1 + k * bns;
+  P.b[1] = bh2 + k * bns;
+  P.b[2] = bh1 + sg * bns;
+  P.b[3] = bh2 + sg * bns;
+  P.c[0] = ch1 + k * cms;
+  P.c[1] = ch2 + k * cms;
+  P.c[2] = ch1 + sg * cms;
+  P.c[3] = ch2 + sg * cms;
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  if (sg == k) pair_tile<true>(P, row0, col0, m, n, s);
+  else pair_tile<false>(P, row0, col0, m, n, s);
+}
+
+}  // namespace
+
+cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                 double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                 cudaStream_t stream) {
+  if (m == 0 || s == 0 || p == 0) return cudaSuccess;
+  {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+      attr_err = cudaFuncSetAttribute(paired_spectral_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)SMEM_BYTES);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+  }
+  const uint64_t npairs = p / 2 + 1;
+  dim3 grid((unsigned)((s + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)npairs);
+  if (grid.y > 65535u || grid.z > 65535u) return cudaErrorInvalidConfiguration;
+  paired_spectral_gemm_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m,
+                                                                      (int)n, (int)s, (int)p);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace qtb

@@ -1,0 +1,70 @@
+// qt_internal.cuh — shared declarations of the sm_100a T-product kernels.
+//
+// Data layout in HBM: every quaternion tensor is two
+// Cayley-Dickson planes (t1, t2), each m*n*p double2 (re, im), slice-major:
+// element (i, j, r) at (r*m + i)*n + j.  A "tube" (i, j) is the stride-m*n
+// sequence over r.  The transformed operands Â, B̂, Ĉ use the same layout, so
+// per frequency k the slice k of each plane is a dense row-major matrix — the
+// GEMM-friendly form the paired-frequency kernel reads.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qtb {
+
+// ---------------------------------------------------------------- tube FFT
+// One "job" = one CD plane of one tensor.  The transform applied per tube is
+//   y = scale * conj_out?( F( conj_in?(x) ) ),   F = unnormalised forward DFT
+// which covers the four TubeOps of transform.cpp:116-147:
+//   ConjInForward   (t1 of qfft3_conj)  : conj_in=1, conj_out=0, scale=+1
+//   NegateForward   (t2 of qfft3_conj)  : conj_in=0, conj_out=0, scale=-1
+//   InverseConjOut  (t1 of qifft3_conj) : conj_in=1, conj_out=0, scale=+1/p
+//   NegateInverse   (t2 of qifft3_conj) : conj_in=1, conj_out=1, scale=-1/p
+// (conj(ifft(x)) = F(conj x)/p and -ifft(x) = -conj(F(conj x))/p.)
+struct TubeJob {
+  const double2* in;
+  double2* out;
+  uint64_t ntubes;  // m*n of the tensor (tubes per plane)
+  int conj_in;
+  int conj_out;
+  double scale;
+};
+
+constexpr int kMaxJobs = 4;
+constexpr int kMaxStages = 40;
+
+struct TubeBatch {
+  TubeJob job[kMaxJobs];
+  int njobs;
+};
+
+struct FftPlan {
+  int p;
+  int nstages;
+  int radix[kMaxStages];
+};
+
+// Radix schedule for length p (8s first, then 4, 2, then odd primes).
+FftPlan make_fft_plan(int p);
+
+// Device twiddle table W_p[k] = exp(-2 pi i k / p), k in [0, p), cached per
+// (device, p).  Returns nullptr on failure (error recorded).
+const double2* twiddles_for(int device, int p, cudaStream_t stream);
+
+// Enqueue the tube transform of every job in `batch` (all jobs share p).
+// Returns cudaSuccess or the launch error.
+cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device);
+
+// ------------------------------------------------------ paired spectral GEMM
+// chat[k] for all k from ahat, bhat (slice-major CD planes), tproduct.cpp:90-104.
+cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2,
+                                 const double2* bh1, const double2* bh2,
+                                 double2* ch1, double2* ch2,
+                                 uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                 cudaStream_t stream);
+
+// Launch accounting (qt_kernel_launches).
+void count_launches(uint64_t k);
+
+}  // namespace qtb

@@ -1,0 +1,44 @@
+"""Row sharding of the T-product over ranks (one process per GPU).
+
+Row i of C = A *_T B depends only on row i of A and all of B (every slice
+product and every tube transform is row-local), so the rows of A
+and C are split into contiguous slabs of ceil(m / world) rows and B is
+replicated by ONE broadcast from rank 0 — the only exchange on the path.  The
+slab computation is the single-GPU pipeline unchanged, so the stitched result
+is bitwise identical to the one-GPU result for every world size.
+
+The same slab rule is used by the C++ single-process driver
+(qt_tprod_f64_multi, csrc/qt_multi.cu).
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+
+def row_slab(m: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) rows of rank `rank`: contiguous slabs of ceil(m/world) rows."""
+    slab = -(-m // world)
+    lo = min(m, rank * slab)
+    hi = min(m, lo + slab)
+    return lo, hi
+
+
+def take_rows(t1: np.ndarray, t2: np.ndarray, lo: int, hi: int):
+    """Rows [lo, hi) of a slice-major (p, m, n) tensor, as a contiguous slab."""
+    return np.ascontiguousarray(t1[:, lo:hi, :]), np.ascontiguousarray(t2[:, lo:hi, :])
+
+
+def sharded_tprod(a_slab, b, compute: Callable, broadcast: Callable, rank: int):
+    """One rank's share of the row-sharded T-product.
+
+    a_slab    : this rank's rows of A (already resident on the rank)
+    b         : B on rank 0 (a preallocated receive buffer elsewhere)
+    broadcast : broadcast(buffers, src=0) over the process group (NCCL on
+                GPUs; gloo in the CPU tests)
+    compute   : compute(a_slab, b) -> C slab (the GPU pipeline, or the oracle
+                in the CPU tests)
+    """
+    broadcast(b, 0)
+    return compute(a_slab, b)

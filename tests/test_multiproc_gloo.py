@@ -1,0 +1,79 @@
+"""CPU, world_size 2 over gloo: the N>1 host path of bench.py / shard.py.
+
+Each rank holds its row slab of A, rank 0 broadcasts B, each rank computes its
+C slab (the oracle stands in for the GPU pipeline on CPU), rank 0 gathers and
+the stitched C must equal the single-process result bitwise."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, m, n, s, p, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2212_14318_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = O.gen_random_tensor(m, n, p, 11)          # every rank can regenerate A; it keeps only its slab
+    lo, hi = shard.row_slab(m, world, rank)
+    a_slab = shard.take_rows(a[0], a[1], lo, hi)
+    if rank == 0:
+        b = O.gen_random_tensor(n, s, p, 12)
+    else:
+        b = (np.zeros((p, n, s), np.complex128), np.zeros((p, n, s), np.complex128))
+    bt = [torch.from_numpy(b[0].view(np.float64)), torch.from_numpy(b[1].view(np.float64))]
+
+    def broadcast(_b, src):
+        for t in bt:
+            dist.broadcast(t, src=src)
+
+    c = shard.sharded_tprod(a_slab, b, lambda x, y: O.tprod_fast(x, y), broadcast, rank)
+    # gather slabs (padded to the max slab size) on rank 0
+    slab = -(-m // world)
+    buf = np.zeros((2, p, slab, s), np.complex128)
+    buf[0, :, :hi - lo] = c[0]
+    buf[1, :, :hi - lo] = c[1]
+    t = torch.from_numpy(buf.view(np.float64))
+    gathered = [torch.zeros_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, gathered, dst=0)
+    if rank == 0:
+        c1 = np.zeros((p, m, s), np.complex128)
+        c2 = np.zeros((p, m, s), np.complex128)
+        for r, g in enumerate(gathered):
+            lo_r, hi_r = shard.row_slab(m, world, r)
+            gg = g.numpy().view(np.complex128)
+            c1[:, lo_r:hi_r] = gg[0, :, :hi_r - lo_r]
+            c2[:, lo_r:hi_r] = gg[1, :, :hi_r - lo_r]
+        np.savez(out_path, c1=c1, c2=c2)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,s,p", [(9, 5, 6, 8), (4, 3, 5, 7), (1, 2, 3, 4)])
+def test_row_sharded_world2_equals_single(tmp_path, m, n, s, p):
+    import oracle as O
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_worker, args=(2, _free_port(), m, n, s, p, out), nprocs=2, join=True)
+    got = np.load(out)
+    a = O.gen_random_tensor(m, n, p, 11)
+    b = O.gen_random_tensor(n, s, p, 12)
+    want = O.tprod_fast(a, b)
+    assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
+    assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
