@@ -9,10 +9,12 @@
 //   K3  inverse tube FFT of Ĉ in place in C (2 jobs)        -> C
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/qtensor_b200.h"
@@ -50,6 +52,20 @@ int current_device(int* dev) {
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, *dev);
   if (major != 10 || minor != 0)
     return fail(QT_ENODEV, "device %d is sm_%d%d; this library is built for sm_100a only", *dev, major, minor);
+  // Keep freed workspace in the device's stream-ordered pool across syncs: the
+  // default release threshold (0) would unmap it at every synchronize and make
+  // the next call pay for fresh page mappings.
+  static std::mutex mu;
+  static bool pool_set[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (*dev >= 0 && *dev < 64 && !pool_set[*dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, *dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set[*dev] = true;
+  }
   return QT_OK;
 }
 
@@ -159,6 +175,9 @@ struct HostCall {
     cudaError_t e = cudaGetDevice(&prev);
     if (e != cudaSuccess) { prev = -1; return cuda_fail(e, "cudaGetDevice"); }
     if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    int dev = 0;
+    int rc = current_device(&dev);
+    if (rc) return rc;
     if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
     return QT_OK;
   }
@@ -221,6 +240,97 @@ int qt_spectral_product_f64_device(const double* ah1, const double* ah2, const d
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "K2 paired spectral GEMM");
 }
 
+// Row-slab pipelined host path.  Row i of C depends only on row i of A, so A
+// and C stream through the GPU in slabs of R rows while B is uploaded and
+// transformed once: two slab streams alternate so that the H2D copy of slab
+// j+1 and the D2H copy of slab j-1 (separate copy engines) overlap the
+// K1 -> K2 -> K3 compute of slab j.  Output is bitwise identical to the
+// one-shot path (same kernels, same per-row arithmetic).
+static int tprod_host_pipelined(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
+                                double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t R,
+                                HostCall& hc) {
+  const size_t cx = sizeof(double2);
+  const size_t bb = n * s * p * cx, slab_a = R * n * p * cx, slab_c = R * s * p * cx;
+  cudaError_t e;
+  int dev = 0;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t ss[2] = {nullptr, nullptr};
+  cudaEvent_t evB = nullptr;
+  char* d = nullptr;
+  const size_t total = 4 * bb + 2 * (4 * slab_a + 2 * slab_c) + 256;
+  auto cleanup = [&](int code) {
+    for (auto& x : ss)
+      if (x) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+    if (d) cudaFreeAsync(d, hc.st);
+    if (evB) cudaEventDestroy(evB);
+    cudaError_t se = cudaStreamSynchronize(hc.st);
+    if (!code && se != cudaSuccess) return cuda_fail(se, "tprod_fast (host) sync");
+    return code;
+  };
+  for (auto& x : ss)
+    if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return cleanup(cuda_fail(e, "stream"));
+  if ((e = cudaEventCreateWithFlags(&evB, cudaEventDisableTiming)) != cudaSuccess) return cleanup(cuda_fail(e, "event"));
+  if ((e = cudaMallocAsync((void**)&d, total, hc.st)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMallocAsync(host call)"));
+  double* dB1 = (double*)d;
+  double* dB2 = (double*)(d + bb);
+  double* dBh1 = (double*)(d + 2 * bb);
+  double* dBh2 = (double*)(d + 3 * bb);
+  char* slabs = d + 4 * bb;
+  // B: upload + K1(B) once on the call stream
+  if ((rc = h2d(dB1, b1, bb, hc.st)) || (rc = h2d(dB2, b2, bb, hc.st))) return cleanup(rc);
+  {
+    TubeBatch fb{};
+    add_forward(fb, dB1, dB2, dBh1, dBh2, n * s);
+    if ((e = launch_tube_fft(fb, (int)p, hc.st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (B)"));
+  }
+  if ((e = cudaEventRecord(evB, hc.st)) != cudaSuccess) return cleanup(cuda_fail(e, "event"));
+  for (auto& x : ss)
+    if ((e = cudaStreamWaitEvent(x, evB, 0)) != cudaSuccess) return cleanup(cuda_fail(e, "wait"));
+
+  for (uint64_t r0 = 0, j = 0; r0 < m; r0 += R, ++j) {
+    const uint64_t rows = std::min<uint64_t>(R, m - r0);
+    cudaStream_t st = ss[j & 1];
+    char* base = slabs + (j & 1) * (4 * slab_a + 2 * slab_c);
+    double* dA1 = (double*)base;
+    double* dA2 = (double*)(base + slab_a);
+    double* dAh1 = (double*)(base + 2 * slab_a);
+    double* dAh2 = (double*)(base + 3 * slab_a);
+    double* dC1 = (double*)(base + 4 * slab_a);
+    double* dC2 = (double*)(base + 4 * slab_a + slab_c);
+    // slab of A = p strided chunks of rows x n complex (slice-major)
+    const size_t apitch = m * n * cx, awidth = rows * n * cx;
+    if ((e = cudaMemcpy2DAsync(dA1, awidth, a1 + 2 * r0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpy2DAsync(dA2, awidth, a2 + 2 * r0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, st)))
+      return cleanup(cuda_fail(e, "H2D A slab"));
+    TubeBatch fa{};
+    add_forward(fa, dA1, dA2, dAh1, dAh2, rows * n);
+    if ((e = launch_tube_fft(fa, (int)p, st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (A)"));
+    if ((e = launch_spectral_gemm((const double2*)dAh1, (const double2*)dAh2, (const double2*)dBh1,
+                                  (const double2*)dBh2, (double2*)dC1, (double2*)dC2, rows, n, s, p, st)) !=
+        cudaSuccess)
+      return cleanup(cuda_fail(e, "K2 paired spectral GEMM"));
+    TubeBatch ic{};
+    add_inverse(ic, dC1, dC2, dC1, dC2, rows * s, p);
+    if ((e = launch_tube_fft(ic, (int)p, st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K3 inverse tube FFT"));
+    const size_t cpitch = m * s * cx, cwidth = rows * s * cx;
+    if ((e = cudaMemcpy2DAsync(c1 + 2 * r0 * s, cpitch, dC1, cwidth, cwidth, p, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpy2DAsync(c2 + 2 * r0 * s, cpitch, dC2, cwidth, cwidth, p, cudaMemcpyDeviceToHost, st)))
+      return cleanup(cuda_fail(e, "D2H C slab"));
+  }
+  // the call stream frees the buffers only after both slab streams are done
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2; ++k) {
+    cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+    cudaEventRecord(done[k], ss[k]);
+    cudaStreamWaitEvent(hc.st, done[k], 0);
+  }
+  rc = cleanup(QT_OK);
+  for (auto& ev : done) cudaEventDestroy(ev);
+  return rc;
+}
+
 int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                       double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device) {
   t_err.clear();
@@ -229,6 +339,14 @@ int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, cons
   HostCall hc;
   if ((rc = hc.begin(device))) return rc;
   const size_t ab = m * n * p * sizeof(double2), bb = n * s * p * sizeof(double2), cb = m * s * p * sizeof(double2);
+  // Large problems stream row slabs (>= 4 slabs of >= 64 rows, <= ~256 MB of A each).
+  if (n > 0 && s > 0 && m >= 256 && ab + cb >= (64ull << 20)) {
+    uint64_t R = std::max<uint64_t>(64, (m + 7) / 8);
+    const uint64_t row_bytes = n * p * sizeof(double2) * 2;
+    while (R > 64 && R * row_bytes > (256ull << 20)) R = (R + 1) / 2;
+    R = (R + 63) / 64 * 64;
+    return tprod_host_pipelined(a1, a2, b1, b2, c1, c2, m, n, s, p, R, hc);
+  }
   double* d = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d, 2 * (ab + bb + cb) + 64, hc.st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host call)");

@@ -179,53 +179,193 @@ __device__ __forceinline__ void stage_generic(const double2* __restrict__ src, d
   }
 }
 
-// K1 / K3 kernel: grid (tiles, njobs), T = 1 << logT tubes per CTA.
-__global__ void __launch_bounds__(256) tube_fft_smem_kernel(TubeBatch batch, FftPlan plan,
-                                                            const double2* __restrict__ tw, int logT) {
+// ---------------------------------------------------------------------------
+// K1 / K3 kernel.  grid = (tiles, njobs); a CTA owns T = 1 << logT consecutive
+// tubes of one CD plane.  Stage 0 (radix 2/4/8) reads its butterfly inputs
+// straight from HBM (R independent 16-byte loads per thread, consecutive
+// threads on consecutive tubes -> T*16-byte coalesced rows) with the conj-in
+// fused; middle stages ping-pong in shared memory; the last stage (radix
+// 2/4/8) writes straight to HBM with the conj-out/scale fused.  A 64-point
+// tube is therefore one HBM read, one shared-memory round trip and one HBM
+// write.  Generic (odd prime) first/last stages fall back to an explicit
+// shared-memory tile load / store.
+__device__ __forceinline__ bool is_reg_radix(int R) { return R == 2 || R == 4 || R == 8; }
+
+template <int R>
+__device__ __forceinline__ void twiddle_dft(double2 (&v)[R], const double2* __restrict__ tw, int step) {
+  if (step != 0) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * step]));
+  }
+  dft_reg<R>(v);
+}
+
+// stage 0: HBM -> registers -> smem (Ns = 1, so no twiddles)
+template <int R>
+__device__ __forceinline__ void stage_first_global(const TubeJob& job, uint64_t t0, int tcount, double2* __restrict__ dst,
+                                                   int p, int logT) {
+  const int T = 1 << logT;
+  const int pR = p / R;
+  const double2* __restrict__ in = job.in + t0;
+  for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
+    const int j = b >> logT, t = b & (T - 1);
+    double2 v[R];
+    const bool ok = t < tcount;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v[r] = ok ? __ldg(&in[(uint64_t)(j + r * pR) * job.ntubes + t]) : make_double2(0.0, 0.0);
+      if (job.conj_in) v[r].y = -v[r].y;
+    }
+    dft_reg<R>(v);
+    // Ns = 1: idxD = j*R, outputs at j*R + k
+#pragma unroll
+    for (int k = 0; k < R; ++k) dst[((j * R + k) << logT) + t] = v[k];
+  }
+}
+
+// last stage: smem -> registers -> HBM with conj-out/scale fused
+template <int R>
+__device__ __forceinline__ void stage_last_global(const double2* __restrict__ src, const TubeJob& job, uint64_t t0,
+                                                  int tcount, const double2* __restrict__ tw, int p, int logT,
+                                                  int Ns) {
+  const int T = 1 << logT;
+  const int pR = p / R;
+  const int twmul = p / (Ns * R);
+  double2* __restrict__ out = job.out + t0;
+  const double sc = job.scale;
+  const double sci = job.conj_out ? -sc : sc;
+  for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
+    const int j = b >> logT, t = b & (T - 1);
+    const int jm = j % Ns;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[((j + r * pR) << logT) + t];
+    twiddle_dft<R>(v, tw, jm * twmul);
+    if (t < tcount) {
+      const int idxD = (j - jm) * R + jm;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        out[(uint64_t)(idxD + k * Ns) * job.ntubes + t] = make_double2(v[k].x * sc, v[k].y * sci);
+    }
+  }
+}
+
+// single-stage tube (p in {2, 4, 8}): HBM -> registers -> HBM
+template <int R>
+__device__ __forceinline__ void stage_only_global(const TubeJob& job, uint64_t t0, int tcount, int logT) {
+  const int T = 1 << logT;
+  const double2* __restrict__ in = job.in + t0;
+  double2* __restrict__ out = job.out + t0;
+  const double sc = job.scale;
+  const double sci = job.conj_out ? -sc : sc;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    if (t >= tcount) continue;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v[r] = __ldg(&in[(uint64_t)r * job.ntubes + t]);
+      if (job.conj_in) v[r].y = -v[r].y;
+    }
+    dft_reg<R>(v);
+#pragma unroll
+    for (int k = 0; k < R; ++k) out[(uint64_t)k * job.ntubes + t] = make_double2(v[k].x * sc, v[k].y * sci);
+  }
+}
+
+__device__ __forceinline__ void stage_smem(const double2* src, double2* dst, const double2* __restrict__ tw, int p,
+                                           int logT, int Ns, int R) {
+  if (R == 8) stage_reg<8>(src, dst, tw, p, logT, Ns);
+  else if (R == 4) stage_reg<4>(src, dst, tw, p, logT, Ns);
+  else if (R == 2) stage_reg<2>(src, dst, tw, p, logT, Ns);
+  else stage_generic(src, dst, tw, p, logT, Ns, R);
+}
+
+__global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan plan, const double2* __restrict__ tw,
+                                                       int logT) {
   extern __shared__ double2 sm[];
   const TubeJob job = batch.job[blockIdx.y];
   const int T = 1 << logT;
   const uint64_t t0 = (uint64_t)blockIdx.x << logT;
   if (t0 >= job.ntubes) return;
   const int p = plan.p;
+  const int S = plan.nstages;
   const int tcount = (int)min((uint64_t)T, job.ntubes - t0);
-  double2* src = sm;
-  double2* dst = sm + ((size_t)p << logT);
 
-  // coalesced tile load, conj fused
-  const double2* __restrict__ in = job.in + t0;
-  for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
-    const int r = idx >> logT, t = idx & (T - 1);
-    double2 v = make_double2(0.0, 0.0);
-    if (t < tcount) v = __ldg(&in[(uint64_t)r * job.ntubes + t]);
-    if (job.conj_in) v.y = -v.y;
-    src[idx] = v;
+  if (S == 0) {  // p == 1: the transform is the identity, ops only
+    const double sc = job.scale, sci = job.conj_out ? -sc : sc;
+    for (int t = threadIdx.x; t < tcount; t += blockDim.x) {
+      double2 v = __ldg(&job.in[t0 + t]);
+      if (job.conj_in) v.y = -v.y;
+      job.out[t0 + t] = make_double2(v.x * sc, v.y * sci);
+    }
+    return;
   }
-  __syncthreads();
-
-  int Ns = 1;
-  for (int s = 0; s < plan.nstages; ++s) {
-    const int R = plan.radix[s];
-    if (R == 8) stage_reg<8>(src, dst, tw, p, logT, Ns);
-    else if (R == 4) stage_reg<4>(src, dst, tw, p, logT, Ns);
-    else if (R == 2) stage_reg<2>(src, dst, tw, p, logT, Ns);
-    else stage_generic(src, dst, tw, p, logT, Ns, R);
-    __syncthreads();
-    double2* tmp = src; src = dst; dst = tmp;
-    Ns *= R;
+  const int R0 = plan.radix[0];
+  if (S == 1 && is_reg_radix(R0)) {
+    if (R0 == 8) stage_only_global<8>(job, t0, tcount, logT);
+    else if (R0 == 4) stage_only_global<4>(job, t0, tcount, logT);
+    else stage_only_global<2>(job, t0, tcount, logT);
+    return;
   }
 
-  // store with conj/scale fused
-  double2* __restrict__ out = job.out + t0;
-  const double sc = job.scale;
-  const double sci = job.conj_out ? -sc : sc;
-  for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
-    const int r = idx >> logT, t = idx & (T - 1);
-    if (t < tcount) {
-      const double2 v = src[idx];
-      out[(uint64_t)r * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
+  double2* cbuf = sm;                          // holds the current data
+  double2* obuf = sm + ((size_t)p << logT);    // other ping-pong buffer
+  int s = 0, Ns = 1;
+  if (is_reg_radix(R0)) {
+    if (R0 == 8) stage_first_global<8>(job, t0, tcount, cbuf, p, logT);
+    else if (R0 == 4) stage_first_global<4>(job, t0, tcount, cbuf, p, logT);
+    else stage_first_global<2>(job, t0, tcount, cbuf, p, logT);
+    s = 1;
+    Ns = R0;
+  } else {  // explicit coalesced tile load, conj fused
+    const double2* __restrict__ in = job.in + t0;
+    for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+      const int r = idx >> logT, t = idx & (T - 1);
+      double2 v = make_double2(0.0, 0.0);
+      if (t < tcount) v = __ldg(&in[(uint64_t)r * job.ntubes + t]);
+      if (job.conj_in) v.y = -v.y;
+      cbuf[idx] = v;
     }
   }
+  __syncthreads();
+  const int last_reg = is_reg_radix(plan.radix[S - 1]) ? 1 : 0;
+  for (; s < S - last_reg; ++s) {
+    stage_smem(cbuf, obuf, tw, p, logT, Ns, plan.radix[s]);
+    __syncthreads();
+    double2* tmp = cbuf;
+    cbuf = obuf;
+    obuf = tmp;
+    Ns *= plan.radix[s];
+  }
+  if (last_reg) {
+    const int R = plan.radix[S - 1];
+    if (R == 8) stage_last_global<8>(cbuf, job, t0, tcount, tw, p, logT, Ns);
+    else if (R == 4) stage_last_global<4>(cbuf, job, t0, tcount, tw, p, logT, Ns);
+    else stage_last_global<2>(cbuf, job, t0, tcount, tw, p, logT, Ns);
+  } else {  // generic last stage already ran into cbuf: explicit store
+    double2* __restrict__ out = job.out + t0;
+    const double sc = job.scale, sci = job.conj_out ? -sc : sc;
+    for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+      const int r = idx >> logT, t = idx & (T - 1);
+      if (t < tcount) {
+        const double2 v = cbuf[idx];
+        out[(uint64_t)r * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
+      }
+    }
+  }
+}
+
+// shared-memory buffers the kernel needs for a plan (host mirror of the
+// control flow above)
+static int fft_smem_buffers(const FftPlan& pl) {
+  const int S = pl.nstages;
+  if (S == 0) return 0;
+  const bool r0 = pl.radix[0] == 2 || pl.radix[0] == 4 || pl.radix[0] == 8;
+  const bool rl = pl.radix[S - 1] == 2 || pl.radix[S - 1] == 4 || pl.radix[S - 1] == 8;
+  if (S == 1 && r0) return 0;
+  // stages executed smem->smem
+  const int smem_stages = S - (r0 ? 1 : 0) - (rl ? 1 : 0);
+  return smem_stages == 0 ? 1 : 2;
 }
 
 // Large-p fallback: one Stockham stage per launch over global memory
@@ -277,10 +417,14 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
   if (!tw) return cudaErrorMemoryAllocation;
   const FftPlan plan = make_fft_plan(p);
 
-  const size_t per_tube = 2 * sizeof(double2) * (size_t)p;  // ping-pong
+  const int nbuf = fft_smem_buffers(plan);
+  const size_t per_tube = (size_t)nbuf * sizeof(double2) * (size_t)p;
   if (per_tube <= kSmemMax) {
+    // ~2048 elements (32 KB) per tile: T*16-byte coalesced rows, several CTAs/SM
     int logT = 0;
-    while (logT < 6 && (per_tube << (logT + 1)) <= kSmemBudget && (uint64_t(1) << logT) < maxtubes) ++logT;
+    while (logT < 6 && ((size_t)p << (logT + 1)) <= 2048 && (per_tube << (logT + 1)) <= kSmemBudget) ++logT;
+    if (logT < 3 && (per_tube << 3) <= kSmemBudget) logT = 3;  // >= 128-byte rows when it fits
+    while (logT > 0 && (uint64_t(1) << (logT - 1)) >= maxtubes) --logT;  // tiny jobs
     // small problems: trade tile width for CTA count (keep >= 8 tubes = 128 B rows)
     while (logT > 3 && (maxtubes >> logT) * (uint64_t)batch.njobs < 296) --logT;
     const size_t smem = per_tube << logT;
@@ -289,7 +433,7 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
       static bool attr_set[64] = {};
       std::lock_guard<std::mutex> lk(mu);
       if (device >= 0 && device < 64 && !attr_set[device]) {
-        cudaError_t e = cudaFuncSetAttribute(tube_fft_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(tube_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kSmemMax);
         if (e != cudaSuccess) return e;
         attr_set[device] = true;
@@ -297,7 +441,7 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
     }
     const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
     dim3 grid((unsigned)tiles, batch.njobs);
-    tube_fft_smem_kernel<<<grid, kFftThreads, smem, stream>>>(batch, plan, tw, logT);
+    tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, plan, tw, logT);
     count_launches(1);
     return cudaGetLastError();
   }
