@@ -2,18 +2,28 @@
 //
 // Replaces transform_tubes/fft_rec (/root/reference/proj/src/transform.cpp:12-68,
 // 116-147).  The reference gathers each stride-m*n tube into a heap vector and
-// runs a recursive smallest-prime-factor DIT with per-call twiddles; here a CTA
-// owns T consecutive tubes of one CD plane, reads the p x T tile with coalesced
-// 16-byte loads (consecutive tubes are consecutive in memory), runs a
-// mixed-radix Stockham FFT in shared memory (radix-8/4/2 register butterflies,
-// generic direct-DFT stages for odd prime factors — the same O(p^2) fallback the
-// reference takes for prime lengths, transform.cpp:48) and writes the tile back
-// with the conj/negate/scale of the TubeOp fused into the store.
+// runs a recursive smallest-prime-factor DIT with per-call twiddles.  Here a
+// CTA owns T consecutive tubes of one CD plane (consecutive tubes are
+// consecutive in memory, so every access is a T*16-byte coalesced row) and
+// runs a mixed-radix Stockham FFT: radix-8/4/2 register butterflies, generic
+// direct-DFT stages for odd prime factors (the same O(p^2) fallback the
+// reference takes for prime lengths, transform.cpp:48).  The first stage reads
+// HBM directly and the last stage writes HBM directly with the conj/negate/
+// scale of the TubeOp fused in, so a 64-point tube costs one HBM read, one
+// shared-memory round trip and one HBM write.
 //
-// Bytes per tube element: 16 B read + 16 B written per CD plane — the kernel is
-// HBM-bound (roofline of K1/K3).
+// Long tubes (p*T*16 B does not fit shared memory with T >= 8, e.g. p = 4096)
+// use a two-pass four-step split p = p1*p2: pass A transforms the p1-point
+// stride-p2 sub-tubes and applies the W_p^(n2*k1) twiddle, pass B transforms the
+// p2-point contiguous sub-tubes and writes the transposed result; both passes
+// keep T = 32-tube coalesced rows.  Lengths with no usable split (large primes)
+// use one generic stage per launch over global memory.
+//
+// Bytes per tube element: 16 B read + 16 B written per CD plane (x2 for the
+// two-pass split) — HBM-bound.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -52,7 +62,7 @@ const double2* twiddles_for(int device, int p, cudaStream_t stream) {
   auto it = g_tw.find(key);
   if (it != g_tw.end()) return it->second;
   // exp(-2 pi i k/p) evaluated in x87 long double (64-bit mantissa) and
-  // rounded once to double.
+  // rounded once to double; exact at the quarter points.
   std::vector<double2> h(p);
   const long double two_pi = 6.283185307179586476925286766559005768L;
   for (int k = 0; k < p; ++k) {
@@ -60,7 +70,6 @@ const double2* twiddles_for(int device, int p, cudaStream_t stream) {
     h[k].x = (double)cosl(ang);
     h[k].y = (double)(-sinl(ang));
   }
-  // exact values at the quarter points
   h[0] = make_double2(1.0, 0.0);
   if (p % 2 == 0) h[p / 2] = make_double2(-1.0, 0.0);
   if (p % 4 == 0) { h[p / 4] = make_double2(0.0, -1.0); h[3 * p / 4] = make_double2(0.0, 1.0); }
@@ -81,8 +90,7 @@ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
-// a * (-i)
-__device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }  // a * (-i)
 
 template <int R>
 __device__ __forceinline__ void dft_reg(double2 (&v)[R]);
@@ -125,14 +133,25 @@ __device__ __forceinline__ void dft_reg<8>(double2 (&v)[8]) {
   v[7] = csub(e[3], o3);
 }
 
-// One Stockham stage of radix R over a p x T smem tile (tube index fastest).
+__host__ __device__ __forceinline__ bool is_reg_radix(int R) { return R == 2 || R == 4 || R == 8; }
+
+// Row geometry of one launch.  A CTA in group g transforms, for each of its T
+// tubes, the L elements at rows  g*ig + i*is  (i < L) and writes output k to
+// row  g*og + k*os, optionally multiplied by W_p^(g*k) (four-step twiddle).
+// W_L^e is read from the length-p table as tw[e * tws], tws = p / L.
+struct FftGeom {
+  int L, ig, is, og, os, post_tw, tws;
+};
+
+// One Stockham stage of radix R over an L x T smem tile (tube index fastest).
 // src/dst element (r, t) at [r*T + t].  Ns = product of earlier radices.
 template <int R>
 __device__ __forceinline__ void stage_reg(const double2* __restrict__ src, double2* __restrict__ dst,
-                                          const double2* __restrict__ tw, int p, int logT, int Ns) {
+                                          const double2* __restrict__ tw, const FftGeom& G, int logT, int Ns) {
   const int T = 1 << logT;
-  const int pR = p / R;
-  const int twmul = p / (Ns * R);
+  const int L = G.L;
+  const int pR = L / R;
+  const int twmul = (L / (Ns * R)) * G.tws;
   for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
     const int j = b >> logT, t = b & (T - 1);
     const int jm = j % Ns;
@@ -154,23 +173,24 @@ __device__ __forceinline__ void stage_reg(const double2* __restrict__ src, doubl
 // Generic radix-R stage: one output per thread iteration, direct R-point DFT
 // folded with the stage twiddle into one table lookup.
 __device__ __forceinline__ void stage_generic(const double2* __restrict__ src, double2* __restrict__ dst,
-                                              const double2* __restrict__ tw, int p, int logT, int Ns,
+                                              const double2* __restrict__ tw, const FftGeom& G, int logT, int Ns,
                                               int R) {
   const int T = 1 << logT;
-  const int pR = p / R;
-  const int twmul = p / (Ns * R);
-  for (int b = threadIdx.x; b < (p << logT); b += blockDim.x) {
+  const int L = G.L;
+  const int pR = L / R;
+  const int twmul = L / (Ns * R);
+  for (int b = threadIdx.x; b < (L << logT); b += blockDim.x) {
     const int o = b >> logT, t = b & (T - 1);
     const int j = o / R, k = o - j * R;
     const int jm = j % Ns;
-    const int base = jm * twmul + k * pR;  // < p
+    const int base = jm * twmul + k * pR;  // < L
     double2 acc = src[(j << logT) + t];
     int e = 0;
     for (int r = 1; r < R; ++r) {
       e += base;
-      if (e >= p) e -= p;
+      if (e >= L) e -= L;
       const double2 x = src[((j + r * pR) << logT) + t];
-      const double2 w = __ldg(&tw[e]);
+      const double2 w = __ldg(&tw[e * G.tws]);
       acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
       acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
     }
@@ -179,33 +199,29 @@ __device__ __forceinline__ void stage_generic(const double2* __restrict__ src, d
   }
 }
 
-// ---------------------------------------------------------------------------
-// K1 / K3 kernel.  grid = (tiles, njobs); a CTA owns T = 1 << logT consecutive
-// tubes of one CD plane.  Stage 0 (radix 2/4/8) reads its butterfly inputs
-// straight from HBM (R independent 16-byte loads per thread, consecutive
-// threads on consecutive tubes -> T*16-byte coalesced rows) with the conj-in
-// fused; middle stages ping-pong in shared memory; the last stage (radix
-// 2/4/8) writes straight to HBM with the conj-out/scale fused.  A 64-point
-// tube is therefore one HBM read, one shared-memory round trip and one HBM
-// write.  Generic (odd prime) first/last stages fall back to an explicit
-// shared-memory tile load / store.
-__device__ __forceinline__ bool is_reg_radix(int R) { return R == 2 || R == 4 || R == 8; }
+__device__ __forceinline__ void stage_smem(const double2* src, double2* dst, const double2* __restrict__ tw,
+                                           const FftGeom& G, int logT, int Ns, int R) {
+  if (R == 8) stage_reg<8>(src, dst, tw, G, logT, Ns);
+  else if (R == 4) stage_reg<4>(src, dst, tw, G, logT, Ns);
+  else if (R == 2) stage_reg<2>(src, dst, tw, G, logT, Ns);
+  else stage_generic(src, dst, tw, G, logT, Ns, R);
+}
 
-template <int R>
-__device__ __forceinline__ void twiddle_dft(double2 (&v)[R], const double2* __restrict__ tw, int step) {
-  if (step != 0) {
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * step]));
-  }
-  dft_reg<R>(v);
+// output store with the four-step twiddle, conj-out and scale fused
+__device__ __forceinline__ void store_out(double2* __restrict__ out, const TubeJob& job, const FftGeom& G,
+                                          const double2* __restrict__ tw, int g, int kk, int t, double2 v) {
+  if (G.post_tw && g != 0) v = cmul(v, __ldg(&tw[g * kk]));
+  const double sc = job.scale;
+  const double sci = job.conj_out ? -sc : sc;
+  out[(uint64_t)(g * G.og + kk * G.os) * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
 }
 
 // stage 0: HBM -> registers -> smem (Ns = 1, so no twiddles)
 template <int R>
-__device__ __forceinline__ void stage_first_global(const TubeJob& job, uint64_t t0, int tcount, double2* __restrict__ dst,
-                                                   int p, int logT) {
+__device__ __forceinline__ void stage_first_global(const TubeJob& job, const FftGeom& G, int g, uint64_t t0,
+                                                   int tcount, double2* __restrict__ dst, int logT) {
   const int T = 1 << logT;
-  const int pR = p / R;
+  const int pR = G.L / R;
   const double2* __restrict__ in = job.in + t0;
   for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
     const int j = b >> logT, t = b & (T - 1);
@@ -213,116 +229,112 @@ __device__ __forceinline__ void stage_first_global(const TubeJob& job, uint64_t 
     const bool ok = t < tcount;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      v[r] = ok ? __ldg(&in[(uint64_t)(j + r * pR) * job.ntubes + t]) : make_double2(0.0, 0.0);
+      const int row = g * G.ig + (j + r * pR) * G.is;
+      v[r] = ok ? __ldg(&in[(uint64_t)row * job.ntubes + t]) : make_double2(0.0, 0.0);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
-    // Ns = 1: idxD = j*R, outputs at j*R + k
 #pragma unroll
     for (int k = 0; k < R; ++k) dst[((j * R + k) << logT) + t] = v[k];
   }
 }
 
-// last stage: smem -> registers -> HBM with conj-out/scale fused
+// last stage: smem -> registers -> HBM with the output ops fused
 template <int R>
-__device__ __forceinline__ void stage_last_global(const double2* __restrict__ src, const TubeJob& job, uint64_t t0,
-                                                  int tcount, const double2* __restrict__ tw, int p, int logT,
-                                                  int Ns) {
+__device__ __forceinline__ void stage_last_global(const double2* __restrict__ src, const TubeJob& job,
+                                                  const FftGeom& G, int g, uint64_t t0, int tcount,
+                                                  const double2* __restrict__ tw, int logT, int Ns) {
   const int T = 1 << logT;
-  const int pR = p / R;
-  const int twmul = p / (Ns * R);
+  const int pR = G.L / R;
+  const int twmul = (G.L / (Ns * R)) * G.tws;
   double2* __restrict__ out = job.out + t0;
-  const double sc = job.scale;
-  const double sci = job.conj_out ? -sc : sc;
   for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
     const int j = b >> logT, t = b & (T - 1);
     const int jm = j % Ns;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = src[((j + r * pR) << logT) + t];
-    twiddle_dft<R>(v, tw, jm * twmul);
+    const int step = jm * twmul;
+    if (step != 0) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * step]));
+    }
+    dft_reg<R>(v);
     if (t < tcount) {
       const int idxD = (j - jm) * R + jm;
 #pragma unroll
-      for (int k = 0; k < R; ++k)
-        out[(uint64_t)(idxD + k * Ns) * job.ntubes + t] = make_double2(v[k].x * sc, v[k].y * sci);
+      for (int k = 0; k < R; ++k) store_out(out, job, G, tw, g, idxD + k * Ns, t, v[k]);
     }
   }
 }
 
-// single-stage tube (p in {2, 4, 8}): HBM -> registers -> HBM
+// single-stage transform (L in {2, 4, 8}): HBM -> registers -> HBM
 template <int R>
-__device__ __forceinline__ void stage_only_global(const TubeJob& job, uint64_t t0, int tcount, int logT) {
+__device__ __forceinline__ void stage_only_global(const TubeJob& job, const FftGeom& G, int g, uint64_t t0,
+                                                  int tcount, const double2* __restrict__ tw, int logT) {
   const int T = 1 << logT;
   const double2* __restrict__ in = job.in + t0;
   double2* __restrict__ out = job.out + t0;
-  const double sc = job.scale;
-  const double sci = job.conj_out ? -sc : sc;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     if (t >= tcount) continue;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      v[r] = __ldg(&in[(uint64_t)r * job.ntubes + t]);
+      v[r] = __ldg(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
 #pragma unroll
-    for (int k = 0; k < R; ++k) out[(uint64_t)k * job.ntubes + t] = make_double2(v[k].x * sc, v[k].y * sci);
+    for (int k = 0; k < R; ++k) store_out(out, job, G, tw, g, k, t, v[k]);
   }
 }
 
-__device__ __forceinline__ void stage_smem(const double2* src, double2* dst, const double2* __restrict__ tw, int p,
-                                           int logT, int Ns, int R) {
-  if (R == 8) stage_reg<8>(src, dst, tw, p, logT, Ns);
-  else if (R == 4) stage_reg<4>(src, dst, tw, p, logT, Ns);
-  else if (R == 2) stage_reg<2>(src, dst, tw, p, logT, Ns);
-  else stage_generic(src, dst, tw, p, logT, Ns, R);
-}
-
-__global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan plan, const double2* __restrict__ tw,
-                                                       int logT) {
+// K1 / K3 kernel: grid = (tube tiles, jobs, groups), T = 1 << logT tubes per CTA.
+__global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan plan, FftGeom G,
+                                                       const double2* __restrict__ tw, int logT) {
   extern __shared__ double2 sm[];
   const TubeJob job = batch.job[blockIdx.y];
+  const int g = blockIdx.z;
   const int T = 1 << logT;
   const uint64_t t0 = (uint64_t)blockIdx.x << logT;
   if (t0 >= job.ntubes) return;
-  const int p = plan.p;
+  const int L = G.L;
   const int S = plan.nstages;
   const int tcount = (int)min((uint64_t)T, job.ntubes - t0);
 
-  if (S == 0) {  // p == 1: the transform is the identity, ops only
-    const double sc = job.scale, sci = job.conj_out ? -sc : sc;
+  if (S == 0) {  // L == 1: the transform is the identity, ops only
+    const double2* __restrict__ in = job.in + t0;
+    double2* __restrict__ out = job.out + t0;
     for (int t = threadIdx.x; t < tcount; t += blockDim.x) {
-      double2 v = __ldg(&job.in[t0 + t]);
+      double2 v = __ldg(&in[(uint64_t)(g * G.ig) * job.ntubes + t]);
       if (job.conj_in) v.y = -v.y;
-      job.out[t0 + t] = make_double2(v.x * sc, v.y * sci);
+      store_out(out, job, G, tw, g, 0, t, v);
     }
     return;
   }
   const int R0 = plan.radix[0];
   if (S == 1 && is_reg_radix(R0)) {
-    if (R0 == 8) stage_only_global<8>(job, t0, tcount, logT);
-    else if (R0 == 4) stage_only_global<4>(job, t0, tcount, logT);
-    else stage_only_global<2>(job, t0, tcount, logT);
+    if (R0 == 8) stage_only_global<8>(job, G, g, t0, tcount, tw, logT);
+    else if (R0 == 4) stage_only_global<4>(job, G, g, t0, tcount, tw, logT);
+    else stage_only_global<2>(job, G, g, t0, tcount, tw, logT);
     return;
   }
 
-  double2* cbuf = sm;                          // holds the current data
-  double2* obuf = sm + ((size_t)p << logT);    // other ping-pong buffer
+  double2* cbuf = sm;                        // holds the current data
+  double2* obuf = sm + ((size_t)L << logT);  // other ping-pong buffer
   int s = 0, Ns = 1;
   if (is_reg_radix(R0)) {
-    if (R0 == 8) stage_first_global<8>(job, t0, tcount, cbuf, p, logT);
-    else if (R0 == 4) stage_first_global<4>(job, t0, tcount, cbuf, p, logT);
-    else stage_first_global<2>(job, t0, tcount, cbuf, p, logT);
+    if (R0 == 8) stage_first_global<8>(job, G, g, t0, tcount, cbuf, logT);
+    else if (R0 == 4) stage_first_global<4>(job, G, g, t0, tcount, cbuf, logT);
+    else stage_first_global<2>(job, G, g, t0, tcount, cbuf, logT);
     s = 1;
     Ns = R0;
   } else {  // explicit coalesced tile load, conj fused
     const double2* __restrict__ in = job.in + t0;
-    for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < (L << logT); idx += blockDim.x) {
       const int r = idx >> logT, t = idx & (T - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (t < tcount) v = __ldg(&in[(uint64_t)r * job.ntubes + t]);
+      if (t < tcount) v = __ldg(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
       if (job.conj_in) v.y = -v.y;
       cbuf[idx] = v;
     }
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   __syncthreads();
   const int last_reg = is_reg_radix(plan.radix[S - 1]) ? 1 : 0;
   for (; s < S - last_reg; ++s) {
-    stage_smem(cbuf, obuf, tw, p, logT, Ns, plan.radix[s]);
+    stage_smem(cbuf, obuf, tw, G, logT, Ns, plan.radix[s]);
     __syncthreads();
     double2* tmp = cbuf;
     cbuf = obuf;
@@ -339,37 +351,20 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   }
   if (last_reg) {
     const int R = plan.radix[S - 1];
-    if (R == 8) stage_last_global<8>(cbuf, job, t0, tcount, tw, p, logT, Ns);
-    else if (R == 4) stage_last_global<4>(cbuf, job, t0, tcount, tw, p, logT, Ns);
-    else stage_last_global<2>(cbuf, job, t0, tcount, tw, p, logT, Ns);
+    if (R == 8) stage_last_global<8>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
+    else if (R == 4) stage_last_global<4>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
+    else stage_last_global<2>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
   } else {  // generic last stage already ran into cbuf: explicit store
     double2* __restrict__ out = job.out + t0;
-    const double sc = job.scale, sci = job.conj_out ? -sc : sc;
-    for (int idx = threadIdx.x; idx < (p << logT); idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < (L << logT); idx += blockDim.x) {
       const int r = idx >> logT, t = idx & (T - 1);
-      if (t < tcount) {
-        const double2 v = cbuf[idx];
-        out[(uint64_t)r * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
-      }
+      if (t < tcount) store_out(out, job, G, tw, g, r, t, cbuf[idx]);
     }
   }
 }
 
-// shared-memory buffers the kernel needs for a plan (host mirror of the
-// control flow above)
-static int fft_smem_buffers(const FftPlan& pl) {
-  const int S = pl.nstages;
-  if (S == 0) return 0;
-  const bool r0 = pl.radix[0] == 2 || pl.radix[0] == 4 || pl.radix[0] == 8;
-  const bool rl = pl.radix[S - 1] == 2 || pl.radix[S - 1] == 4 || pl.radix[S - 1] == 8;
-  if (S == 1 && r0) return 0;
-  // stages executed smem->smem
-  const int smem_stages = S - (r0 ? 1 : 0) - (rl ? 1 : 0);
-  return smem_stages == 0 ? 1 : 2;
-}
-
-// Large-p fallback: one Stockham stage per launch over global memory
-// (element (r, tube) at [r*ntubes + tube]).  Generic direct-DFT butterflies.
+// Fallback for long tubes with no usable split: one generic Stockham stage per
+// launch over global memory (element (r, tube) at [r*ntubes + tube]).
 __global__ void tube_fft_global_stage_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
                                              uint64_t ntubes, int p, int Ns, int R,
                                              const double2* __restrict__ tw, int conj_in, int conj_out,
@@ -404,55 +399,141 @@ __global__ void tube_fft_global_stage_kernel(const double2* __restrict__ src, do
 // ------------------------------------------------------------------ launch
 namespace {
 constexpr int kFftThreads = 256;
-constexpr size_t kSmemBudget = 96 * 1024;   // two CTAs per SM
-constexpr size_t kSmemMax = 224 * 1024;     // one CTA per SM
+constexpr size_t kSmemBudget = 96 * 1024;  // two CTAs per SM
+constexpr size_t kSmemMax = 224 * 1024;    // one CTA per SM
+
+// shared-memory buffers the kernel needs for a plan (host mirror of the
+// control flow above)
+int fft_smem_buffers(const FftPlan& pl) {
+  const int S = pl.nstages;
+  if (S == 0) return 0;
+  const bool r0 = is_reg_radix(pl.radix[0]);
+  const bool rl = is_reg_radix(pl.radix[S - 1]);
+  if (S == 1 && r0) return 0;
+  const int smem_stages = S - (r0 ? 1 : 0) - (rl ? 1 : 0);
+  return smem_stages == 0 ? 1 : 2;
+}
+
+cudaError_t ensure_smem_attr(int device) {
+  static std::mutex mu;
+  static bool attr_set[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device >= 0 && device < 64 && !attr_set[device]) {
+    cudaError_t e = cudaFuncSetAttribute(tube_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (e != cudaSuccess) return e;
+    attr_set[device] = true;
+  }
+  return cudaSuccess;
+}
+
+// tile width: ~2048 elements (32 KB) per tile, >= 8 tubes (128-byte rows)
+// when it fits, fewer for tiny jobs; returns -1 if even T = 1 does not fit.
+int choose_logT(const FftPlan& pl, int L, uint64_t maxtubes, int njobs, uint64_t groups, size_t* smem) {
+  const size_t per_tube = (size_t)fft_smem_buffers(pl) * sizeof(double2) * (size_t)L;
+  if (per_tube > kSmemMax) return -1;
+  int logT = 0;
+  while (logT < 6 && ((size_t)L << (logT + 1)) <= 2048 && (per_tube << (logT + 1)) <= kSmemBudget) ++logT;
+  if (logT < 3 && (per_tube << 3) <= kSmemBudget) logT = 3;
+  while (logT > 0 && (uint64_t(1) << (logT - 1)) >= maxtubes) --logT;
+  while (logT > 3 && (maxtubes >> logT) * (uint64_t)njobs * groups < 296) --logT;
+  *smem = per_tube << logT;
+  return logT;
+}
+
+cudaError_t launch_pass(const TubeBatch& batch, const FftPlan& pl, const FftGeom& G, const double2* tw,
+                        uint64_t maxtubes, int groups, int logT, size_t smem, cudaStream_t stream) {
+  const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
+  dim3 grid((unsigned)tiles, batch.njobs, groups);
+  tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// balanced split p = p1 * p2 (p1 >= p2 > 1) from the prime factors; 0 if prime
+void split_length(int p, int* p1, int* p2) {
+  std::vector<int> f;
+  int r = p;
+  for (int d = 2; (long long)d * d <= r; ++d)
+    while (r % d == 0) { f.push_back(d); r /= d; }
+  if (r > 1) f.push_back(r);
+  *p1 = *p2 = 0;
+  if (f.size() < 2) return;
+  std::sort(f.rbegin(), f.rend());
+  long long a = 1, b = 1;
+  for (int x : f) (a <= b ? a : b) *= x;
+  *p1 = (int)std::max(a, b);
+  *p2 = (int)std::min(a, b);
+}
 }  // namespace
 
 cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device) {
   if (batch.njobs == 0) return cudaSuccess;
   uint64_t maxtubes = 0;
-  for (int i = 0; i < batch.njobs; ++i) maxtubes = batch.job[i].ntubes > maxtubes ? batch.job[i].ntubes : maxtubes;
+  for (int i = 0; i < batch.njobs; ++i) maxtubes = std::max(maxtubes, batch.job[i].ntubes);
   if (maxtubes == 0) return cudaSuccess;
   const double2* tw = twiddles_for(device, p, stream);
   if (!tw) return cudaErrorMemoryAllocation;
-  const FftPlan plan = make_fft_plan(p);
+  cudaError_t e = ensure_smem_attr(device);
+  if (e != cudaSuccess) return e;
 
-  const int nbuf = fft_smem_buffers(plan);
-  const size_t per_tube = (size_t)nbuf * sizeof(double2) * (size_t)p;
-  if (per_tube <= kSmemMax) {
-    // ~2048 elements (32 KB) per tile: T*16-byte coalesced rows, several CTAs/SM
-    int logT = 0;
-    while (logT < 6 && ((size_t)p << (logT + 1)) <= 2048 && (per_tube << (logT + 1)) <= kSmemBudget) ++logT;
-    if (logT < 3 && (per_tube << 3) <= kSmemBudget) logT = 3;  // >= 128-byte rows when it fits
-    while (logT > 0 && (uint64_t(1) << (logT - 1)) >= maxtubes) --logT;  // tiny jobs
-    // small problems: trade tile width for CTA count (keep >= 8 tubes = 128 B rows)
-    while (logT > 3 && (maxtubes >> logT) * (uint64_t)batch.njobs < 296) --logT;
-    const size_t smem = per_tube << logT;
-    {
-      static std::mutex mu;
-      static bool attr_set[64] = {};
-      std::lock_guard<std::mutex> lk(mu);
-      if (device >= 0 && device < 64 && !attr_set[device]) {
-        cudaError_t e = cudaFuncSetAttribute(tube_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmemMax);
-        if (e != cudaSuccess) return e;
-        attr_set[device] = true;
-      }
-    }
-    const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
-    dim3 grid((unsigned)tiles, batch.njobs);
-    tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, plan, tw, logT);
-    count_launches(1);
-    return cudaGetLastError();
+  // 1) single pass when a >= 8-tube tile fits in shared memory
+  const FftPlan plan = make_fft_plan(p);
+  size_t smem = 0;
+  int logT = choose_logT(plan, p, maxtubes, batch.njobs, 1, &smem);
+  const bool narrow = logT >= 0 && logT < 3 && maxtubes >= 8;
+  int p1 = 0, p2 = 0;
+  if (logT < 0 || narrow) split_length(p, &p1, &p2);
+  const bool split_ok = p1 > 1 && p2 > 1 && p1 <= 2048;
+  if (logT >= 0 && !(narrow && split_ok)) {
+    const FftGeom G{p, 0, 1, 0, 1, 0, 1};
+    return launch_pass(batch, plan, G, tw, maxtubes, 1, logT, smem, stream);
   }
 
-  // global multi-pass path (p > ~7000): one launch per stage per job
+  // 2) four-step split p = p1 * p2 through a scratch plane per job
+  if (split_ok) {
+    const FftPlan pl1 = make_fft_plan(p1), pl2 = make_fft_plan(p2);
+    size_t sm1 = 0, sm2 = 0;
+    const int lt1 = choose_logT(pl1, p1, maxtubes, batch.njobs, p2, &sm1);
+    const int lt2 = choose_logT(pl2, p2, maxtubes, batch.njobs, p1, &sm2);
+    if (lt1 >= 0 && lt2 >= 0) {
+      uint64_t total = 0;
+      for (int i = 0; i < batch.njobs; ++i) total += batch.job[i].ntubes * (uint64_t)p;
+      double2* scratch = nullptr;
+      if ((e = cudaMallocAsync(&scratch, total * sizeof(double2), stream)) != cudaSuccess) return e;
+      TubeBatch A = batch, B = batch;
+      uint64_t off = 0;
+      for (int i = 0; i < batch.njobs; ++i) {
+        const TubeJob& J = batch.job[i];
+        // pass A: conj-in, no output ops, into scratch
+        A.job[i].out = scratch + off;
+        A.job[i].conj_out = 0;
+        A.job[i].scale = 1.0;
+        // pass B: from scratch, output ops of the job
+        B.job[i].in = scratch + off;
+        B.job[i].conj_in = 0;
+        B.job[i].out = J.out;
+        off += J.ntubes * (uint64_t)p;
+      }
+      const FftGeom GA{p1, 1, p2, 1, p2, 1, p2};  // rows g + p2*i -> g + p2*k, twiddle W_p^(g*k)
+      const FftGeom GB{p2, p2, 1, 1, p1, 0, p1};  // rows p2*g + i -> g + p1*k
+      e = launch_pass(A, pl1, GA, tw, maxtubes, p2, lt1, sm1, stream);
+      if (e == cudaSuccess) e = launch_pass(B, pl2, GB, tw, maxtubes, p1, lt2, sm2, stream);
+      cudaError_t fe = cudaFreeAsync(scratch, stream);
+      return e != cudaSuccess ? e : fe;
+    }
+  }
+  if (logT >= 0) {  // narrow tile but no split: still correct
+    const FftGeom G{p, 0, 1, 0, 1, 0, 1};
+    return launch_pass(batch, plan, G, tw, maxtubes, 1, logT, smem, stream);
+  }
+
+  // 3) global multi-pass path (long prime-ish lengths): one launch per stage per job
   for (int i = 0; i < batch.njobs; ++i) {
     const TubeJob& J = batch.job[i];
     if (J.ntubes == 0) continue;
     const size_t bytes = sizeof(double2) * (size_t)p * J.ntubes;
     double2* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(&scratch, 2 * bytes, stream);
+    e = cudaMallocAsync(&scratch, 2 * bytes, stream);
     if (e != cudaSuccess) return e;
     double2* bufs[2] = {scratch, scratch + (size_t)p * J.ntubes};
     const double2* src = J.in;
@@ -462,8 +543,8 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
       // a single in-place stage must not write the buffer it is reading
       const bool bounce = last && first && J.in == J.out;
       double2* dst = (last && !bounce) ? J.out : bufs[s & 1];
-      const uint64_t total = (uint64_t)p * J.ntubes;
-      const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+      const uint64_t tot = (uint64_t)p * J.ntubes;
+      const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, 148ull * 16);
       tube_fft_global_stage_kernel<<<blocks, 256, 0, stream>>>(src, dst, J.ntubes, p, Ns, plan.radix[s], tw,
                                                                first ? J.conj_in : 0, last ? J.conj_out : 0,
                                                                last ? J.scale : 1.0);
@@ -474,10 +555,6 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
       }
       src = dst;
       Ns *= plan.radix[s];
-    }
-    if (plan.nstages == 0) {  // p == 1 cannot reach here; kept for completeness
-      cudaFreeAsync(scratch, stream);
-      continue;
     }
     e = cudaFreeAsync(scratch, stream);
     if (e != cudaSuccess) return e;

@@ -17,9 +17,14 @@
 // tcgen05 has no f64 kind); conjugation and the minus signs are sign-bit XORs
 // on the B fragments (ALU pipe), so the FP64 pipe only ever sees DMMA.
 //
+// Two tile shapes: the main one (64 x 16 tile, 8 warps, 2 CTAs/SM) for
+// GEMM-sized slices, and a small one (16 x 16 tile, whole K <= 16 per stage,
+// 4 warps) for many tiny slices (long tubes, e.g. m = n = s = 16, p = 4096).
+//
 // Determinism: no split-K, no atomics; each accumulator adds its four terms in
-// a fixed order for K-steps 0..n-1, independent of the M/N tiling, so results
-// are bitwise reproducible and identical across row shardings.
+// a fixed order for K-steps 0..n-1, independent of the M/N tiling and of the
+// tile shape, so results are bitwise reproducible and identical across row
+// shardings.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,24 +36,28 @@ namespace qtb {
 
 namespace {
 
-constexpr int BM = 64;       // rows of C per CTA
-constexpr int BN = 16;       // columns of C per CTA
-constexpr int BK = 8;        // complex K per pipeline stage
-constexpr int STAGES = 2;    // cp.async ring depth
-constexpr int NTHREADS = 256;  // 8 warps: 4 (M) x 2 (N), warp tile 16 x 8
+// Tile configuration.  Warps are laid out WM x WN; a warp owns RB 8-row blocks
+// x one 8-column block of the tile, for all 8 (or 4, SELF) real components.
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int RB_, int STAGES_, int MINB_>
+struct TileCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, RB = RB_, STAGES = STAGES_;
+  static constexpr int MINB = MINB_;
+  static constexpr int NTHREADS = 32 * WM * WN;
+  // smem tile geometry (double2 units); XOR swizzles make every fragment load
+  // a conflict-free LDS.128 without padding:
+  //   A plane: [BM][BK], element (i, c) at i*BK + (c ^ ((i & 1) << 2))
+  //   B plane: [BK][BN], element (k, j) at k*BN + (j ^ ((k & 3) << 1))
+  static constexpr int A_PLANE = BM * BK;
+  static constexpr int B_PLANE = BK * BN;
+  static constexpr int STAGE_ELEMS = 4 * A_PLANE + 4 * B_PLANE;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * 16;
+  static_assert(BM == WM * RB * 8 && BN == WN * 8, "warp layout must tile the CTA tile");
+  static_assert(BK % 8 == 0 && BN % 8 == 0, "swizzles need BK, BN multiples of 8");
+};
+using BigCfg = TileCfg<64, 16, 8, 4, 2, 2, 2, 2>;     // 256 threads, 80 KB smem
+using SmallCfg = TileCfg<16, 16, 16, 2, 2, 1, 2, 4>;  // 128 threads, 64 KB smem
 
-// smem tile geometry (double2 units); XOR swizzles make every fragment load a
-// conflict-free LDS.128 without padding:
-//   A plane: [BM][BK], element (i, c) at i*BK + (c ^ ((i & 1) << 2))
-//   B plane: [BK][BN], element (k, j) at k*BN + (j ^ ((k & 3) << 1))
-constexpr int A_PLANE = BM * BK;
-constexpr int B_PLANE = BK * BN;
-constexpr int STAGE_ELEMS = 4 * A_PLANE + 4 * B_PLANE;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
   const int n = valid ? 16 : 0;  // zero-fill out-of-range chunks
@@ -76,85 +85,83 @@ struct PairArgs {
   double2* c[4];        // Ĉ1_k, Ĉ2_k, Ĉ1_σ, Ĉ2_σ   (m x s each)
 };
 
-template <bool SELF>
-__device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int kt, int row0, int col0, int m,
-                                           int n, int s) {
+template <class C, bool SELF>
+__device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int kt, int row0, int col0, int m, int n,
+                                           int s) {
   constexpr int NP = SELF ? 2 : 4;
   const int tid = threadIdx.x;
-  const int k0 = kt * BK;
-  // A: NP planes x BM rows x BK chunks (plane index static -> no local-memory indexing)
+  const int k0 = kt * C::BK;
+  // plane index is static in every loop (no local-memory pointer indexing)
 #pragma unroll
   for (int pl = 0; pl < NP; ++pl) {
 #pragma unroll
-    for (int it = 0; it < A_PLANE / NTHREADS; ++it) {
-      const int id = tid + it * NTHREADS;
-      const int c = id & (BK - 1);
-      const int i = id / BK;
+    for (int id = tid; id < C::A_PLANE; id += C::NTHREADS) {
+      const int c = id % C::BK;
+      const int i = id / C::BK;
       const int gr = row0 + i, gc = k0 + c;
       const bool ok = gr < m && gc < n;
       const double2* src = P.a[pl] + (ok ? (size_t)gr * n + gc : 0);
-      double2* dst = st + pl * A_PLANE + i * BK + (c ^ ((i & 1) << 2));
+      double2* dst = st + pl * C::A_PLANE + i * C::BK + (c ^ ((i & 1) << 2));
       cp_async16(smem_u32(dst), src, ok);
     }
   }
-  // B: NP planes x BK rows x BN chunks; two planes per pass of 256 threads
-  static_assert(2 * B_PLANE == NTHREADS, "B tile mapping assumes 2 planes per pass");
-  double2* sb = st + 4 * A_PLANE;
+  double2* sb = st + 4 * C::A_PLANE;
 #pragma unroll
-  for (int it = 0; it < NP / 2; ++it) {
-    const int hi = tid >= B_PLANE;
-    const int id = tid - hi * B_PLANE;
-    const int j = id & (BN - 1);
-    const int k = id / BN;
-    const int gk = k0 + k, gj = col0 + j;
-    const bool ok = gk < n && gj < s;
-    const double2* plane = hi ? P.b[2 * it + 1] : P.b[2 * it];
-    const double2* src = plane + (ok ? (size_t)gk * s + gj : 0);
-    double2* dst = sb + (2 * it + hi) * B_PLANE + k * BN + (j ^ ((k & 3) << 1));
-    cp_async16(smem_u32(dst), src, ok);
+  for (int pl = 0; pl < NP; ++pl) {
+#pragma unroll
+    for (int id = tid; id < C::B_PLANE; id += C::NTHREADS) {
+      const int j = id % C::BN;
+      const int k = id / C::BN;
+      const int gk = k0 + k, gj = col0 + j;
+      const bool ok = gk < n && gj < s;
+      const double2* src = P.b[pl] + (ok ? (size_t)gk * s + gj : 0);
+      double2* dst = sb + pl * C::B_PLANE + k * C::BN + (j ^ ((k & 3) << 1));
+      cp_async16(smem_u32(dst), src, ok);
+    }
   }
 }
 
-template <bool SELF>
+template <class C, bool SELF>
 __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0, int m, int n, int s) {
   extern __shared__ double2 smem[];
   constexpr int NC = SELF ? 4 : 8;  // accumulated real components
+  constexpr int RB = C::RB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % C::WM, wn = warp / C::WM;
 
-  double acc[NC][2][2];
+  double acc[NC][RB][2];
 #pragma unroll
   for (int c = 0; c < NC; ++c)
 #pragma unroll
-    for (int rb = 0; rb < 2; ++rb) acc[c][rb][0] = acc[c][rb][1] = 0.0;
+    for (int rb = 0; rb < RB; ++rb) acc[c][rb][0] = acc[c][rb][1] = 0.0;
 
-  const int ktiles = (n + BK - 1) / BK;
+  const int ktiles = (n + C::BK - 1) / C::BK;
 #pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < ktiles) load_stage<SELF>(smem + st * STAGE_ELEMS, P, st, row0, col0, m, n, s);
+  for (int st = 0; st < C::STAGES - 1; ++st) {
+    if (st < ktiles) load_stage<C, SELF>(smem + st * C::STAGE_ELEMS, P, st, row0, col0, m, n, s);
     cp_async_commit();
   }
 
   for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<C::STAGES - 2>();
     __syncthreads();
     {
-      const int nk = kt + STAGES - 1;
-      if (nk < ktiles) load_stage<SELF>(smem + (nk % STAGES) * STAGE_ELEMS, P, nk, row0, col0, m, n, s);
+      const int nk = kt + C::STAGES - 1;
+      if (nk < ktiles) load_stage<C, SELF>(smem + (nk % C::STAGES) * C::STAGE_ELEMS, P, nk, row0, col0, m, n, s);
       cp_async_commit();
     }
-    const double2* sa = smem + (kt % STAGES) * STAGE_ELEMS;
-    const double2* sb = sa + 4 * A_PLANE;
+    const double2* sa = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
+    const double2* sb = sa + 4 * C::A_PLANE;
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
+    for (int ks = 0; ks < C::BK / 4; ++ks) {
       // B fragments: element (k = ks*4 + q, j = wn*8 + g); swizzle j ^ (q << 1)
       const int kb = ks * 4 + q;
       const int jb = (wn * 8 + g) ^ (q << 1);
       double br[4], bi[4];
 #pragma unroll
       for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
-        const double2 v = sb[pl * B_PLANE + kb * BN + jb];
+        const double2 v = sb[pl * C::B_PLANE + kb * C::BN + jb];
         br[pl] = v.x;
         bi[pl] = v.y;
       }
@@ -162,21 +169,20 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
       const double nb2k_r = dneg(br[1]);
       const double nb2k_i = dneg(bi[1]);
 #pragma unroll
-      for (int rb = 0; rb < 2; ++rb) {
-        const int i = wm * 16 + rb * 8 + g;
+      for (int rb = 0; rb < RB; ++rb) {
+        const int i = wm * (RB * 8) + rb * 8 + g;
         const int ca = (ks * 4 + q) ^ ((i & 1) << 2);
         double ar[4], ai[4];
 #pragma unroll
         for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
-          const double2 v = sa[pl * A_PLANE + i * BK + ca];
+          const double2 v = sa[pl * C::A_PLANE + i * C::BK + ca];
           ar[pl] = v.x;
           ai[pl] = v.y;
         }
-        if (SELF) {
-          // A1s = A1k, A2s = A2k
+        if (SELF) {  // A1s = A1k, A2s = A2k
           ar[2] = ar[0]; ai[2] = ai[0]; ar[3] = ar[1]; ai[3] = ai[1];
         }
-        // C1_k
+        // C1_k = A1k B1k - conj(A2s) B2k
         dmma(acc[0][rb], ar[0], br[0]);
         dmma(acc[0][rb], ai[0], nb1k_i);
         dmma(acc[0][rb], ar[3], nb2k_r);
@@ -185,7 +191,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
         dmma(acc[1][rb], ai[0], br[0]);
         dmma(acc[1][rb], ar[3], nb2k_i);
         dmma(acc[1][rb], ai[3], br[1]);
-        // C2_k
+        // C2_k = conj(A1s) B2k + A2k B1k
         dmma(acc[2][rb], ar[2], br[1]);
         dmma(acc[2][rb], ai[2], bi[1]);
         dmma(acc[2][rb], ar[1], br[0]);
@@ -198,7 +204,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
           const double nb1s_i = dneg(bi[2]);
           const double nb2s_r = dneg(br[3]);
           const double nb2s_i = dneg(bi[3]);
-          // C1_σ
+          // C1_σ = A1s B1s - conj(A2k) B2s
           dmma(acc[4 % NC][rb], ar[2], br[2]);
           dmma(acc[4 % NC][rb], ai[2], nb1s_i);
           dmma(acc[4 % NC][rb], ar[1], nb2s_r);
@@ -207,7 +213,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
           dmma(acc[5 % NC][rb], ai[2], br[2]);
           dmma(acc[5 % NC][rb], ar[1], nb2s_i);
           dmma(acc[5 % NC][rb], ai[1], br[3]);
-          // C2_σ
+          // C2_σ = conj(A1k) B2s + A2s B1s
           dmma(acc[6 % NC][rb], ar[0], br[3]);
           dmma(acc[6 % NC][rb], ai[0], bi[3]);
           dmma(acc[6 % NC][rb], ar[3], br[2]);
@@ -228,13 +234,13 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
   for (int f = 0; f < (SELF ? 1 : 2); ++f) {
 #pragma unroll
     for (int part = 0; part < 2; ++part) {
-      double2* C = P.c[f * 2 + part];
+      double2* Cp = P.c[f * 2 + part];
       const int cr = f * 4 + part * 2;
 #pragma unroll
-      for (int rb = 0; rb < 2; ++rb) {
-        const int row = row0 + wm * 16 + rb * 8 + g;
+      for (int rb = 0; rb < RB; ++rb) {
+        const int row = row0 + wm * (RB * 8) + rb * 8 + g;
         if (row < m) {
-          double2* dst = C + (size_t)row * s + col;
+          double2* dst = Cp + (size_t)row * s + col;
           if (col < s) dst[0] = make_double2(acc[cr % NC][rb][0], acc[(cr + 1) % NC][rb][0]);
           if (col + 1 < s) dst[1] = make_double2(acc[cr % NC][rb][1], acc[(cr + 1) % NC][rb][1]);
         }
@@ -243,13 +249,29 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 2)
+// Tile rasterisation: a CTA's linear index walks GROUP_M row tiles fastest
+// inside a band of the output, so the ~300 co-resident CTAs cover a squarish
+// GROUP_M x ~37 block of tiles and share both their Â rows and their B̂
+// columns through L2 (the plain column-fastest order re-reads B̂ from HBM once
+// per row tile: 146 GB vs 67 GB of DRAM reads per launch on config 5).
+constexpr int GROUP_M = 8;
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_spectral_gemm_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                 const double2* __restrict__ bh1, const double2* __restrict__ bh2,
-                                double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s,
-                                int p) {
-  const int k = blockIdx.z;
+                                double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
+                                int pair0) {
+  const int k = pair0 + blockIdx.y;
   const int sg = (p - k) % p;
+  const int ntm = (m + C::BM - 1) / C::BM, ntn = (s + C::BN - 1) / C::BN;
+  const int bid = blockIdx.x;
+  const int per_group = GROUP_M * ntn;
+  const int grp = bid / per_group;
+  const int first_m = grp * GROUP_M;
+  const int gsz = min(GROUP_M, ntm - first_m);
+  const int w = bid - grp * per_group;
+  const int tm = first_m + w % gsz, tn = w / gsz;
   const size_t amn = (size_t)m * n, bns = (size_t)n * s, cms = (size_t)m * s;
   PairArgs P;
   P.a[0] = ah1 + k * amn;
@@ -264,9 +286,37 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   P.c[1] = ch2 + k * cms;
   P.c[2] = ch1 + sg * cms;
   P.c[3] = ch2 + sg * cms;
-  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
-  if (sg == k) pair_tile<true>(P, row0, col0, m, n, s);
-  else pair_tile<false>(P, row0, col0, m, n, s);
+  const int row0 = tm * C::BM, col0 = tn * C::BN;
+  if (sg == k) pair_tile<C, true>(P, row0, col0, m, n, s);
+  else pair_tile<C, false>(P, row0, col0, m, n, s);
+}
+
+template <class C>
+cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2, double2* ch1,
+                       double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, cudaStream_t stream) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(paired_spectral_gemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)C::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const uint64_t npairs = p / 2 + 1;
+  const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
+  // a K that fits one stage (e.g. n <= 16 on the small tile) needs one buffer only
+  const uint64_t ktiles = (n + C::BK - 1) / C::BK;
+  const size_t smem = (size_t)std::min<uint64_t>(C::STAGES, std::max<uint64_t>(1, ktiles)) * C::STAGE_ELEMS * 16;
+  if (tiles > 0x7fffffffULL) return cudaErrorInvalidConfiguration;
+  for (uint64_t k0 = 0; k0 < npairs; k0 += 65535) {
+    const unsigned chunk = (unsigned)std::min<uint64_t>(65535, npairs - k0);
+    dim3 grid((unsigned)tiles, chunk);
+    paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m,
+                                                                                (int)n, (int)s, (int)p, (int)k0);
+    count_launches(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -275,22 +325,11 @@ cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2, const d
                                  double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                  cudaStream_t stream) {
   if (m == 0 || s == 0 || p == 0) return cudaSuccess;
-  {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-      attr_err = cudaFuncSetAttribute(paired_spectral_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM_BYTES);
-    });
-    if (attr_err != cudaSuccess) return attr_err;
-  }
-  const uint64_t npairs = p / 2 + 1;
-  dim3 grid((unsigned)((s + BN - 1) / BN), (unsigned)((m + BM - 1) / BM), (unsigned)npairs);
-  if (grid.y > 65535u || grid.z > 65535u) return cudaErrorInvalidConfiguration;
-  paired_spectral_gemm_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m,
-                                                                      (int)n, (int)s, (int)p);
-  count_launches(1);
-  return cudaGetLastError();
+  // Small slices (m, s <= 32): the 64-row tile would waste >= half its DMMAs
+  // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
+  if (m <= 32 && s <= 32)
+    return launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, stream);
+  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, stream);
 }
 
 }  // namespace qtb
