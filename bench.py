@@ -45,6 +45,24 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def ncu_traffic(cfg, kernel: str, rows: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the latest committed ncu capture of this config (profiles/r*/ncu_traffic_cfgN.json),
+    only when this run's launch is the captured one (full rows, N = 1)."""
+    import glob
+    if rows != cfg.m:
+        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_traffic_cfg{cfg.idx}.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    rec = d.get("per_launch", {}).get(kernel)
+    if not rec:
+        return None, None
+    return rec.get("traffic_bytes"), os.path.relpath(files[-1], ROOT)
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -349,6 +367,10 @@ def run_ours(args, cfg):
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
                 "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "kernel_ms": gemm_ms, "share_of_step": gemm_ms / ms,
                 "traffic": None}
+    traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+    roof["traffic"] = traffic
+    roof["traffic_source"] = traffic_src
+    roof["algorithmic_bytes"] = gemm_bytes
     stages = {
         "K1_fft_A": {"ms": fftA_ms, "GB_s": fftA_gbs, "frac_hbm": fftA_gbs / peaks["hbm_gbs"]},
         "K2_gemm": {"ms": gemm_ms, "TFLOP_s": gemm_tf, "frac_fp64": gemm_tf / PEAK_FP64_DMMA_TFLOPS},

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/qtensor_b200.h"
 #include "qt_internal.cuh"
@@ -240,95 +241,204 @@ int qt_spectral_product_f64_device(const double* ah1, const double* ah2, const d
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "K2 paired spectral GEMM");
 }
 
-// Row-slab pipelined host path.  Row i of C depends only on row i of A, so A
-// and C stream through the GPU in slabs of R rows while B is uploaded and
-// transformed once: two slab streams alternate so that the H2D copy of slab
-// j+1 and the D2H copy of slab j-1 (separate copy engines) overlap the
-// K1 -> K2 -> K3 compute of slab j.  Output is bitwise identical to the
-// one-shot path (same kernels, same per-row arithmetic).
-static int tprod_host_pipelined(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
-                                double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t R,
-                                HostCall& hc) {
+// Optional phase tracing of the host pipeline ($QTB_TRACE=1): CUDA events at
+// phase boundaries, printed to stderr as milliseconds from the call start.
+struct PhaseTrace {
+  bool on = false;
+  cudaEvent_t t0 = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  explicit PhaseTrace(cudaStream_t st) {
+    const char* env = getenv("QTB_TRACE");
+    on = env && *env && *env != '0';
+    if (on) {
+      cudaEventCreate(&t0);
+      cudaEventRecord(t0, st);
+    }
+  }
+  void mark(const std::string& label, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.emplace_back(label, e);
+  }
+  void dump() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    for (auto& [label, e] : marks) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, e);
+      fprintf(stderr, "[qtb trace] %8.3f ms  %s\n", ms, label.c_str());
+      cudaEventDestroy(e);
+    }
+    cudaEventDestroy(t0);
+  }
+};
+
+// Tiled streaming host path (large problems).  Row i of C depends only on row
+// i of A and column j of C only on column j of B, so C is computed in
+// (row slab x column chunk) tiles while A and B stream in over PCIe:
+//   copy-in stream : A slab 0, B chunk 0, A slab 1, B chunk 1, ...  (wavefront)
+//   compute stream : K1 of each arriving slab/chunk into resident Â / B̂, then
+//                    every tile (i, j) whose slab i and chunk j have arrived:
+//                    K2 -> K3 into one of three tile buffers
+//   copy-out stream: the tile's strided 3-D copy back into host C
+// so the GPU starts computing after one slab + one chunk instead of after all
+// of B, and the compute stream never waits on a download.  Every tile runs the
+// same kernels with the same per-element arithmetic, so the result is bitwise
+// identical to the device-resident path.
+static int tprod_host_tiled(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
+                            double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t R, uint64_t Q,
+                            HostCall& hc) {
   const size_t cx = sizeof(double2);
-  const size_t bb = n * s * p * cx, slab_a = R * n * p * cx, slab_c = R * s * p * cx;
+  const uint64_t NI = (m + R - 1) / R, NJ = (s + Q - 1) / Q;
+  const size_t ahat = m * n * p * cx, bhat = n * s * p * cx;       // per plane, resident
+  const size_t stA = R * n * p * cx, stB = n * Q * p * cx;        // per plane, staging
+  const size_t tile = R * Q * p * cx;                              // per plane, C tile
   cudaError_t e;
   int dev = 0;
   int rc = current_device(&dev);
   if (rc) return rc;
-  cudaStream_t ss[2] = {nullptr, nullptr};
-  cudaEvent_t evB = nullptr;
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&]() {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) evs.push_back(ev);
+    return ev;
+  };
   char* d = nullptr;
-  const size_t total = 4 * bb + 2 * (4 * slab_a + 2 * slab_c) + 256;
+  const size_t total = 2 * ahat + 2 * bhat + 2 * (2 * stA) + 2 * (2 * stB) + 3 * (2 * tile) + 256;
   auto cleanup = [&](int code) {
-    for (auto& x : ss)
-      if (x) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+    for (cudaStream_t x : {sin, scomp, sout})
+      if (x) cudaStreamSynchronize(x);
     if (d) cudaFreeAsync(d, hc.st);
-    if (evB) cudaEventDestroy(evB);
     cudaError_t se = cudaStreamSynchronize(hc.st);
+    for (cudaStream_t x : {sin, scomp, sout})
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     if (!code && se != cudaSuccess) return cuda_fail(se, "tprod_fast (host) sync");
     return code;
   };
-  for (auto& x : ss)
-    if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess) return cleanup(cuda_fail(e, "stream"));
-  if ((e = cudaEventCreateWithFlags(&evB, cudaEventDisableTiming)) != cudaSuccess) return cleanup(cuda_fail(e, "event"));
+  for (cudaStream_t* x : {&sin, &scomp, &sout})
+    if ((e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking)) != cudaSuccess) return cleanup(cuda_fail(e, "stream"));
   if ((e = cudaMallocAsync((void**)&d, total, hc.st)) != cudaSuccess)
     return cleanup(cuda_fail(e, "cudaMallocAsync(host call)"));
-  double* dB1 = (double*)d;
-  double* dB2 = (double*)(d + bb);
-  double* dBh1 = (double*)(d + 2 * bb);
-  double* dBh2 = (double*)(d + 3 * bb);
-  char* slabs = d + 4 * bb;
-  // B: upload + K1(B) once on the call stream
-  if ((rc = h2d(dB1, b1, bb, hc.st)) || (rc = h2d(dB2, b2, bb, hc.st))) return cleanup(rc);
-  {
-    TubeBatch fb{};
-    add_forward(fb, dB1, dB2, dBh1, dBh2, n * s);
-    if ((e = launch_tube_fft(fb, (int)p, hc.st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (B)"));
-  }
-  if ((e = cudaEventRecord(evB, hc.st)) != cudaSuccess) return cleanup(cuda_fail(e, "event"));
-  for (auto& x : ss)
-    if ((e = cudaStreamWaitEvent(x, evB, 0)) != cudaSuccess) return cleanup(cuda_fail(e, "wait"));
+  cudaEvent_t ready = mkev();
+  cudaEventRecord(ready, hc.st);  // allocation visible to the worker streams
+  for (cudaStream_t x : {sin, scomp, sout}) cudaStreamWaitEvent(x, ready, 0);
 
-  for (uint64_t r0 = 0, j = 0; r0 < m; r0 += R, ++j) {
-    const uint64_t rows = std::min<uint64_t>(R, m - r0);
-    cudaStream_t st = ss[j & 1];
-    char* base = slabs + (j & 1) * (4 * slab_a + 2 * slab_c);
-    double* dA1 = (double*)base;
-    double* dA2 = (double*)(base + slab_a);
-    double* dAh1 = (double*)(base + 2 * slab_a);
-    double* dAh2 = (double*)(base + 3 * slab_a);
-    double* dC1 = (double*)(base + 4 * slab_a);
-    double* dC2 = (double*)(base + 4 * slab_a + slab_c);
-    // slab of A = p strided chunks of rows x n complex (slice-major)
-    const size_t apitch = m * n * cx, awidth = rows * n * cx;
-    if ((e = cudaMemcpy2DAsync(dA1, awidth, a1 + 2 * r0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, st)) ||
-        (e = cudaMemcpy2DAsync(dA2, awidth, a2 + 2 * r0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, st)))
-      return cleanup(cuda_fail(e, "H2D A slab"));
-    TubeBatch fa{};
-    add_forward(fa, dA1, dA2, dAh1, dAh2, rows * n);
-    if ((e = launch_tube_fft(fa, (int)p, st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (A)"));
-    if ((e = launch_spectral_gemm((const double2*)dAh1, (const double2*)dAh2, (const double2*)dBh1,
-                                  (const double2*)dBh2, (double2*)dC1, (double2*)dC2, rows, n, s, p, st)) !=
-        cudaSuccess)
-      return cleanup(cuda_fail(e, "K2 paired spectral GEMM"));
+  char* cur = d;
+  auto take = [&](size_t bytes) { char* r = cur; cur += (bytes + 255) / 256 * 256; return (double*)r; };
+  double* Ah1 = take(ahat);
+  double* Ah2 = take(ahat);
+  double* Bh1 = take(bhat);
+  double* Bh2 = take(bhat);
+  double* SA[2][2] = {{take(stA), take(stA)}, {take(stA), take(stA)}};
+  double* SB[2][2] = {{take(stB), take(stB)}, {take(stB), take(stB)}};
+  double* T[3][2] = {{take(tile), take(tile)}, {take(tile), take(tile)}, {take(tile), take(tile)}};
+  cudaEvent_t stA_free[2] = {nullptr, nullptr}, stB_free[2] = {nullptr, nullptr};
+  cudaEvent_t tile_free[3] = {nullptr, nullptr, nullptr};
+  PhaseTrace tr(hc.st);
+
+  auto rows_of = [&](uint64_t i) { return std::min<uint64_t>(R, m - i * R); };
+  auto cols_of = [&](uint64_t j) { return std::min<uint64_t>(Q, s - j * Q); };
+  // B̂ chunk j is stored as its own contiguous n x cols(j) x p tensor
+  auto bh_chunk = [&](double* base, uint64_t j) { return (double*)((char*)base + j * Q * n * p * cx); };
+  auto ah_slab = [&](double* base, uint64_t i) { return (double*)((char*)base + i * R * n * p * cx); };
+
+  auto upload_a = [&](uint64_t i) -> int {
+    const int b = (int)(i & 1);
+    if (stA_free[b]) cudaStreamWaitEvent(sin, stA_free[b], 0);
+    const uint64_t rows = rows_of(i);
+    const size_t pitch = m * n * cx, width = rows * n * cx;
+    if ((e = cudaMemcpy2DAsync(SA[b][0], width, a1 + 2 * i * R * n, pitch, width, p, cudaMemcpyHostToDevice, sin)) ||
+        (e = cudaMemcpy2DAsync(SA[b][1], width, a2 + 2 * i * R * n, pitch, width, p, cudaMemcpyHostToDevice, sin)))
+      return cuda_fail(e, "H2D A slab");
+    cudaEvent_t in = mkev();
+    cudaEventRecord(in, sin);
+    cudaStreamWaitEvent(scomp, in, 0);
+    TubeBatch fb{};
+    add_forward(fb, SA[b][0], SA[b][1], ah_slab(Ah1, i), ah_slab(Ah2, i), rows * n);
+    if ((e = launch_tube_fft(fb, (int)p, scomp, dev)) != cudaSuccess) return cuda_fail(e, "K1 tube FFT (A)");
+    stA_free[b] = mkev();
+    cudaEventRecord(stA_free[b], scomp);
+    tr.mark("A slab " + std::to_string(i) + " transformed", scomp);
+    return QT_OK;
+  };
+  auto upload_b = [&](uint64_t j) -> int {
+    const int b = (int)(j & 1);
+    if (stB_free[b]) cudaStreamWaitEvent(sin, stB_free[b], 0);
+    const uint64_t cols = cols_of(j);
+    // column chunk: p*n rows of `cols` complex at host pitch s (uniform over slices)
+    const size_t pitch = s * cx, width = cols * cx;
+    if ((e = cudaMemcpy2DAsync(SB[b][0], width, b1 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice, sin)) ||
+        (e = cudaMemcpy2DAsync(SB[b][1], width, b2 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice, sin)))
+      return cuda_fail(e, "H2D B chunk");
+    cudaEvent_t in = mkev();
+    cudaEventRecord(in, sin);
+    cudaStreamWaitEvent(scomp, in, 0);
+    TubeBatch fb{};
+    add_forward(fb, SB[b][0], SB[b][1], bh_chunk(Bh1, j), bh_chunk(Bh2, j), n * cols);
+    if ((e = launch_tube_fft(fb, (int)p, scomp, dev)) != cudaSuccess) return cuda_fail(e, "K1 tube FFT (B)");
+    stB_free[b] = mkev();
+    cudaEventRecord(stB_free[b], scomp);
+    tr.mark("B chunk " + std::to_string(j) + " transformed", scomp);
+    return QT_OK;
+  };
+  uint64_t unit = 0;
+  auto compute_tile = [&](uint64_t i, uint64_t j) -> int {
+    const int t = (int)(unit % 3);
+    ++unit;
+    if (tile_free[t]) cudaStreamWaitEvent(scomp, tile_free[t], 0);
+    const uint64_t rows = rows_of(i), cols = cols_of(j);
+    if ((e = launch_spectral_gemm((const double2*)ah_slab(Ah1, i), (const double2*)ah_slab(Ah2, i),
+                                  (const double2*)bh_chunk(Bh1, j), (const double2*)bh_chunk(Bh2, j),
+                                  (double2*)T[t][0], (double2*)T[t][1], rows, n, cols, p, scomp)) != cudaSuccess)
+      return cuda_fail(e, "K2 paired spectral GEMM");
     TubeBatch ic{};
-    add_inverse(ic, dC1, dC2, dC1, dC2, rows * s, p);
-    if ((e = launch_tube_fft(ic, (int)p, st, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K3 inverse tube FFT"));
-    const size_t cpitch = m * s * cx, cwidth = rows * s * cx;
-    if ((e = cudaMemcpy2DAsync(c1 + 2 * r0 * s, cpitch, dC1, cwidth, cwidth, p, cudaMemcpyDeviceToHost, st)) ||
-        (e = cudaMemcpy2DAsync(c2 + 2 * r0 * s, cpitch, dC2, cwidth, cwidth, p, cudaMemcpyDeviceToHost, st)))
-      return cleanup(cuda_fail(e, "D2H C slab"));
+    add_inverse(ic, T[t][0], T[t][1], T[t][0], T[t][1], rows * cols, p);
+    if ((e = launch_tube_fft(ic, (int)p, scomp, dev)) != cudaSuccess) return cuda_fail(e, "K3 inverse tube FFT");
+    cudaEvent_t done = mkev();
+    cudaEventRecord(done, scomp);
+    cudaStreamWaitEvent(sout, done, 0);
+    // tile [p][rows][cols] -> host C rows i*R.., cols j*Q.. of every slice
+    for (int plane = 0; plane < 2; ++plane) {
+      cudaMemcpy3DParms cp{};
+      cp.srcPtr = make_cudaPitchedPtr(T[t][plane], cols * cx, cols * cx, rows);
+      double* hc_base = plane == 0 ? c1 : c2;
+      cp.dstPtr = make_cudaPitchedPtr(hc_base, s * cx, s * cx, m);
+      cp.dstPos = make_cudaPos(j * Q * cx, i * R, 0);
+      cp.extent = make_cudaExtent(cols * cx, rows, p);
+      cp.kind = cudaMemcpyDeviceToHost;
+      if ((e = cudaMemcpy3DAsync(&cp, sout)) != cudaSuccess) return cuda_fail(e, "D2H C tile");
+    }
+    tile_free[t] = mkev();
+    cudaEventRecord(tile_free[t], sout);
+    return QT_OK;
+  };
+
+  // wavefront over shells k: slab k and chunk k arrive, then every new tile
+  const uint64_t K = std::max(NI, NJ);
+  for (uint64_t k = 0; k < K; ++k) {
+    if (k < NI && (rc = upload_a(k))) return cleanup(rc);
+    if (k < NJ && (rc = upload_b(k))) return cleanup(rc);
+    if (k < NI)
+      for (uint64_t j = 0; j < std::min<uint64_t>(k + 1, NJ); ++j)
+        if ((rc = compute_tile(k, j))) return cleanup(rc);
+    if (k < NJ)
+      for (uint64_t i = 0; i < std::min<uint64_t>(k, NI); ++i)
+        if ((rc = compute_tile(i, k))) return cleanup(rc);
   }
-  // the call stream frees the buffers only after both slab streams are done
-  cudaEvent_t done[2] = {nullptr, nullptr};
-  for (int k = 0; k < 2; ++k) {
-    cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
-    cudaEventRecord(done[k], ss[k]);
-    cudaStreamWaitEvent(hc.st, done[k], 0);
+  tr.mark("all tiles computed", scomp);
+  tr.mark("all tiles downloaded", sout);
+  // the call stream frees the buffers only after every worker stream is done
+  for (cudaStream_t x : {sin, scomp, sout}) {
+    cudaEvent_t fin = mkev();
+    cudaEventRecord(fin, x);
+    cudaStreamWaitEvent(hc.st, fin, 0);
   }
-  rc = cleanup(QT_OK);
-  for (auto& ev : done) cudaEventDestroy(ev);
-  return rc;
+  tr.dump();
+  return cleanup(QT_OK);
 }
 
 int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
@@ -339,13 +449,14 @@ int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, cons
   HostCall hc;
   if ((rc = hc.begin(device))) return rc;
   const size_t ab = m * n * p * sizeof(double2), bb = n * s * p * sizeof(double2), cb = m * s * p * sizeof(double2);
-  // Large problems stream row slabs (>= 4 slabs of >= 64 rows, <= ~256 MB of A each).
-  if (n > 0 && s > 0 && m >= 256 && ab + cb >= (64ull << 20)) {
+  // Large problems stream (row slab x column chunk) tiles: ~8 slabs of >= 64
+  // rows and ~8 chunks of >= 64 columns (a multiple of the GEMM tile).
+  if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20)) {
     uint64_t R = std::max<uint64_t>(64, (m + 7) / 8);
-    const uint64_t row_bytes = n * p * sizeof(double2) * 2;
-    while (R > 64 && R * row_bytes > (256ull << 20)) R = (R + 1) / 2;
     R = (R + 63) / 64 * 64;
-    return tprod_host_pipelined(a1, a2, b1, b2, c1, c2, m, n, s, p, R, hc);
+    uint64_t Q = s >= 128 ? std::max<uint64_t>(64, (s + 7) / 8) : s;
+    if (Q < s) Q = (Q + 15) / 16 * 16;
+    return tprod_host_tiled(a1, a2, b1, b2, c1, c2, m, n, s, p, R, Q, hc);
   }
   double* d = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d, 2 * (ab + bb + cb) + 64, hc.st);
