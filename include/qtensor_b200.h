@@ -96,6 +96,19 @@ int qt_spectral_product_f64_device(const double* ahat1, const double* ahat2,
                                    uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                    void* stream);
 
+/* Stage 2 with explicit strides: B̂ rows at pitch ldb and slices bslice apart,
+ * Ĉ rows at pitch ldc and slices cslice apart (all in complex elements).  A
+ * column chunk of B̂ then writes straight into its columns of a wider Ĉ (pass
+ * chat + column offset): the building block of the chunked-broadcast
+ * multi-GPU pipeline (B arrives in column chunks, tproduct.cpp:90-104 per
+ * chunk). */
+int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
+                                      const double* bhat1, const double* bhat2,
+                                      double* chat1, double* chat2,
+                                      uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                      uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
+                                      void* stream);
+
 /* ---- host-buffer entry points (what the C++ drop-in calls) ------------
  * All pointers are host pointers (pageable or pinned).  The call copies to
  * device `device`, computes, copies back and synchronises. */

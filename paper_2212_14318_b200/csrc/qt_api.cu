@@ -441,6 +441,22 @@ static int tprod_host_tiled(const double* a1, const double* a2, const double* b1
   return cleanup(QT_OK);
 }
 
+int qt_spectral_product_f64_device_ld(const double* ah1, const double* ah2, const double* bh1, const double* bh2,
+                                      double* ch1, double* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                      uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream) {
+  t_err.clear();
+  int rc = check_dims(m, n, s, p, "spectral_product");
+  if (rc) return rc;
+  if (ldb < s || ldc < s || bslice < n * ldb || cslice < m * ldc || ldb > kIntMax || ldc > kIntMax)
+    return fail(QT_EINVAL, "spectral_product: leading dimensions smaller than the matrices");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  cudaError_t e = launch_spectral_gemm_ld((const double2*)ah1, (const double2*)ah2, (const double2*)bh1,
+                                          (const double2*)bh2, (double2*)ch1, (double2*)ch2, m, n, s, p, ldb, ldc,
+                                          bslice, cslice, (cudaStream_t)stream);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "K2 paired spectral GEMM");
+}
+
 int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                       double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device) {
   t_err.clear();

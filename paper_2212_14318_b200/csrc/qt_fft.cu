@@ -476,13 +476,17 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
   cudaError_t e = ensure_smem_attr(device);
   if (e != cudaSuccess) return e;
 
-  // 1) single pass when a >= 8-tube tile fits in shared memory
+  // 1) single pass when a >= 8-tube tile fits in shared memory.  The choice
+  // between single pass and split depends on p ONLY (never on the number of
+  // tubes), so every tube is transformed with the same arithmetic whatever the
+  // batch — results stay bitwise identical across row/column shardings.
   const FftPlan plan = make_fft_plan(p);
   size_t smem = 0;
   int logT = choose_logT(plan, p, maxtubes, batch.njobs, 1, &smem);
-  const bool narrow = logT >= 0 && logT < 3 && maxtubes >= 8;
+  const size_t per_tube = (size_t)fft_smem_buffers(plan) * sizeof(double2) * (size_t)p;
+  const bool narrow = per_tube > kSmemMax || (per_tube << 3) > kSmemMax;  // no 8-tube tile fits
   int p1 = 0, p2 = 0;
-  if (logT < 0 || narrow) split_length(p, &p1, &p2);
+  if (narrow) split_length(p, &p1, &p2);
   const bool split_ok = p1 > 1 && p2 > 1 && p1 <= 2048;
   if (logT >= 0 && !(narrow && split_ok)) {
     const FftGeom G{p, 0, 1, 0, 1, 0, 1};

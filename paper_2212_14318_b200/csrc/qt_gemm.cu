@@ -87,7 +87,7 @@ struct PairArgs {
 
 template <class C, bool SELF>
 __device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int kt, int row0, int col0, int m, int n,
-                                           int s) {
+                                           int s, int ldb) {
   constexpr int NP = SELF ? 2 : 4;
   const int tid = threadIdx.x;
   const int k0 = kt * C::BK;
@@ -114,7 +114,7 @@ __device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int k
       const int k = id / C::BN;
       const int gk = k0 + k, gj = col0 + j;
       const bool ok = gk < n && gj < s;
-      const double2* src = P.b[pl] + (ok ? (size_t)gk * s + gj : 0);
+      const double2* src = P.b[pl] + (ok ? (size_t)gk * ldb + gj : 0);
       double2* dst = sb + pl * C::B_PLANE + k * C::BN + (j ^ ((k & 3) << 1));
       cp_async16(smem_u32(dst), src, ok);
     }
@@ -122,7 +122,8 @@ __device__ __forceinline__ void load_stage(double2* st, const PairArgs& P, int k
 }
 
 template <class C, bool SELF>
-__device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0, int m, int n, int s) {
+__device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0, int m, int n, int s, int ldb,
+                                          int ldc) {
   extern __shared__ double2 smem[];
   constexpr int NC = SELF ? 4 : 8;  // accumulated real components
   constexpr int RB = C::RB;
@@ -139,7 +140,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
   const int ktiles = (n + C::BK - 1) / C::BK;
 #pragma unroll
   for (int st = 0; st < C::STAGES - 1; ++st) {
-    if (st < ktiles) load_stage<C, SELF>(smem + st * C::STAGE_ELEMS, P, st, row0, col0, m, n, s);
+    if (st < ktiles) load_stage<C, SELF>(smem + st * C::STAGE_ELEMS, P, st, row0, col0, m, n, s, ldb);
     cp_async_commit();
   }
 
@@ -148,7 +149,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
     __syncthreads();
     {
       const int nk = kt + C::STAGES - 1;
-      if (nk < ktiles) load_stage<C, SELF>(smem + (nk % C::STAGES) * C::STAGE_ELEMS, P, nk, row0, col0, m, n, s);
+      if (nk < ktiles) load_stage<C, SELF>(smem + (nk % C::STAGES) * C::STAGE_ELEMS, P, nk, row0, col0, m, n, s, ldb);
       cp_async_commit();
     }
     const double2* sa = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
@@ -240,7 +241,7 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
       for (int rb = 0; rb < RB; ++rb) {
         const int row = row0 + wm * (RB * 8) + rb * 8 + g;
         if (row < m) {
-          double2* dst = Cp + (size_t)row * s + col;
+          double2* dst = Cp + (size_t)row * ldc + col;
           if (col < s) dst[0] = make_double2(acc[cr % NC][rb][0], acc[(cr + 1) % NC][rb][0]);
           if (col + 1 < s) dst[1] = make_double2(acc[cr % NC][rb][1], acc[(cr + 1) % NC][rb][1]);
         }
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_spectral_gemm_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                 const double2* __restrict__ bh1, const double2* __restrict__ bh2,
                                 double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
-                                int pair0) {
+                                int pair0, int ldb, int ldc, long long bslice, long long cslice) {
   const int k = pair0 + blockIdx.y;
   const int sg = (p - k) % p;
   const int ntm = (m + C::BM - 1) / C::BM, ntn = (s + C::BN - 1) / C::BN;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
   const int gsz = min(GROUP_M, ntm - first_m);
   const int w = bid - grp * per_group;
   const int tm = first_m + w % gsz, tn = w / gsz;
-  const size_t amn = (size_t)m * n, bns = (size_t)n * s, cms = (size_t)m * s;
+  const size_t amn = (size_t)m * n, bns = (size_t)bslice, cms = (size_t)cslice;
   PairArgs P;
   P.a[0] = ah1 + k * amn;
   P.a[1] = ah2 + k * amn;
@@ -287,13 +288,14 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
   P.c[2] = ch1 + sg * cms;
   P.c[3] = ch2 + sg * cms;
   const int row0 = tm * C::BM, col0 = tn * C::BN;
-  if (sg == k) pair_tile<C, true>(P, row0, col0, m, n, s);
-  else pair_tile<C, false>(P, row0, col0, m, n, s);
+  if (sg == k) pair_tile<C, true>(P, row0, col0, m, n, s, ldb, ldc);
+  else pair_tile<C, false>(P, row0, col0, m, n, s, ldb, ldc);
 }
 
 template <class C>
 cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2, double2* ch1,
-                       double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, cudaStream_t stream) {
+                       double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc,
+                       uint64_t bslice, uint64_t cslice, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -310,8 +312,9 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
   for (uint64_t k0 = 0; k0 < npairs; k0 += 65535) {
     const unsigned chunk = (unsigned)std::min<uint64_t>(65535, npairs - k0);
     dim3 grid((unsigned)tiles, chunk);
-    paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m,
-                                                                                (int)n, (int)s, (int)p, (int)k0);
+    paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(
+        ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)k0, (int)ldb, (int)ldc, (long long)bslice,
+        (long long)cslice);
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -321,15 +324,21 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
 
 }  // namespace
 
-cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
-                                 double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                                 cudaStream_t stream) {
+cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                    double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                    uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream) {
   if (m == 0 || s == 0 || p == 0) return cudaSuccess;
   // Small slices (m, s <= 32): the 64-row tile would waste >= half its DMMAs
   // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
   if (m <= 32 && s <= 32)
-    return launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, stream);
-  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, stream);
+    return launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
+  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
+}
+
+cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                 double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                 cudaStream_t stream) {
+  return launch_spectral_gemm_ld(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, s, s, n * s, m * s, stream);
 }
 
 }  // namespace qtb

@@ -64,6 +64,14 @@ cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2,
                                  uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                  cudaStream_t stream);
 
+// Same with explicit leading dimensions: B̂ rows at pitch ldb (slice stride
+// bslice), Ĉ rows at pitch ldc (slice stride cslice) — lets a column chunk of
+// B̂ write straight into its columns of a wider Ĉ (multi-GPU chunked broadcast).
+cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                    double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                    uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
+                                    cudaStream_t stream);
+
 // Launch accounting (qt_kernel_launches).
 void count_launches(uint64_t k);
 

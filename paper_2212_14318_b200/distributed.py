@@ -1,0 +1,95 @@
+"""One rank's share of the row-sharded T-product, with B broadcast in column
+chunks that overlap the compute (one process per GPU, torch.distributed/NCCL
+for the plumbing).
+
+Row i of C depends only on row i of A, and column j of C only on column j of
+B.  Rank r owns rows shard.row_slab(m, world, r) of A and C; B
+lives on rank 0 as NJ column chunks and is broadcast chunk by chunk
+(async NCCL collectives on the process group's stream).  The compute stream
+transforms the A slab once, then for every chunk j waits only for chunk j's
+broadcast, transforms it (K1) and runs the paired-frequency GEMM (K2) straight
+into columns [c0_j, c1_j) of the C slab (qt_spectral_product_f64_device_ld);
+one inverse transform (K3) of the slab finishes the step.  So the transfer of
+chunk j+1 overlaps the K1/K2 of chunk j, and only chunk 0's broadcast is
+exposed.  Every element is computed with the same kernels and the same
+arithmetic as the single-GPU path: the stitched C is bitwise identical for
+every world size and chunk count (tests/test_gpu_parity.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, shard
+
+
+class RowShardedTProduct:
+    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None,
+                 nchunks: int = 8):
+        import torch
+        self.torch = torch
+        self.m, self.n, self.s, self.p = m, n, s, p
+        self.rank, self.world = rank, world
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.lo, self.hi = shard.row_slab(m, world, rank)
+        self.rows = self.hi - self.lo
+        q = -(-s // max(1, nchunks))
+        q = min(s, -(-q // 16) * 16)  # multiple of the GEMM column tile
+        self.chunks = [(c0, min(s, c0 + q)) for c0 in range(0, s, q)]
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.a = torch.empty((2, p, self.rows, 2 * n), **f64)
+        self.ah = torch.empty_like(self.a)
+        self.bc = [torch.empty((2, p, n, 2 * (c1 - c0)), **f64) for c0, c1 in self.chunks]
+        self.bh = [torch.empty_like(t) for t in self.bc]
+        self.c = torch.empty((2, p, self.rows, 2 * s), **f64)
+        self.L = _native.lib()
+
+    # ---------------------------------------------------------------- inputs
+    def load_a(self, a1: np.ndarray, a2: np.ndarray) -> None:
+        """Rows of this rank from full host planes (p, m, n) complex128."""
+        for k, src in enumerate((a1, a2)):
+            slab = np.ascontiguousarray(src[:, self.lo:self.hi]).view(np.float64)
+            self.a[k].copy_(self.torch.from_numpy(slab))
+
+    def load_b(self, b1: np.ndarray, b2: np.ndarray) -> None:
+        """Rank 0: B (p, n, s) host planes into the chunk buffers."""
+        for t, (c0, c1) in zip(self.bc, self.chunks):
+            for k, src in enumerate((b1, b2)):
+                t[k].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, :, c0:c1]).view(np.float64)))
+
+    # ----------------------------------------------------------------- step
+    def step(self, broadcast=None, stream=None) -> None:
+        """One T-product step.  `broadcast(tensor)` must enqueue an async
+        broadcast from rank 0 and return an object with .wait() (a
+        torch.distributed Work); None on a single rank."""
+        torch = self.torch
+        st = torch.cuda.current_stream() if stream is None else stream
+        sh = st.cuda_stream
+        L, n, s, p, rows = self.L, self.n, self.s, self.p, self.rows
+        works = [broadcast(t) for t in self.bc] if broadcast is not None else None
+        if rows:
+            _native.check(L.qt_qfft3_conj_f64_device(self.a[0].data_ptr(), self.a[1].data_ptr(),
+                                                     self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh),
+                          "qfft3_conj(A slab)")
+        for j, (c0, c1) in enumerate(self.chunks):
+            if works is not None:
+                works[j].wait()  # compute stream waits for chunk j only
+            if not rows:
+                continue
+            cols = c1 - c0
+            _native.check(L.qt_qfft3_conj_f64_device(self.bc[j][0].data_ptr(), self.bc[j][1].data_ptr(),
+                                                     self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), n, cols, p,
+                                                     sh), "qfft3_conj(B chunk)")
+            off = 16 * c0  # bytes: column c0 of every row of the C slab
+            _native.check(L.qt_spectral_product_f64_device_ld(
+                self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(),
+                self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, rows, n, cols, p,
+                cols, s, n * cols, rows * s, sh), "spectral_product(chunk)")
+        if rows:
+            _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
+                                                      self.c[0].data_ptr(), self.c[1].data_ptr(), rows, s, p, sh),
+                          "qifft3_conj(C slab)")
+
+    def result(self):
+        """(c1, c2) of this rank's rows as host complex128 (p, rows, s)."""
+        out = self.c.cpu().numpy().view(np.complex128)
+        return out[0], out[1]

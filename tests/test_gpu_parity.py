@@ -237,3 +237,39 @@ def test_multi_driver_single_device_matches():
     c = qt.tprod_fast(a, b)
     cm = qt.tprod_fast_multi(a, b, [0])
     assert bits_equal(c.t1, cm.t1) and bits_equal(c.t2, cm.t2)
+
+
+@pytest.mark.parametrize("world,nchunks", [(1, 1), (1, 8), (2, 3), (3, 8), (8, 5)])
+def test_chunked_row_sharded_pipeline_bitwise(world, nchunks):
+    """The N > 1 bench/driver pipeline (K1 of the A slab, per-column-chunk K1 of
+    B + strided K2 into the C slab, one K3) run rank by rank on one GPU
+    (B loaded directly instead of broadcast) equals tprod_fast bitwise."""
+    import torch
+    from paper_2212_14318_b200.distributed import RowShardedTProduct
+    m, n, s, p = 150, 40, 70, 12
+    a = qt.gen_random_tensor(m, n, p, 31)
+    b = qt.gen_random_tensor(n, s, p, 32)
+    want = qt.tprod_fast(a, b)
+    for r in range(world):
+        sh = RowShardedTProduct(m, n, s, p, r, world, "cuda:0", nchunks=nchunks)
+        sh.load_a(a.t1, a.t2)
+        sh.load_b(b.t1, b.t2)
+        sh.step()
+        torch.cuda.synchronize()
+        c1, c2 = sh.result()
+        assert bits_equal(c1, want.t1[:, sh.lo:sh.hi]) and bits_equal(c2, want.t2[:, sh.lo:sh.hi]), (world, r)
+
+
+def test_long_tube_sharding_bitwise():
+    """p = 4096 (four-step split) and a tiny shard still use the same per-tube
+    arithmetic: slabs of 1..16 rows stitch to the full result bitwise."""
+    from paper_2212_14318_b200 import shard
+    a = qt.gen_random_tensor(16, 16, 4096, 41)
+    b = qt.gen_random_tensor(16, 16, 4096, 42)
+    c = qt.tprod_fast(a, b)
+    for world in (2, 16):
+        for r in range(world):
+            lo, hi = shard.row_slab(16, world, r)
+            s1, s2 = shard.take_rows(a.t1, a.t2, lo, hi)
+            part = qt.tprod_fast(qt.CdTensor3(hi - lo, 16, 4096, s1, s2), b)
+            assert bits_equal(part.t1, c.t1[:, lo:hi]) and bits_equal(part.t2, c.t2[:, lo:hi])
