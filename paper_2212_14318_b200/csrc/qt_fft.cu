@@ -363,6 +363,71 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   }
 }
 
+// Two-stage specialisation (L = R0*R1 with R0, R1 in {2, 4, 8}: p = 16, 32, 64
+// and the 64-point halves of the four-step split — every BASELINE config):
+// radices, the sub-FFT length and the stage-1 twiddle stride are compile-time,
+// so the index math has no divisions and the kernel needs few registers
+// (higher occupancy for the small, latency-bound launches).  Arithmetic per
+// tube is the same Stockham formula as tube_fft_kernel.
+template <int R0, int R1>
+__global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom G, const double2* __restrict__ tw,
+                                                        int logT) {
+  constexpr int L = R0 * R1;
+  constexpr int P0 = L / R0, P1 = L / R1;
+  extern __shared__ double2 sm[];
+  const TubeJob job = batch.job[blockIdx.y];
+  const int g = blockIdx.z;
+  const int T = 1 << logT;
+  const uint64_t t0 = (uint64_t)blockIdx.x << logT;
+  if (t0 >= job.ntubes) return;
+  const int tcount = (int)min((uint64_t)T, job.ntubes - t0);
+  const uint64_t nt = job.ntubes;
+  const double2* __restrict__ in = job.in + t0 + (uint64_t)(g * G.ig) * nt;
+  const uint64_t istr = (uint64_t)G.is * nt;
+  // stage 0: HBM -> registers -> smem (no twiddles)
+  for (int b = threadIdx.x; b < (P0 << logT); b += blockDim.x) {
+    const int j = b >> logT, t = b & (T - 1);
+    double2 v[R0];
+    const bool ok = t < tcount;
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      v[r] = ok ? __ldg(&in[(uint64_t)(j + r * P0) * istr + t]) : make_double2(0.0, 0.0);
+      if (job.conj_in) v[r].y = -v[r].y;
+    }
+    dft_reg<R0>(v);
+#pragma unroll
+    for (int k = 0; k < R0; ++k) sm[((j * R0 + k) << logT) + t] = v[k];
+  }
+  __syncthreads();
+  // stage 1 (Ns = R0): smem -> registers -> HBM, output ops fused
+  double2* __restrict__ out = job.out + t0 + (uint64_t)(g * G.og) * nt;
+  const uint64_t ostr = (uint64_t)G.os * nt;
+  const double sc = job.scale;
+  const double sci = job.conj_out ? -sc : sc;
+  for (int b = threadIdx.x; b < (P1 << logT); b += blockDim.x) {
+    const int j = b >> logT, t = b & (T - 1);
+    const int jm = j % R0;
+    double2 v[R1];
+#pragma unroll
+    for (int r = 0; r < R1; ++r) v[r] = sm[((j + r * P1) << logT) + t];
+    if (jm != 0) {
+#pragma unroll
+      for (int r = 1; r < R1; ++r) v[r] = cmul(v[r], __ldg(&tw[r * jm * G.tws]));
+    }
+    dft_reg<R1>(v);
+    if (t < tcount) {
+      const int idxD = (j - jm) * R1 + jm;
+#pragma unroll
+      for (int k = 0; k < R1; ++k) {
+        const int kk = idxD + k * R0;
+        double2 y = v[k];
+        if (G.post_tw && g != 0) y = cmul(y, __ldg(&tw[g * kk]));
+        out[(uint64_t)kk * ostr + t] = make_double2(y.x * sc, y.y * sci);
+      }
+    }
+  }
+}
+
 // Fallback for long tubes with no usable split: one generic Stockham stage per
 // launch over global memory (element (r, tube) at [r*ntubes + tube]).
 __global__ void tube_fft_global_stage_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
@@ -440,8 +505,38 @@ int choose_logT(const FftPlan& pl, int L, uint64_t maxtubes, int njobs, uint64_t
   return logT;
 }
 
+template <int R0, int R1>
+cudaError_t launch_fft2(const TubeBatch& batch, const FftGeom& G, const double2* tw, uint64_t maxtubes, int groups,
+                        int njobs, cudaStream_t stream) {
+  constexpr int L = R0 * R1;
+  // stage 0 has exactly one butterfly per thread at full width (T = 256*R0/L)
+  int logT = 0;
+  while ((1 << logT) < 256 * R0 / L) ++logT;
+  while (logT > 0 && (uint64_t(1) << (logT - 1)) >= maxtubes) --logT;           // tiny jobs
+  while (logT > 3 && (maxtubes >> logT) * (uint64_t)njobs * groups < 296) --logT;  // >= 2 CTAs/SM
+  const size_t smem = sizeof(double2) * ((size_t)L << logT);
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(tube_fft2_kernel<R0, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  });
+  if (attr != cudaSuccess) return attr;
+  const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
+  dim3 grid((unsigned)tiles, njobs, groups);
+  tube_fft2_kernel<R0, R1><<<grid, kFftThreads, smem, stream>>>(batch, G, tw, logT);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pass(const TubeBatch& batch, const FftPlan& pl, const FftGeom& G, const double2* tw,
                         uint64_t maxtubes, int groups, int logT, size_t smem, cudaStream_t stream) {
+  if (pl.nstages == 2) {
+    const int r0 = pl.radix[0], r1 = pl.radix[1];
+    if (r0 == 8 && r1 == 8) return launch_fft2<8, 8>(batch, G, tw, maxtubes, groups, batch.njobs, stream);
+    if (r0 == 8 && r1 == 4) return launch_fft2<8, 4>(batch, G, tw, maxtubes, groups, batch.njobs, stream);
+    if (r0 == 8 && r1 == 2) return launch_fft2<8, 2>(batch, G, tw, maxtubes, groups, batch.njobs, stream);
+    if (r0 == 4 && r1 == 2) return launch_fft2<4, 2>(batch, G, tw, maxtubes, groups, batch.njobs, stream);
+  }
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
   dim3 grid((unsigned)tiles, batch.njobs, groups);
   tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
