@@ -109,6 +109,16 @@ int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
                                       uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                       void* stream);
 
+/* Definitional product tprod_naive = fold(bcirc(A) . unfold(B))
+ * (tproduct.hpp:23-25, tproduct.cpp:49-53) without materialising bcirc:
+ * C_k = sum_r A_{(k-r) mod p} (.) B_r on FP64 DMMA.  16 m n s p^2 real
+ * multiplications — the O(p^2) oracle the fast path is checked against. */
+int qt_tprod_naive_f64_device(const double* a1, const double* a2,
+                              const double* b1, const double* b2,
+                              double* c1, double* c2,
+                              uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                              void* stream);
+
 /* ---- host-buffer entry points (what the C++ drop-in calls) ------------
  * All pointers are host pointers (pageable or pinned).  The call copies to
  * device `device`, computes, copies back and synchronises. */
@@ -117,6 +127,11 @@ int qt_tprod_f64_host(const double* a1, const double* a2,
                       const double* b1, const double* b2,
                       double* c1, double* c2,
                       uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device);
+
+int qt_tprod_naive_f64_host(const double* a1, const double* a2,
+                            const double* b1, const double* b2,
+                            double* c1, double* c2,
+                            uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device);
 
 int qt_qfft3_conj_f64_host(const double* x1, const double* x2,
                            double* y1, double* y2,

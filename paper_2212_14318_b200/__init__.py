@@ -8,10 +8,10 @@ from . import _native
 from .configs import CONFIGS, Config, make_inputs
 from .tproduct import (CdTensor3, TProdWorkspace, TprodFlops, derive_seed, flops_estimate, gen_random_tensor,
                        gen_tensor, qfft3_conj, qfft3_conj_device, qifft3_conj, qifft3_conj_device, slice_reflect,
-                       spectral_product_device, tprod_fast, tprod_fast_device, tprod_fast_multi)
+                       spectral_product_device, tprod_fast, tprod_fast_device, tprod_fast_multi, tprod_naive)
 
 __all__ = [
-    "CdTensor3", "TProdWorkspace", "TprodFlops", "tprod_fast", "tprod_fast_device", "tprod_fast_multi",
+    "CdTensor3", "TProdWorkspace", "TprodFlops", "tprod_fast", "tprod_fast_device", "tprod_fast_multi", "tprod_naive",
     "qfft3_conj", "qifft3_conj", "qfft3_conj_device", "qifft3_conj_device", "spectral_product_device",
     "slice_reflect", "flops_estimate", "gen_random_tensor", "gen_tensor", "derive_seed",
     "CONFIGS", "Config", "make_inputs", "_native",

@@ -498,6 +498,49 @@ int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, cons
   return rc;
 }
 
+int qt_tprod_naive_f64_device(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
+                              double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream) {
+  t_err.clear();
+  int rc = check_dims(m, n, s, p, "tprod_naive");
+  if (rc) return rc;
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  cudaError_t e = launch_naive_tprod((const double2*)a1, (const double2*)a2, (const double2*)b1, (const double2*)b2,
+                                     (double2*)c1, (double2*)c2, m, n, s, p, (cudaStream_t)stream);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "definitional T-product");
+}
+
+int qt_tprod_naive_f64_host(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
+                            double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device) {
+  t_err.clear();
+  int rc = check_dims(m, n, s, p, "tprod_naive");
+  if (rc) return rc;
+  HostCall hc;
+  if ((rc = hc.begin(device))) return rc;
+  const size_t ab = m * n * p * sizeof(double2), bb = n * s * p * sizeof(double2), cb = m * s * p * sizeof(double2);
+  char* d = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&d, 2 * (ab + bb + cb) + 64, hc.st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host call)");
+  double* da1 = (double*)d;
+  double* da2 = (double*)(d + ab);
+  double* db1 = (double*)(d + 2 * ab);
+  double* db2 = (double*)(d + 2 * ab + bb);
+  double* dc1 = (double*)(d + 2 * ab + 2 * bb);
+  double* dc2 = (double*)(d + 2 * ab + 2 * bb + cb);
+  rc = QT_OK;
+  if (!rc && ab) rc = h2d(da1, a1, ab, hc.st);
+  if (!rc && ab) rc = h2d(da2, a2, ab, hc.st);
+  if (!rc && bb) rc = h2d(db1, b1, bb, hc.st);
+  if (!rc && bb) rc = h2d(db2, b2, bb, hc.st);
+  if (!rc) rc = qt_tprod_naive_f64_device(da1, da2, db1, db2, dc1, dc2, m, n, s, p, hc.st);
+  if (!rc && cb) rc = d2h(c1, dc1, cb, hc.st);
+  if (!rc && cb) rc = d2h(c2, dc2, cb, hc.st);
+  cudaFreeAsync(d, hc.st);
+  e = cudaStreamSynchronize(hc.st);
+  if (!rc && e != cudaSuccess) rc = cuda_fail(e, "tprod_naive (host) sync");
+  return rc;
+}
+
 static int transform_host(bool inverse, const double* x1, const double* x2, double* y1, double* y2, uint64_t m,
                           uint64_t n, uint64_t p, int device) {
   t_err.clear();

@@ -72,6 +72,11 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                     cudaStream_t stream);
 
+// Definitional product C_k = sum_r A_{(k-r) mod p} (.) B_r (qt_naive.cu).
+cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,
+                               double2* c1, double2* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                               cudaStream_t stream);
+
 // Launch accounting (qt_kernel_launches).
 void count_launches(uint64_t k);
 

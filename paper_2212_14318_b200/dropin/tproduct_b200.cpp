@@ -60,11 +60,16 @@ CdTensor3 identity_tensor(std::size_t n, std::size_t p) {
   return out;
 }
 
-// Definitional product fold(bcirc(a) . unfold(b)) (tproduct.hpp:23-25), via
-// the library's own quaternion matrix product (linalg module, unchanged).
+// Definitional product fold(bcirc(a) . unfold(b)) (tproduct.hpp:23-25) on the
+// B200: C_k = sum_r A_{(k-r) mod p} (.) B_r without materialising bcirc
+// (qt_tprod_naive_f64_host, csrc/qt_naive.cu).
 CdTensor3 tprod_naive(const CdTensor3& a, const CdTensor3& b) {
   if (a.n != b.m || a.p != b.p) throw std::invalid_argument("tprod_naive: dimension mismatch");
-  return fold(qmatmul(bcirc_of_tensor(a), unfold(b)), a.p);
+  CdTensor3 c(a.m, b.n, a.p);
+  b200::check(qt_tprod_naive_f64_host(b200::dp(a.t1), b200::dp(a.t2), b200::dp(b.t1), b200::dp(b.t2),
+                                      b200::dp(c.t1), b200::dp(c.t2), a.m, a.n, b.n, a.p, b200::device()),
+              "tprod_naive");
+  return c;
 }
 
 // FFT-domain T-product on the B200 (tproduct.hpp:35-46).  The transformed

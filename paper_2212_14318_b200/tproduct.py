@@ -28,7 +28,7 @@ import numpy as np
 from . import _native
 
 __all__ = [
-    "CdTensor3", "TProdWorkspace", "TprodFlops", "tprod_fast", "qfft3_conj", "qifft3_conj",
+    "CdTensor3", "TProdWorkspace", "TprodFlops", "tprod_fast", "tprod_naive", "qfft3_conj", "qifft3_conj",
     "slice_reflect", "flops_estimate", "gen_random_tensor", "gen_tensor", "derive_seed",
     "tprod_fast_device", "qfft3_conj_device", "qifft3_conj_device", "spectral_product_device",
     "tprod_fast_multi",
@@ -133,6 +133,19 @@ def tprod_fast(a: CdTensor3, b: CdTensor3, ws: TProdWorkspace | None = None, dev
     rc = L.qt_tprod_f64_host(_ptr(a.t1), _ptr(a.t2), _ptr(b.t1), _ptr(b.t2), _ptr(c.t1), _ptr(c.t2),
                              m, n, s, p, _device_index(device))
     _native.check(rc, "tprod_fast")
+    return c
+
+
+def tprod_naive(a: CdTensor3, b: CdTensor3, device=None) -> CdTensor3:
+    """Definitional product fold(bcirc(a) . unfold(b)) on the GPU
+    (tprod_naive, tproduct.hpp:23-25): C_k = sum_r A_{(k-r) mod p} (.) B_r."""
+    if a.n != b.m or a.p != b.p:
+        raise ValueError("tprod_naive: dimension mismatch")
+    m, n, s, p = a.m, a.n, b.n, a.p
+    c = CdTensor3(m, s, p)
+    rc = _native.lib().qt_tprod_naive_f64_host(_ptr(a.t1), _ptr(a.t2), _ptr(b.t1), _ptr(b.t2), _ptr(c.t1),
+                                               _ptr(c.t2), m, n, s, p, _device_index(device))
+    _native.check(rc, "tprod_naive")
     return c
 
 

@@ -273,3 +273,43 @@ def test_long_tube_sharding_bitwise():
             s1, s2 = shard.take_rows(a.t1, a.t2, lo, hi)
             part = qt.tprod_fast(qt.CdTensor3(hi - lo, 16, 4096, s1, s2), b)
             assert bits_equal(part.t1, c.t1[:, lo:hi]) and bits_equal(part.t2, c.t2[:, lo:hi])
+
+
+# ------------------------------------------------ GPU definitional product
+def test_gpu_naive_reference_kats():  # test_tproduct.cpp:60-86 through the GPU tprod_naive
+    rng = RefRng(7)
+    a, b = rng.tensor(3, 2, 1), rng.tensor(2, 4, 1)
+    c = as_pair(qt.tprod_naive(to_cd(a), to_cd(b)))
+    w1 = a[0][0] @ b[0][0] - a[1][0] @ np.conj(b[1][0])
+    w2 = a[0][0] @ b[1][0] + a[1][0] @ np.conj(b[0][0])
+    assert np.sqrt(np.sum(np.abs(c[0][0] - w1) ** 2) + np.sum(np.abs(c[1][0] - w2) ** 2)) <= 1e-14
+    t = rng.tensor(3, 4, 6)
+    eye = (np.zeros((6, 4, 4), np.complex128), np.zeros((6, 4, 4), np.complex128))
+    eye[0][0] = np.eye(4)
+    assert O.rel_frob_error(as_pair(qt.tprod_naive(to_cd(t), to_cd(eye))), t) <= 1e-12
+    with pytest.raises(ValueError):
+        qt.tprod_naive(to_cd(a), to_cd(rng.tensor(3, 2, 1)))
+
+
+@pytest.mark.parametrize("m,n,s,p", [(5, 4, 3, 6), (1, 1, 1, 5), (8, 8, 8, 12), (33, 17, 40, 7), (70, 9, 20, 4),
+                                     (3, 3, 3, 1), (2, 0, 3, 4)])
+def test_gpu_naive_against_oracle_naive(m, n, s, p):
+    a = O.gen_random_tensor(m, max(n, 1), p, 500 + m)
+    b = O.gen_random_tensor(max(n, 1), s, p, 600 + s)
+    if n == 0:
+        a = (a[0][:, :, :0], a[1][:, :, :0])
+        b = (b[0][:, :0, :], b[1][:, :0, :])
+        got = as_pair(qt.tprod_naive(to_cd(a) if m else qt.CdTensor3(m, 0, p), qt.CdTensor3(0, s, p)))
+        assert not np.any(got[0]) and not np.any(got[1])
+        return
+    got = as_pair(qt.tprod_naive(to_cd(a), to_cd(b)))
+    assert O.rel_frob_error(got, O.tprod_naive(a, b)) <= 1e-13
+
+
+def test_gpu_naive_equals_fast_full_config3():
+    """Full-tensor check of the FFT path against the O(p^2) definitional
+    product on the GPU at BASELINE config 3 (p = 4096, 16 m n s p^2 = 4.4e12)."""
+    a, b = qt.make_inputs(qt.CONFIGS[3])
+    fast = qt.tprod_fast(a, b)
+    naive = qt.tprod_naive(a, b)
+    assert O.rel_frob_error(as_pair(fast), as_pair(naive)) <= 1e-12
