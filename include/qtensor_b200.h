@@ -46,7 +46,12 @@ enum qt_status {
   QT_ECUDA = 2,  /* CUDA runtime / launch error                       */
   QT_ENOMEM = 3, /* device or pinned-host allocation failed            */
   QT_ENCCL = 4,  /* NCCL unavailable or failed (multi-GPU driver)      */
-  QT_ENODEV = 5  /* no usable sm_100 device                            */
+  QT_ENODEV = 5, /* no usable sm_100 device                            */
+  /* QT3 file I/O: TensorIoErrorKind of tensor_io.hpp:22 (+ open/read/write) */
+  QT_EBADMAGIC = 6,
+  QT_ETRUNCATED = 7,
+  QT_EDIMOVERFLOW = 8,
+  QT_EIO = 9
 };
 
 /* ---- library ---------------------------------------------------------- */
@@ -151,6 +156,23 @@ int qt_tprod_f64_multi(const double* a1, const double* a2,
                        double* c1, double* c2,
                        uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                        const int* devices, int ndev);
+
+/* ---- QT3 tensor files <-> device planes ---------------------------------
+ * The reference's binary format (tensor_io.hpp:16-20): "QT3\0", m, n, p as
+ * little-endian u64, then m*n*p records (w, x, y, z) little-endian doubles,
+ * slice-major.  Reading streams the file through pinned staging into the two
+ * device CD planes (a de-interleave kernel splits each 32-byte record);
+ * writing is the reverse.  Both return after the data is on the device / in
+ * the file, bit-exact.  Header errors follow parse_tensor
+ * (tensor_io.cpp:56-80): QT_EBADMAGIC, QT_ETRUNCATED, QT_EDIMOVERFLOW;
+ * open/read/write failures QT_EIO. */
+int qt_qt3_probe(const char* path, uint64_t* m, uint64_t* n, uint64_t* p);
+
+int qt_qt3_read_f64_device(const char* path, double* t1, double* t2,
+                           uint64_t m, uint64_t n, uint64_t p, void* stream);
+
+int qt_qt3_write_f64_device(const char* path, const double* t1, const double* t2,
+                            uint64_t m, uint64_t n, uint64_t p, void* stream);
 
 /* ---- seeded synthetic inputs (host) -----------------------------------
  * dist: QT_DIST_UNIFORM_SYM    all four components U[-1,1) — bitwise equal to

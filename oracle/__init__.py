@@ -82,6 +82,10 @@ def _load_ref():
             f = getattr(L, nm)
             f.restype = ctypes.c_int
             f.argtypes = args
+        L.ref_write_tensor.restype = ctypes.c_int
+        L.ref_write_tensor.argtypes = [ctypes.c_char_p, _p, _p, _u64, _u64, _u64]
+        L.ref_read_tensor.restype = ctypes.c_int
+        L.ref_read_tensor.argtypes = [ctypes.c_char_p, _p, _p, _p]
         L.ref_derive_seed.restype = _u64
         L.ref_derive_seed.argtypes = [_u64, _u64]
         L.ref_flops.restype = _u64
@@ -258,3 +262,39 @@ def ref_flops_estimate(m, n, s, p):
     out = np.zeros(4, np.uint64)
     _chk(int(_load_ref().ref_flops(m, n, s, p, out.ctypes.data)), "ref_flops")
     return [int(v) for v in out]
+
+
+def ref_write_tensor(path: str, t):
+    """The reference's write_tensor (tensor_io.cpp:85-92) on (t1, t2)."""
+    t1, p1 = _a(t[0])
+    t2, p2 = _a(t[1])
+    p, m, n = t1.shape
+    rc = _load_ref().ref_write_tensor(path.encode(), p1, p2, m, n, p)
+    if rc:
+        raise RuntimeError(f"ref_write_tensor rc={rc}")
+
+
+def ref_read_tensor(path: str):
+    """The reference's read_tensor (tensor_io.cpp:94-103): (t1, t2) or an
+    int error code 6/7/8 (TensorIoErrorKind BadMagic/Truncated/DimOverflow), 9."""
+    dims = np.zeros(3, np.uint64)
+    rc = _load_ref().ref_read_tensor(path.encode(), None, None, dims.ctypes.data)
+    if rc:
+        return rc
+    m, n, p = (int(v) for v in dims)
+    t1 = np.empty((p, m, n), np.complex128)
+    t2 = np.empty((p, m, n), np.complex128)
+    rc = _load_ref().ref_read_tensor(path.encode(), t1.ctypes.data, t2.ctypes.data, dims.ctypes.data)
+    return (t1, t2) if rc == 0 else rc
+
+
+def qt3_bytes(t1: np.ndarray, t2: np.ndarray) -> bytes:
+    """QT3 serialisation restated (tensor_io.cpp:37-50): magic, m, n, p (LE u64),
+    then per entry w, x, y, z (LE f64), slice-major."""
+    p, m, n = t1.shape
+    rec = np.empty((t1.size, 4), "<f8")
+    rec[:, 0] = t1.reshape(-1).real
+    rec[:, 1] = t1.reshape(-1).imag
+    rec[:, 2] = t2.reshape(-1).real
+    rec[:, 3] = t2.reshape(-1).imag
+    return b"QT3\x00" + np.array([m, n, p], "<u8").tobytes() + rec.tobytes()

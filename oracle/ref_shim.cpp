@@ -10,6 +10,7 @@
 #include <stdexcept>
 
 #include "qtensor/rng.hpp"
+#include "qtensor/tensor_io.hpp"
 #include "qtensor/tproduct.hpp"
 #include "qtensor/transform.hpp"
 
@@ -98,6 +99,31 @@ int ref_gen_random_tensor(uint64_t m, uint64_t n, uint64_t p, uint64_t seed, dou
     return 0;
   } catch (const std::invalid_argument&) {
     return 1;
+  }
+}
+
+// write_tensor / read_tensor (tensor_io.cpp:85-103): 0 ok, 6/7/8 TensorIoError kind, 9 other
+int ref_write_tensor(const char* path, const double* t1, const double* t2, uint64_t m, uint64_t n, uint64_t p) {
+  try {
+    qtref::write_tensor(path, in_tensor(t1, t2, m, n, p));
+    return 0;
+  } catch (...) {
+    return 9;
+  }
+}
+
+int ref_read_tensor(const char* path, double* t1, double* t2, uint64_t* dims) {
+  try {
+    CdTensor3 t = qtref::read_tensor(path);
+    dims[0] = t.m;
+    dims[1] = t.n;
+    dims[2] = t.p;
+    if (t1) out_tensor(t, t1, t2);
+    return 0;
+  } catch (const qtref::TensorIoError& e) {
+    return 6 + static_cast<int>(e.kind());
+  } catch (...) {
+    return 9;
   }
 }
 

@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqtensor_b200.so")
 
 QT_OK, QT_EINVAL, QT_ECUDA, QT_ENOMEM, QT_ENCCL, QT_ENODEV = 0, 1, 2, 3, 4, 5
+QT_EBADMAGIC, QT_ETRUNCATED, QT_EDIMOVERFLOW, QT_EIO = 6, 7, 8, 9
 QT_DIST_UNIFORM_SYM, QT_DIST_NORMAL, QT_DIST_PURE_UNIT = 0, 1, 2
 
 # Every symbol include/qtensor_b200.h declares: name -> (restype, argtypes)
@@ -36,12 +37,25 @@ SIGNATURES = {
     "qt_qfft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_qifft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_tprod_f64_multi": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
+    "qt_qt3_probe": (ctypes.c_int, [ctypes.c_char_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3),
+    "qt_qt3_read_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),
+    "qt_qt3_write_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),
     "qt_gen_tensor_f64": (ctypes.c_int, [ctypes.c_int] + [_u64] * 4 + [ctypes.c_double, _dp, _dp]),
     "qt_derive_seed": (_u64, [_u64, _u64]),
 }
 
 _lock = threading.Lock()
 _lib = None
+
+
+class TensorIoError(RuntimeError):
+    """QT3 header/payload errors (the reference's TensorIoError, tensor_io.hpp:22-32)."""
+
+    KINDS = {6: "BadMagic", 7: "Truncated", 8: "DimOverflow"}
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.kind = self.KINDS.get(code, "Io")
 
 
 class QtError(RuntimeError):
@@ -77,4 +91,6 @@ def check(rc: int, who: str) -> None:
     msg = (lib().qt_last_error() or b"").decode(errors="replace")
     if rc == QT_EINVAL:
         raise ValueError(f"{who}: {msg}")  # std::invalid_argument in the reference
+    if rc in (QT_EBADMAGIC, QT_ETRUNCATED, QT_EDIMOVERFLOW, QT_EIO):
+        raise TensorIoError(rc, f"{who}: {msg}")
     raise QtError(rc, f"{who}: {msg}")

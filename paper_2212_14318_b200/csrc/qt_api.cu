@@ -541,6 +541,38 @@ int qt_tprod_naive_f64_host(const double* a1, const double* a2, const double* b1
   return rc;
 }
 
+int qt_qt3_probe(const char* path, uint64_t* m, uint64_t* n, uint64_t* p) {
+  t_err.clear();
+  if (!path || !m || !n || !p) return fail(QT_EINVAL, "qt3_probe: null argument");
+  std::string err;
+  const int rc = qt3_probe(path, m, n, p, &err);
+  return rc ? fail(rc, "read_tensor: %s", err.c_str()) : QT_OK;
+}
+
+int qt_qt3_read_f64_device(const char* path, double* t1, double* t2, uint64_t m, uint64_t n, uint64_t p,
+                           void* stream) {
+  t_err.clear();
+  if (!path) return fail(QT_EINVAL, "qt3_read: null path");
+  int dev = 0;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  std::string err;
+  rc = qt3_read_device(path, t1, t2, m, n, p, (cudaStream_t)stream, &err);
+  return rc ? fail(rc, "read_tensor: %s", err.c_str()) : QT_OK;
+}
+
+int qt_qt3_write_f64_device(const char* path, const double* t1, const double* t2, uint64_t m, uint64_t n, uint64_t p,
+                            void* stream) {
+  t_err.clear();
+  if (!path) return fail(QT_EINVAL, "qt3_write: null path");
+  int dev = 0;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  std::string err;
+  rc = qt3_write_device(path, t1, t2, m, n, p, (cudaStream_t)stream, &err);
+  return rc ? fail(rc, "write_tensor: %s", err.c_str()) : QT_OK;
+}
+
 static int transform_host(bool inverse, const double* x1, const double* x2, double* y1, double* y2, uint64_t m,
                           uint64_t n, uint64_t p, int device) {
   t_err.clear();

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace qtb {
 
 // ---------------------------------------------------------------- tube FFT
@@ -76,6 +78,13 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
 cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,
                                double2* c1, double2* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                cudaStream_t stream);
+
+// QT3 file I/O (qt_io.cu); status codes of qtensor_b200.h, message in *err.
+int qt3_probe(const char* path, uint64_t* m, uint64_t* n, uint64_t* p, std::string* err);
+int qt3_read_device(const char* path, double* t1, double* t2, uint64_t m, uint64_t n, uint64_t p,
+                    cudaStream_t stream, std::string* err);
+int qt3_write_device(const char* path, const double* t1, const double* t2, uint64_t m, uint64_t n, uint64_t p,
+                     cudaStream_t stream, std::string* err);
 
 // Launch accounting (qt_kernel_launches).
 void count_launches(uint64_t k);

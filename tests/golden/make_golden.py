@@ -8,6 +8,8 @@ Fixture contents
 * small.npz    — full inputs and reference outputs (tprod_fast, tprod_naive,
                  qfft3_conj, qifft3_conj) for small seeded cases covering p = 1,
                  even/odd/prime p and degenerate m, n, s = 1.
+* ref_gen_3x2x4_seed9.qt3 — gen_random_tensor(3, 2, 4, 9) written by the
+                 reference's write_tensor (QT3 format, tensor_io.hpp:16-20).
 * configs.npz  — per BASELINE config: the input seeds, an input checksum, and
                  reference tprod_fast outputs on sampled (row-set x column-set)
                  tiles.  Row i / column j of C depend only on row i of A /
@@ -107,6 +109,9 @@ def main():
             cfg_out["cfg1_naive_err"] = np.array(O.rel_frob_error((f1, f2), (n1, n2)))
         print(f"cfg{c}: {len(rows)} rows x {len(cols)} cols sampled", flush=True)
     np.savez_compressed(os.path.join(HERE, "configs.npz"), **cfg_out)
+
+    # a QT3 file written by the reference's own write_tensor (tensor_io.cpp:85-92)
+    O.ref_write_tensor(os.path.join(HERE, "ref_gen_3x2x4_seed9.qt3"), O.ref_gen_random_tensor(3, 2, 4, 9))
 
 
 if __name__ == "__main__":
