@@ -3,13 +3,18 @@
 // The reference is single-threaded and has no distributed path;
 // this is the B200-native scale-out of tprod_fast (tproduct.cpp:75-111):
 //   * rows of A and C are split into contiguous slabs of ceil(m/G) rows — row i
-//     of C depends only on row i of A and all of B, so slabs are independent
-//     and the result is bitwise identical for every G;
-//   * B is copied host->device once (to devices[0]) and broadcast over NVLink /
-//     NVSwitch with one ncclBroadcast per call (both CD planes in one buffer);
-//   * each device runs the same K1 -> K2 -> K3 pipeline on its slab.
-// NCCL is resolved at run time with dlopen("libnccl.so.2") so the library does
-// not pin an NCCL build (torch bundles its own); G == 1 never touches NCCL.
+//     of C depends only on row i of A and all of B, so slabs are independent;
+//   * B is the only exchange: devices[0] uploads it column chunk by column
+//     chunk and each chunk is broadcast over NVLink / NVSwitch with
+//     ncclBroadcast on a communication stream; every device's compute stream
+//     waits only for the chunk it needs, transforms it (K1) and multiplies it
+//     into the matching columns of its C slab (strided K2), so the broadcast of
+//     chunk j+1 overlaps the compute of chunk j;
+//   * one inverse transform (K3) per slab, then the slab goes back to the host.
+// Every element is computed with the same kernels and arithmetic as the
+// single-GPU path, so the result is bitwise identical for every G (and equal to
+// qt_tprod_f64_host).  NCCL is resolved at run time with dlopen("libnccl.so.2")
+// so the library does not pin an NCCL build (torch bundles its own).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -31,7 +36,6 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
 };
 
@@ -39,8 +43,7 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names) {
+    for (const char* nm : {"libnccl.so.2", "libnccl.so"}) {
       api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
       if (api.h) break;
     }
@@ -49,8 +52,7 @@ NcclApi& nccl() {
     api.Broadcast = (decltype(api.Broadcast))dlsym(api.h, "ncclBroadcast");
     api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
-    api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
-    api.ok = api.CommInitAll && api.Broadcast && api.GroupStart && api.GroupEnd && api.GetErrorString;
+    api.ok = api.CommInitAll && api.Broadcast && api.GroupStart && api.GroupEnd;
   });
   return api;
 }
@@ -58,20 +60,24 @@ NcclApi& nccl() {
 std::mutex g_comm_mu;
 std::map<std::vector<int>, std::vector<ncclComm_t>> g_comms;
 
-thread_local std::string t_multi_err;
+struct DevState {
+  int dev = 0;
+  cudaStream_t comp = nullptr, comm = nullptr;
+  double* buf = nullptr;  // A slab, Â slab, C slab, B chunks, B̂ chunk (2 planes each)
+  std::vector<cudaEvent_t> evs;
+  int rc = QT_OK;
+};
 
 }  // namespace
 
 extern "C" {
 
-// declared in qtensor_b200.h
 int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                        double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, const int* devices, int ndev) {
   if (ndev <= 0 || !devices) return QT_EINVAL;
   if (p == 0) return QT_EINVAL;
-  if (ndev == 1 || m < (uint64_t)ndev) {
+  if (m == 0 || s == 0 || n == 0 || (uint64_t)ndev > m)
     return qt_tprod_f64_host(a1, a2, b1, b2, c1, c2, m, n, s, p, devices[0]);
-  }
   NcclApi& api = nccl();
   if (!api.ok) return QT_ENCCL;
 
@@ -82,53 +88,56 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     auto it = g_comms.find(key);
     if (it == g_comms.end()) {
       std::vector<ncclComm_t> c(ndev);
-      ncclResult_t r = api.CommInitAll(c.data(), ndev, devices);
-      if (r != ncclSuccess) return QT_ENCCL;
+      if (api.CommInitAll(c.data(), ndev, devices) != ncclSuccess) return QT_ENCCL;
       it = g_comms.emplace(key, c).first;
     }
     comms = it->second;
   }
 
+  const size_t cx = 2 * sizeof(double);
   const uint64_t slab = (m + ndev - 1) / ndev;
-  const size_t cx = sizeof(double) * 2;
-  const size_t bbytes = n * s * p * cx;
-  std::vector<int> rcs(ndev, QT_OK);
-  std::vector<cudaStream_t> streams(ndev, nullptr);
-  std::vector<double*> dB(ndev, nullptr), dA(ndev, nullptr), dC(ndev, nullptr);
+  // column chunks of B: ~8, a multiple of the 16-column GEMM tile
+  uint64_t Q = std::max<uint64_t>(16, (s + 7) / 8);
+  Q = std::min<uint64_t>(s, (Q + 15) / 16 * 16);
+  const uint64_t NJ = (s + Q - 1) / Q;
+  std::vector<DevState> st(ndev);
   std::vector<uint64_t> r0(ndev), rows(ndev);
   for (int g = 0; g < ndev; ++g) {
     r0[g] = std::min<uint64_t>(m, g * slab);
     rows[g] = std::min<uint64_t>(m, r0[g] + slab) - r0[g];
   }
+  auto chunk_cols = [&](uint64_t j) { return std::min<uint64_t>(Q, s - j * Q); };
+  const size_t bchunk = n * Q * p * cx;  // per plane
 
-  // 1) per-device setup + A slab upload; B to device 0
+  // 1) per device: streams, buffers, A slab upload + K1(A)
   auto setup = [&](int g) {
-    int& rc = rcs[g];
-    if (cudaSetDevice(devices[g]) != cudaSuccess) { rc = QT_ECUDA; return; }
-    if (cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking) != cudaSuccess) { rc = QT_ECUDA; return; }
-    cudaStream_t st = streams[g];
+    DevState& d = st[g];
+    d.dev = devices[g];
+    if (cudaSetDevice(d.dev) != cudaSuccess) { d.rc = QT_ECUDA; return; }
+    if (cudaStreamCreateWithFlags(&d.comp, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking) != cudaSuccess) {
+      d.rc = QT_ECUDA;
+      return;
+    }
     const size_t ab = rows[g] * n * p * cx, cb = rows[g] * s * p * cx;
-    if (cudaMallocAsync((void**)&dB[g], 2 * bbytes + 16, st) != cudaSuccess) { rc = QT_ENOMEM; return; }
-    if (cudaMallocAsync((void**)&dA[g], 2 * ab + 16, st) != cudaSuccess) { rc = QT_ENOMEM; return; }
-    if (cudaMallocAsync((void**)&dC[g], 2 * cb + 16, st) != cudaSuccess) { rc = QT_ENOMEM; return; }
-    if (rows[g] && n) {
-      // slab = p strided chunks of rows x n complex (slice-major layout)
-      const size_t spitch = m * n * cx, width = rows[g] * n * cx;
-      const double* src1 = a1 + 2 * r0[g] * n;
-      const double* src2 = a2 + 2 * r0[g] * n;
-      if (cudaMemcpy2DAsync(dA[g], width, src1, spitch, width, p, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-          cudaMemcpy2DAsync((char*)dA[g] + ab, width, src2, spitch, width, p, cudaMemcpyHostToDevice, st) !=
-              cudaSuccess) {
-        rc = QT_ECUDA;
-        return;
-      }
+    const size_t total = 4 * ab + 2 * cb + NJ * 2 * bchunk + 2 * bchunk + 1024;
+    if (cudaMallocAsync((void**)&d.buf, total, d.comp) != cudaSuccess) { d.rc = QT_ENOMEM; return; }
+    cudaEvent_t ready;
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventRecord(ready, d.comp);
+    cudaStreamWaitEvent(d.comm, ready, 0);
+    d.evs.push_back(ready);
+    char* base = (char*)d.buf;
+    double* A1 = (double*)base;
+    double* A2 = (double*)(base + ab);
+    const size_t spitch = m * n * cx, width = rows[g] * n * cx;
+    if (cudaMemcpy2DAsync(A1, width, a1 + 2 * r0[g] * n, spitch, width, p, cudaMemcpyHostToDevice, d.comp) ||
+        cudaMemcpy2DAsync(A2, width, a2 + 2 * r0[g] * n, spitch, width, p, cudaMemcpyHostToDevice, d.comp)) {
+      d.rc = QT_ECUDA;
+      return;
     }
-    if (g == 0 && bbytes) {
-      if (cudaMemcpyAsync(dB[0], b1, bbytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-          cudaMemcpyAsync((char*)dB[0] + bbytes, b2, bbytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-        rc = QT_ECUDA;
-      }
-    }
+    d.rc = qt_qfft3_conj_f64_device(A1, A2, (double*)(base + 2 * ab), (double*)(base + 3 * ab), rows[g], n, p,
+                                    d.comp);
   };
   {
     std::vector<std::thread> th;
@@ -136,53 +145,98 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     for (auto& t : th) t.join();
   }
   int rc = QT_OK;
-  for (int g = 0; g < ndev; ++g) rc = rc ? rc : rcs[g];
+  for (int g = 0; g < ndev; ++g) rc = rc ? rc : st[g].rc;
 
-  // 2) broadcast both B planes from devices[0] (one NCCL group)
-  if (!rc && bbytes) {
-    const size_t count = 2 * bbytes / sizeof(double) + 0;
-    api.GroupStart();
-    for (int g = 0; g < ndev && !rc; ++g) {
-      cudaSetDevice(devices[g]);
-      if (api.Broadcast(dB[g], dB[g], count, ncclFloat64, 0, comms[g], streams[g]) != ncclSuccess) rc = QT_ENCCL;
+  auto chunk_ptr = [&](int g, uint64_t j, int plane) {
+    const size_t ab = rows[g] * n * p * cx, cb = rows[g] * s * p * cx;
+    return (double*)((char*)st[g].buf + 4 * ab + 2 * cb + (2 * j + plane) * bchunk);
+  };
+  auto bhat_ptr = [&](int g, int plane) {
+    const size_t ab = rows[g] * n * p * cx, cb = rows[g] * s * p * cx;
+    return (double*)((char*)st[g].buf + 4 * ab + 2 * cb + 2 * NJ * bchunk + plane * bchunk);
+  };
+
+  // 2) B chunks: upload to devices[0] and broadcast (one NCCL group per chunk)
+  std::vector<std::vector<cudaEvent_t>> arrived(ndev, std::vector<cudaEvent_t>(NJ, nullptr));
+  for (uint64_t j = 0; j < NJ && !rc; ++j) {
+    const uint64_t cols = chunk_cols(j);
+    cudaSetDevice(st[0].dev);
+    const size_t pitch = s * cx, width = cols * cx;
+    if (cudaMemcpy2DAsync(chunk_ptr(0, j, 0), width, b1 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[0].comm) ||
+        cudaMemcpy2DAsync(chunk_ptr(0, j, 1), width, b2 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[0].comm)) {
+      rc = QT_ECUDA;
+      break;
+    }
+    const size_t count = 2 * n * cols * p * 2;  // doubles in both planes (planes are adjacent chunks)
+    if (api.GroupStart() != ncclSuccess) { rc = QT_ENCCL; break; }
+    for (int g = 0; g < ndev; ++g) {
+      cudaSetDevice(st[g].dev);
+      // both planes of chunk j are contiguous: [plane0 (n*cols*p)][gap][plane1] — broadcast each plane
+      if (api.Broadcast(chunk_ptr(g, j, 0), chunk_ptr(g, j, 0), count / 2, ncclFloat64, 0, comms[g], st[g].comm) !=
+              ncclSuccess ||
+          api.Broadcast(chunk_ptr(g, j, 1), chunk_ptr(g, j, 1), count / 2, ncclFloat64, 0, comms[g], st[g].comm) !=
+              ncclSuccess)
+        rc = QT_ENCCL;
     }
     if (api.GroupEnd() != ncclSuccess) rc = QT_ENCCL;
+    for (int g = 0; g < ndev; ++g) {
+      cudaSetDevice(st[g].dev);
+      cudaEventCreateWithFlags(&arrived[g][j], cudaEventDisableTiming);
+      cudaEventRecord(arrived[g][j], st[g].comm);
+    }
   }
 
-  // 3) per-device pipeline + strided download of the C slab
+  // 3) per device: for each chunk K1(B chunk) + strided K2 into the C slab; K3; download
   auto compute = [&](int g) {
-    int& r = rcs[g];
-    cudaSetDevice(devices[g]);
-    cudaStream_t st = streams[g];
+    DevState& d = st[g];
+    cudaSetDevice(d.dev);
     const size_t ab = rows[g] * n * p * cx, cb = rows[g] * s * p * cx;
-    r = qt_tprod_f64_device(dA[g], (double*)((char*)dA[g] + ab), dB[g], (double*)((char*)dB[g] + bbytes), dC[g],
-                            (double*)((char*)dC[g] + cb), rows[g], n, s, p, st);
-    if (r == QT_OK && rows[g] && s) {
+    char* base = (char*)d.buf;
+    const double* Ah1 = (double*)(base + 2 * ab);
+    const double* Ah2 = (double*)(base + 3 * ab);
+    double* C1 = (double*)(base + 4 * ab);
+    double* C2 = (double*)(base + 4 * ab + cb);
+    int& r = d.rc;
+    for (uint64_t j = 0; j < NJ && r == QT_OK; ++j) {
+      const uint64_t cols = chunk_cols(j);
+      cudaStreamWaitEvent(d.comp, arrived[g][j], 0);
+      r = qt_qfft3_conj_f64_device(chunk_ptr(g, j, 0), chunk_ptr(g, j, 1), bhat_ptr(g, 0), bhat_ptr(g, 1), n, cols,
+                                   p, d.comp);
+      if (r == QT_OK)
+        r = qt_spectral_product_f64_device_ld(Ah1, Ah2, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q,
+                                              C2 + 2 * j * Q, rows[g], n, cols, p, cols, s, n * cols, rows[g] * s,
+                                              d.comp);
+    }
+    if (r == QT_OK) r = qt_qifft3_conj_f64_device(C1, C2, C1, C2, rows[g], s, p, d.comp);
+    if (r == QT_OK) {
       const size_t dpitch = m * s * cx, width = rows[g] * s * cx;
-      double* dst1 = c1 + 2 * r0[g] * s;
-      double* dst2 = c2 + 2 * r0[g] * s;
-      if (cudaMemcpy2DAsync(dst1, dpitch, dC[g], width, width, p, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-          cudaMemcpy2DAsync(dst2, dpitch, (char*)dC[g] + cb, width, width, p, cudaMemcpyDeviceToHost, st) !=
-              cudaSuccess)
+      if (cudaMemcpy2DAsync(c1 + 2 * r0[g] * s, dpitch, C1, width, width, p, cudaMemcpyDeviceToHost, d.comp) ||
+          cudaMemcpy2DAsync(c2 + 2 * r0[g] * s, dpitch, C2, width, width, p, cudaMemcpyDeviceToHost, d.comp))
         r = QT_ECUDA;
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess && r == QT_OK) r = QT_ECUDA;
+    if (cudaStreamSynchronize(d.comp) != cudaSuccess && r == QT_OK) r = QT_ECUDA;
   };
   if (!rc) {
     std::vector<std::thread> th;
     for (int g = 0; g < ndev; ++g) th.emplace_back(compute, g);
     for (auto& t : th) t.join();
-    for (int g = 0; g < ndev; ++g) rc = rc ? rc : rcs[g];
+    for (int g = 0; g < ndev; ++g) rc = rc ? rc : st[g].rc;
   }
 
   for (int g = 0; g < ndev; ++g) {
-    if (!streams[g]) continue;
-    cudaSetDevice(devices[g]);
-    cudaFreeAsync(dA[g], streams[g]);
-    cudaFreeAsync(dB[g], streams[g]);
-    cudaFreeAsync(dC[g], streams[g]);
-    cudaStreamSynchronize(streams[g]);
-    cudaStreamDestroy(streams[g]);
+    DevState& d = st[g];
+    if (!d.comp) continue;
+    cudaSetDevice(d.dev);
+    cudaStreamSynchronize(d.comm);
+    if (d.buf) cudaFreeAsync(d.buf, d.comp);
+    cudaStreamSynchronize(d.comp);
+    for (cudaEvent_t e : d.evs) cudaEventDestroy(e);
+    for (cudaEvent_t e : arrived[g])
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(d.comp);
+    cudaStreamDestroy(d.comm);
   }
   return rc;
 }

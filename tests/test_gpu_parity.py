@@ -231,9 +231,13 @@ def test_linearity_at_full_size():
     assert O.rel_frob_error(as_pair(lhs), (r1.t1 + r2.t1, r1.t2 + r2.t2)) <= 1e-13
 
 
-def test_multi_driver_single_device_matches():
-    a = qt.gen_random_tensor(40, 24, 12, 8)
-    b = qt.gen_random_tensor(24, 20, 12, 9)
+@pytest.mark.parametrize("m,n,s,p", [(40, 24, 20, 12), (130, 33, 70, 16), (300, 64, 200, 64), (17, 16, 16, 4096)])
+def test_multi_driver_single_device_matches(m, n, s, p):
+    """qt_tprod_f64_multi on one device runs the whole NCCL pipeline (column-
+    chunked ncclBroadcast of B, per-chunk K1 + strided K2, K3) and must equal
+    the single-GPU host path bitwise."""
+    a = qt.gen_random_tensor(m, n, p, 8)
+    b = qt.gen_random_tensor(n, s, p, 9)
     c = qt.tprod_fast(a, b)
     cm = qt.tprod_fast_multi(a, b, [0])
     assert bits_equal(c.t1, cm.t1) and bits_equal(c.t2, cm.t2)
