@@ -180,27 +180,31 @@ def auto_tile(cfg):
     return {1: 32, 2: 128, 3: 16, 4: 64, 5: 128}.get(cfg.idx, 64)
 
 
-def host_inputs(cfg, pinned: bool):
-    """Seeded host inputs (reference generator / SURVEY §8(d) distributions)."""
+def host_inputs(cfg, pinned: bool, need_b: bool = True):
+    """Seeded host inputs (reference generator / SURVEY §8(d) distributions).
+    B is skipped (None) when need_b is False (ranks != 0 of a sharded run)."""
     import torch
 
     import paper_2212_14318_b200 as qt
     sa, sb = cfg.seeds()
-    shp_a, shp_b = (cfg.p, cfg.m, cfg.n), (cfg.p, cfg.n, cfg.s)
 
-    def alloc(shape):
-        t = torch.empty(shape + (2,), dtype=torch.float64, pin_memory=pinned)
-        return t
+    def alloc(rows, cols):
+        t = torch.empty((cfg.p, rows, cols, 2), dtype=torch.float64, pin_memory=pinned)
+        return t, t.numpy().view(np.complex128)[..., 0]
 
-    bufs = {k: alloc(shp_a if k.startswith("a") else shp_b) for k in ("a1", "a2", "b1", "b2")}
-    a = qt.CdTensor3(cfg.m, cfg.n, cfg.p, bufs["a1"].numpy().view(np.complex128)[..., 0],
-                     bufs["a2"].numpy().view(np.complex128)[..., 0])
-    b = qt.CdTensor3(cfg.n, cfg.s, cfg.p, bufs["b1"].numpy().view(np.complex128)[..., 0],
-                     bufs["b2"].numpy().view(np.complex128)[..., 0])
-    # CdTensor3 keeps views of the pinned buffers (no copy): generate in place
+    bufs = {}
+    bufs["a1"], v1 = alloc(cfg.m, cfg.n)
+    bufs["a2"], v2 = alloc(cfg.m, cfg.n)
+    # CdTensor3 keeps views of the (pinned) buffers (no copy): generate in place
+    a = qt.CdTensor3(cfg.m, cfg.n, cfg.p, v1, v2)
     assert a.t1.ctypes.data == bufs["a1"].data_ptr()
     qt.gen_tensor(cfg.m, cfg.n, cfg.p, sa, cfg.dist_a, cfg.scale_a, out=a)
-    qt.gen_tensor(cfg.n, cfg.s, cfg.p, sb, cfg.dist_b, cfg.scale_b, out=b)
+    b = None
+    if need_b:
+        bufs["b1"], w1 = alloc(cfg.n, cfg.s)
+        bufs["b2"], w2 = alloc(cfg.n, cfg.s)
+        b = qt.CdTensor3(cfg.n, cfg.s, cfg.p, w1, w2)
+        qt.gen_tensor(cfg.n, cfg.s, cfg.p, sb, cfg.dist_b, cfg.scale_b, out=b)
     return a, b, bufs
 
 
@@ -261,7 +265,9 @@ def run_ours(args, cfg):
 
     lo, hi = shard.row_slab(cfg.m, world, rank)
     rows = hi - lo
-    a, b, _ = host_inputs(cfg, pinned=True)
+    # N = 1: pinned host inputs (the e2e leg copies from them); N > 1: every
+    # rank regenerates A (sequential generator) and keeps its slab, rank 0 owns B
+    a, b, _ = host_inputs(cfg, pinned=(world == 1), need_b=(world == 1 or rank == 0))
     l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     big = (cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s)) > 2 * 126e6
     if world == 1:
@@ -283,14 +289,25 @@ def run_ours(args, cfg):
         from paper_2212_14318_b200.distributed import RowShardedTProduct
         sharded = RowShardedTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
         sharded.load_a(a.t1, a.t2)
+        # pinned host copies for the e2e leg: this rank's A slab (+ B chunks on rank 0)
+        pin_a = torch.empty(sharded.a.shape, dtype=torch.float64, pin_memory=True)
+        pin_a.copy_(sharded.a)
+        pin_b = []
         if rank == 0:
             sharded.load_b(b.t1, b.t2)
+            for t in sharded.bc:
+                pb = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+                pb.copy_(t)
+                pin_b.append(pb)
+        del a, b
         da1, da2 = sharded.a[0], sharded.a[1]
-        db1, db2 = sharded.bc[0][0], sharded.bc[0][1]
         dc1, dc2 = sharded.c[0], sharded.c[1]
 
+        def bcast(t):
+            return dist.broadcast(t, 0, async_op=True)
+
         def step():
-            sharded.step(broadcast=lambda t: dist.broadcast(t, 0, async_op=True))
+            sharded.step(broadcast=bcast)
 
     # clocks are sampled from the first warm-up step through the per-kernel
     # timing loops, so short steps still yield samples under load
@@ -314,6 +331,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     launches = L.qt_kernel_launches() - launches0
     if world > 1:
+        tl = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(tl)  # every rank's kernels
+        launches = int(tl.item())
         dist.barrier()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
     if world > 1:
@@ -324,12 +344,13 @@ def run_ours(args, cfg):
 
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
     # (full-B stage kernels; with N > 1 ranks the rank-0-shaped K2 on its slab)
-    if world > 1:
-        db1 = torch.empty((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
-        db2 = torch.empty_like(db1)
+    if world > 1:  # full B for the stage kernels: assemble rank 0's chunks (zeros elsewhere)
+        db1 = torch.zeros((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
+        db2 = torch.zeros_like(db1)
         if rank == 0:
-            db1.copy_(torch.from_numpy(b.t1.view(np.float64)))
-            db2.copy_(torch.from_numpy(b.t2.view(np.float64)))
+            for (c0, c1_), t in zip(sharded.chunks, sharded.bc):
+                db1[:, :, 2 * c0:2 * c1_].copy_(t[0])
+                db2[:, :, 2 * c0:2 * c1_].copy_(t[1])
     ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
     bh = torch.empty((2, cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
     qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
@@ -392,7 +413,7 @@ def run_ours(args, cfg):
         "K3_ifft_C": {"ms": ifft_ms, "GB_s": ifft_gbs, "frac_hbm": ifft_gbs / peaks["hbm_gbs"]},
     }
 
-    # ---- end to end through the host-buffer C-ABI call ----
+    # ---- end to end: host buffers in, host buffers out, copies inside the timed region ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
         c1p = torch.empty((cfg.p, cfg.m, 2 * cfg.s), dtype=torch.float64, pin_memory=True)
@@ -413,6 +434,30 @@ def run_ours(args, cfg):
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
                "api": "qt_tprod_f64_host (pinned host buffers)"}
+    elif world > 1 and args.e2e_steps > 0:
+        pin_c = torch.empty(sharded.c.shape, dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():  # per rank: A slab (+ B on rank 0) H2D, broadcast + pipeline, C slab D2H
+            sharded.a.copy_(pin_a, non_blocking=True)
+            for t, pb in zip(sharded.bc, pin_b):
+                t.copy_(pb, non_blocking=True)
+            sharded.step(broadcast=bcast)
+            pin_c.copy_(sharded.c, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        t = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
+               "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
+               "api": "per rank: pinned A slab (+ B on rank 0) H2D, chunked NCCL broadcast, "
+                      "qt_* device pipeline, pinned C slab D2H; max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
