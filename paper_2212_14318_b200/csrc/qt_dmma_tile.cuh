@@ -12,10 +12,11 @@ namespace {
 
 // Tile configuration.  Warps are laid out WM x WN; a warp owns RB 8-row blocks
 // x one 8-column block of the tile, for all 8 (or 4, SELF) real components.
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int RB_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int RB_, int STAGES_, int MINB_, int GAUSS_ = 0>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, RB = RB_, STAGES = STAGES_;
   static constexpr int MINB = MINB_;
+  static constexpr bool GAUSS = GAUSS_ != 0;  // 3-multiplication complex products (qt_gemm.cu)
   static constexpr int NTHREADS = 32 * WM * WN;
   // smem tile geometry (double2 units); XOR swizzles make every fragment load
   // a conflict-free LDS.128 without padding:
@@ -29,6 +30,10 @@ struct TileCfg {
   static_assert(BK % 8 == 0 && BN % 8 == 0, "swizzles need BK, BN multiples of 8");
 };
 using BigCfg = TileCfg<64, 16, 8, 4, 2, 2, 2, 2>;     // 256 threads, 80 KB smem
+// Gauss 3M variant: 12 accumulator sets per 8x8 block need ~170 registers, so
+// 4 warps (32 x 16 tile) and 3 CTAs per SM; 3-deep cp.async ring (72 KB)
+using GaussCfg = TileCfg<32, 16, 8, 2, 2, 2, 3, 3, 1>;
+using SmallGaussCfg = TileCfg<16, 16, 16, 2, 2, 1, 2, 4, 1>;
 using SmallCfg = TileCfg<16, 16, 16, 2, 2, 1, 2, 4>;  // 128 threads, 64 KB smem
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "qt_dmma_tile.cuh"
@@ -72,6 +73,146 @@ __device__ __forceinline__ void pair_tile(const PairArgs& P, int row0, int col0,
   }
   cp_async_wait<0>();
   store_tile<C, SELF>(P, acc, row0, col0, m, s, ldc, wm, wn, g, q);
+}
+
+// ---------------------------------------------------------------------------
+// Gauss's 3-multiplication complex product on the DMMA pipe.  For a term
+// s * op(X) * Y with op(X) = xr + i*sig*xi (sig = -1 for conj) and Y = yr + i*yi:
+//     T1 += s*xr*yr,  T2 += s*(sig*xi)*yi,  T3 += s*(xr + sig*xi)*(yr + yi)
+// and at the end  Re = T1 - T2,  Im = T3 - T1 - T2.  Both complex products of
+// every output (e.g. C1_k = Â1_k B̂1_k - conj(Â2_σ) B̂2_k) accumulate into the
+// same three sums, so each output costs 6 DMMAs per K-step instead of 8: 24
+// instead of 32 per frequency pair and 8-row block.  The operand sums
+// (xr +- xi, yr + yi) are 12 DADDs per 24 DMMAs on the shared FP64 pipe.  The
+// flop count the metric uses stays the reference's (32 m n s p); the kernel
+// executes 24 m n s p (+ the DADDs).
+template <class C, bool SELF>
+__device__ __forceinline__ void mma_stage_3m(const double2* sa, const double2* sb,
+                                             double (&T)[SELF ? 6 : 12][C::RB][2], int wm, int wn, int g, int q) {
+#pragma unroll
+  for (int ks = 0; ks < C::BK / 4; ++ks) {
+    const int kb = ks * 4 + q;
+    const int jb = (wn * 8 + g) ^ (q << 1);
+    double br[4], bi[4], bp[4];
+#pragma unroll
+    for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
+      const double2 v = sb[pl * C::B_PLANE + kb * C::BN + jb];
+      br[pl] = v.x;
+      bi[pl] = v.y;
+      bp[pl] = v.x + v.y;
+    }
+    // planes: 0 B1k, 1 B2k, 2 B1s, 3 B2s
+    const double nb2k_r = dneg(br[1]), nb2k_i = dneg(bi[1]), nb2k_p = dneg(bp[1]);
+#pragma unroll
+    for (int rb = 0; rb < C::RB; ++rb) {
+      const int i = wm * (C::RB * 8) + rb * 8 + g;
+      const int ca = (ks * 4 + q) ^ ((i & 1) << 2);
+      double ar[4], ai[4], ap[4], am[4];  // planes: 0 A1k, 1 A2k, 2 A1s, 3 A2s
+#pragma unroll
+      for (int pl = 0; pl < (SELF ? 2 : 4); ++pl) {
+        const double2 v = sa[pl * C::A_PLANE + i * C::BK + ca];
+        ar[pl] = v.x;
+        ai[pl] = v.y;
+        ap[pl] = v.x + v.y;
+        am[pl] = v.x - v.y;
+      }
+      if (SELF) {
+        ar[2] = ar[0]; ai[2] = ai[0]; ap[2] = ap[0]; am[2] = am[0];
+        ar[3] = ar[1]; ai[3] = ai[1]; ap[3] = ap[1]; am[3] = am[1];
+      }
+      // C1_k = A1k B1k - conj(A2s) B2k        (T sets 0..2)
+      dmma(T[0][rb], ar[0], br[0]);
+      dmma(T[0][rb], ar[3], nb2k_r);
+      dmma(T[1][rb], ai[0], bi[0]);
+      dmma(T[1][rb], ai[3], bi[1]);
+      dmma(T[2][rb], ap[0], bp[0]);
+      dmma(T[2][rb], am[3], nb2k_p);
+      // C2_k = conj(A1s) B2k + A2k B1k       (T sets 3..5)
+      dmma(T[3][rb], ar[2], br[1]);
+      dmma(T[3][rb], ar[1], br[0]);
+      dmma(T[4][rb], ai[2], nb2k_i);
+      dmma(T[4][rb], ai[1], bi[0]);
+      dmma(T[5][rb], am[2], bp[1]);
+      dmma(T[5][rb], ap[1], bp[0]);
+      if (!SELF) {
+        constexpr int NT = SELF ? 6 : 12;
+        const double nb2s_r = dneg(br[3]), nb2s_i = dneg(bi[3]), nb2s_p = dneg(bp[3]);
+        // C1_s = A1s B1s - conj(A2k) B2s     (T sets 6..8)
+        dmma(T[6 % NT][rb], ar[2], br[2]);
+        dmma(T[6 % NT][rb], ar[1], nb2s_r);
+        dmma(T[7 % NT][rb], ai[2], bi[2]);
+        dmma(T[7 % NT][rb], ai[1], bi[3]);
+        dmma(T[8 % NT][rb], ap[2], bp[2]);
+        dmma(T[8 % NT][rb], am[1], nb2s_p);
+        // C2_s = conj(A1k) B2s + A2s B1s     (T sets 9..11)
+        dmma(T[9 % NT][rb], ar[0], br[3]);
+        dmma(T[9 % NT][rb], ar[3], br[2]);
+        dmma(T[10 % NT][rb], ai[0], nb2s_i);
+        dmma(T[10 % NT][rb], ai[3], bi[2]);
+        dmma(T[11 % NT][rb], am[0], bp[3]);
+        dmma(T[11 % NT][rb], ap[3], bp[2]);
+      }
+    }
+  }
+}
+
+// epilogue of the 3M variant: Re = T1 - T2, Im = T3 - T1 - T2 per output
+template <class C, bool SELF>
+__device__ __forceinline__ void store_tile_3m(const PairArgs& P, const double (&T)[SELF ? 6 : 12][C::RB][2],
+                                              int row0, int col0, int m, int s, int ldc, int wm, int wn, int g,
+                                              int q) {
+  constexpr int NT = SELF ? 6 : 12;
+  const int col = col0 + wn * 8 + 2 * q;
+#pragma unroll
+  for (int o = 0; o < (SELF ? 2 : 4); ++o) {
+    double2* Cp = P.c[o];  // outputs in P.c order: C1_k, C2_k, C1_s, C2_s
+#pragma unroll
+    for (int rb = 0; rb < C::RB; ++rb) {
+      const int row = row0 + wm * (C::RB * 8) + rb * 8 + g;
+      if (row < m) {
+        double2* dst = Cp + (size_t)row * ldc + col;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double t1 = T[(3 * o) % NT][rb][e], t2 = T[(3 * o + 1) % NT][rb][e], t3 = T[(3 * o + 2) % NT][rb][e];
+          if (col + e < s) dst[e] = make_double2(t1 - t2, t3 - t1 - t2);
+        }
+      }
+    }
+  }
+}
+
+template <class C, bool SELF>
+__device__ __forceinline__ void pair_tile_3m(const PairArgs& P, int row0, int col0, int m, int n, int s, int ldb,
+                                             int ldc) {
+  extern __shared__ double2 smem[];
+  constexpr int NT = SELF ? 6 : 12;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  double T[NT][C::RB][2];
+#pragma unroll
+  for (int c = 0; c < NT; ++c)
+#pragma unroll
+    for (int rb = 0; rb < C::RB; ++rb) T[c][rb][0] = T[c][rb][1] = 0.0;
+  const int ktiles = (n + C::BK - 1) / C::BK;
+#pragma unroll
+  for (int st = 0; st < C::STAGES - 1; ++st) {
+    if (st < ktiles) load_stage<C, SELF>(smem + st * C::STAGE_ELEMS, P, st, row0, col0, m, n, s, ldb);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + C::STAGES - 1;
+      if (nk < ktiles) load_stage<C, SELF>(smem + (nk % C::STAGES) * C::STAGE_ELEMS, P, nk, row0, col0, m, n, s, ldb);
+      cp_async_commit();
+    }
+    const double2* sa = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
+    mma_stage_3m<C, SELF>(sa, sa + 4 * C::A_PLANE, T, wm, wn, g, q);
+  }
+  cp_async_wait<0>();
+  store_tile_3m<C, SELF>(P, T, row0, col0, m, s, ldc, wm, wn, g, q);
 }
 
 __device__ __forceinline__ PairArgs pair_args(const double2* ah1, const double2* ah2, const double2* bh1,
@@ -137,14 +278,24 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    double acc[8][C::RB][2];
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int rb = 0; rb < C::RB; ++rb) acc[c][rb][0] = acc[c][rb][1] = 0.0;
     const double2* sa = smem + (it & 1) * C::STAGE_ELEMS;
-    mma_stage<C, false>(sa, sa + 4 * C::A_PLANE, acc, wm, wn, g, q);
-    store_tile<C, false>(P, acc, r0, c0, m, s, ldc, wm, wn, g, q);
+    if constexpr (C::GAUSS) {
+      double T[12][C::RB][2];
+#pragma unroll
+      for (int c = 0; c < 12; ++c)
+#pragma unroll
+        for (int rb = 0; rb < C::RB; ++rb) T[c][rb][0] = T[c][rb][1] = 0.0;
+      mma_stage_3m<C, false>(sa, sa + 4 * C::A_PLANE, T, wm, wn, g, q);
+      store_tile_3m<C, false>(P, T, r0, c0, m, s, ldc, wm, wn, g, q);
+    } else {
+      double acc[8][C::RB][2];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int rb = 0; rb < C::RB; ++rb) acc[c][rb][0] = acc[c][rb][1] = 0.0;
+      mma_stage<C, false>(sa, sa + 4 * C::A_PLANE, acc, wm, wn, g, q);
+      store_tile<C, false>(P, acc, r0, c0, m, s, ldc, wm, wn, g, q);
+    }
     __syncthreads();  // buffer (it & 1) is refilled by the next iteration's prefetch
     if (wn_ < items) {
       P = item_args(wn_, &r0, &c0);
@@ -179,8 +330,13 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
   const size_t amn = (size_t)m * n, bns = (size_t)bslice, cms = (size_t)cslice;
   const PairArgs P = pair_args(ah1, ah2, bh1, bh2, ch1, ch2, k, sg, amn, bns, cms);
   const int row0 = tm * C::BM, col0 = tn * C::BN;
-  if (sg == k) pair_tile<C, true>(P, row0, col0, m, n, s, ldb, ldc);
-  else pair_tile<C, false>(P, row0, col0, m, n, s, ldb, ldc);
+  if constexpr (C::GAUSS) {
+    if (sg == k) pair_tile_3m<C, true>(P, row0, col0, m, n, s, ldb, ldc);
+    else pair_tile_3m<C, false>(P, row0, col0, m, n, s, ldb, ldc);
+  } else {
+    if (sg == k) pair_tile<C, true>(P, row0, col0, m, n, s, ldb, ldc);
+    else pair_tile<C, false>(P, row0, col0, m, n, s, ldb, ldc);
+  }
 }
 
 template <class C>
@@ -213,11 +369,22 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
   return cudaSuccess;
 }
 
+// Every tile shape uses the same complex-product algorithm, so each element of
+// C is computed with the same arithmetic whatever m, s or the sharding: Gauss
+// 3M by default; $QTB_GEMM=4m selects the 4-multiplication kernels everywhere.
+bool gauss_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("QTB_GEMM");
+    return !(e && (e[0] == '4'));
+  }();
+  return on;
+}
+
+template <class C>
 cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                     cudaStream_t stream) {
-  using C = SmallCfg;
   auto kern = paired_small_persistent_kernel<C>;
   const size_t smem = 2 * (size_t)C::STAGE_ELEMS * 16;
   static std::once_flag once;
@@ -249,11 +416,19 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
   if (m == 0 || s == 0 || p == 0) return cudaSuccess;
   // Small slices (m, s <= 32): the 64-row tile would waste >= half its DMMAs
   // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
+  const bool gauss = gauss_enabled();
   if (m <= 32 && s <= 32) {
     if (n <= (uint64_t)SmallCfg::BK)
-      return launch_small_persistent(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
-    return launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
+      return gauss ? launch_small_persistent<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc,
+                                                            bslice, cslice, stream)
+                   : launch_small_persistent<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice,
+                                                       cslice, stream);
+    return gauss ? launch_cfg<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice,
+                                             stream)
+                 : launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
   }
+  if (gauss)
+    return launch_cfg<GaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
   return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
 }
 
