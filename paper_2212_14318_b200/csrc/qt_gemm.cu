@@ -120,36 +120,38 @@ __device__ __forceinline__ void mma_stage_3m(const double2* sa, const double2* s
         ar[2] = ar[0]; ai[2] = ai[0]; ap[2] = ap[0]; am[2] = am[0];
         ar[3] = ar[1]; ai[3] = ai[1]; ap[3] = ap[1]; am[3] = am[1];
       }
-      // C1_k = A1k B1k - conj(A2s) B2k        (T sets 0..2)
+      // Term order per T set is fixed (first product, then second), but the
+      // 12 independent sets are interleaved so consecutive DMMAs never depend
+      // on each other.  Sets: C1_k = A1k B1k - conj(A2s) B2k (0..2),
+      // C2_k = conj(A1s) B2k + A2k B1k (3..5), C1_s = A1s B1s - conj(A2k) B2s
+      // (6..8), C2_s = conj(A1k) B2s + A2s B1s (9..11); each (T1, T2, T3).
+      constexpr int NT = SELF ? 6 : 12;
       dmma(T[0][rb], ar[0], br[0]);
-      dmma(T[0][rb], ar[3], nb2k_r);
       dmma(T[1][rb], ai[0], bi[0]);
-      dmma(T[1][rb], ai[3], bi[1]);
       dmma(T[2][rb], ap[0], bp[0]);
-      dmma(T[2][rb], am[3], nb2k_p);
-      // C2_k = conj(A1s) B2k + A2k B1k       (T sets 3..5)
       dmma(T[3][rb], ar[2], br[1]);
-      dmma(T[3][rb], ar[1], br[0]);
       dmma(T[4][rb], ai[2], nb2k_i);
-      dmma(T[4][rb], ai[1], bi[0]);
       dmma(T[5][rb], am[2], bp[1]);
+      if (!SELF) {
+        dmma(T[6 % NT][rb], ar[2], br[2]);
+        dmma(T[7 % NT][rb], ai[2], bi[2]);
+        dmma(T[8 % NT][rb], ap[2], bp[2]);
+        dmma(T[9 % NT][rb], ar[0], br[3]);
+        dmma(T[10 % NT][rb], ai[0], dneg(bi[3]));
+        dmma(T[11 % NT][rb], am[0], bp[3]);
+      }
+      dmma(T[0][rb], ar[3], nb2k_r);
+      dmma(T[1][rb], ai[3], bi[1]);
+      dmma(T[2][rb], am[3], nb2k_p);
+      dmma(T[3][rb], ar[1], br[0]);
+      dmma(T[4][rb], ai[1], bi[0]);
       dmma(T[5][rb], ap[1], bp[0]);
       if (!SELF) {
-        constexpr int NT = SELF ? 6 : 12;
-        const double nb2s_r = dneg(br[3]), nb2s_i = dneg(bi[3]), nb2s_p = dneg(bp[3]);
-        // C1_s = A1s B1s - conj(A2k) B2s     (T sets 6..8)
-        dmma(T[6 % NT][rb], ar[2], br[2]);
-        dmma(T[6 % NT][rb], ar[1], nb2s_r);
-        dmma(T[7 % NT][rb], ai[2], bi[2]);
+        dmma(T[6 % NT][rb], ar[1], dneg(br[3]));
         dmma(T[7 % NT][rb], ai[1], bi[3]);
-        dmma(T[8 % NT][rb], ap[2], bp[2]);
-        dmma(T[8 % NT][rb], am[1], nb2s_p);
-        // C2_s = conj(A1k) B2s + A2s B1s     (T sets 9..11)
-        dmma(T[9 % NT][rb], ar[0], br[3]);
+        dmma(T[8 % NT][rb], am[1], dneg(bp[3]));
         dmma(T[9 % NT][rb], ar[3], br[2]);
-        dmma(T[10 % NT][rb], ai[0], nb2s_i);
         dmma(T[10 % NT][rb], ai[3], bi[2]);
-        dmma(T[11 % NT][rb], am[0], bp[3]);
         dmma(T[11 % NT][rb], ap[3], bp[2]);
       }
     }
