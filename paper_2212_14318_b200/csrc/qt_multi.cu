@@ -13,13 +13,15 @@
 //   * one inverse transform (K3) per slab, then the slab goes back to the host.
 // Every element is computed with the same kernels and arithmetic as the
 // single-GPU path, so the result is bitwise identical for every G (and equal to
-// qt_tprod_f64_host).  NCCL is resolved at run time with dlopen("libnccl.so.2")
-// so the library does not pin an NCCL build (torch bundles its own).
+// qt_tprod_f64_host).  NCCL is resolved at run time (dlopen) so the library
+// does not pin an NCCL build: an NCCL the process already loaded (torch's) is
+// reused first, then $QTB_NCCL_LIB, then the loader's libnccl.so.2.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -43,9 +45,20 @@ NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
   std::call_once(once, [] {
+    // 1) an NCCL the process already loaded (e.g. torch's bundled build) — a
+    //    second libnccl.so.2 would shadow it by soname and break its users;
+    // 2) $QTB_NCCL_LIB; 3) the loader's libnccl.so.2.
     for (const char* nm : {"libnccl.so.2", "libnccl.so"}) {
-      api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      api.h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD);
       if (api.h) break;
+    }
+    if (!api.h) {
+      const char* env = getenv("QTB_NCCL_LIB");
+      if (env && *env) api.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    }
+    for (const char* nm : {"libnccl.so.2", "libnccl.so"}) {
+      if (api.h) break;
+      api.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
     }
     if (!api.h) return;
     api.CommInitAll = (decltype(api.CommInitAll))dlsym(api.h, "ncclCommInitAll");

@@ -151,6 +151,10 @@ def tprod_naive(a: CdTensor3, b: CdTensor3, device=None) -> CdTensor3:
 
 def tprod_fast_multi(a: CdTensor3, b: CdTensor3, devices) -> CdTensor3:
     """Row-sharded single-process multi-GPU T-product (B broadcast over NCCL)."""
+    try:  # load torch's bundled NCCL first: the C library reuses an already-loaded libnccl.so.2
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     if a.n != b.m or a.p != b.p:
         raise ValueError("tprod_fast: dimension mismatch")
     m, n, s, p = a.m, a.n, b.n, a.p

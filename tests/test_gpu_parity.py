@@ -16,6 +16,7 @@ from conftest import RefRng
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
+ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 
 
 def as_pair(t):
@@ -317,3 +318,17 @@ def test_gpu_naive_equals_fast_full_config3():
     fast = qt.tprod_fast(a, b)
     naive = qt.tprod_naive(a, b)
     assert O.rel_frob_error(as_pair(fast), as_pair(naive)) <= 1e-12
+
+
+def test_multi_driver_before_torch_import_keeps_torch_importable():
+    """The C driver must not load a second libnccl.so.2 that shadows torch's
+    (regression: system NCCL 2.27 loaded first broke `import torch`)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2212_14318_b200 as qt\n"
+            "a = qt.gen_random_tensor(8, 4, 4, 1); b = qt.gen_random_tensor(4, 4, 4, 2)\n"
+            "c = qt.tprod_fast_multi(a, b, [0])\n"
+            "import torch; assert torch.cuda.is_available(); print('ok')\n") % ROOT_DIR
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
