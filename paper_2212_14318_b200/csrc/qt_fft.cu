@@ -230,7 +230,7 @@ __device__ __forceinline__ void stage_first_global(const TubeJob& job, const Fft
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = g * G.ig + (j + r * pR) * G.is;
-      v[r] = ok ? __ldg(&in[(uint64_t)row * job.ntubes + t]) : make_double2(0.0, 0.0);
+      v[r] = ok ? __ldcs(&in[(uint64_t)row * job.ntubes + t]) : make_double2(0.0, 0.0);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
@@ -280,7 +280,7 @@ __device__ __forceinline__ void stage_only_global(const TubeJob& job, const FftG
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      v[r] = __ldg(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
+      v[r] = __ldcs(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
     const double2* __restrict__ in = job.in + t0;
     double2* __restrict__ out = job.out + t0;
     for (int t = threadIdx.x; t < tcount; t += blockDim.x) {
-      double2 v = __ldg(&in[(uint64_t)(g * G.ig) * job.ntubes + t]);
+      double2 v = __ldcs(&in[(uint64_t)(g * G.ig) * job.ntubes + t]);
       if (job.conj_in) v.y = -v.y;
       store_out(out, job, G, tw, g, 0, t, v);
     }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
     for (int idx = threadIdx.x; idx < (L << logT); idx += blockDim.x) {
       const int r = idx >> logT, t = idx & (T - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (t < tcount) v = __ldg(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
+      if (t < tcount) v = __ldcs(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
       if (job.conj_in) v.y = -v.y;
       cbuf[idx] = v;
     }
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom
     const bool ok = t < tcount;
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
-      v[r] = ok ? __ldg(&in[(uint64_t)(j + r * P0) * istr + t]) : make_double2(0.0, 0.0);
+      v[r] = ok ? __ldcs(&in[(uint64_t)(j + r * P0) * istr + t]) : make_double2(0.0, 0.0);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R0>(v);
