@@ -48,24 +48,32 @@ int cuda_fail(cudaError_t e, const char* where) {
 int current_device(int* dev) {
   cudaError_t e = cudaGetDevice(dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  int major = 0, minor = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, *dev);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, *dev);
-  if (major != 10 || minor != 0)
-    return fail(QT_ENODEV, "device %d is sm_%d%d; this library is built for sm_100a only", *dev, major, minor);
-  // Keep freed workspace in the device's stream-ordered pool across syncs: the
-  // default release threshold (0) would unmap it at every synchronize and make
-  // the next call pay for fresh page mappings.
+  // Per-device one-time checks, cached: (1) sm_100 only; (2) keep freed
+  // workspace in the device's stream-ordered pool across syncs — the default
+  // release threshold (0) would unmap it at every synchronize and make the next
+  // call pay for fresh page mappings.
   static std::mutex mu;
-  static bool pool_set[64] = {};
-  std::lock_guard<std::mutex> lk(mu);
-  if (*dev >= 0 && *dev < 64 && !pool_set[*dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, *dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  static int state[64] = {};  // 0 unchecked, 1 ok, 2 wrong arch
+  static int arch[64] = {};
+  const int d = *dev;
+  if (d >= 0 && d < 64) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (state[d] == 0) {
+      int major = 0, minor = 0;
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, d);
+      arch[d] = major * 10 + minor;
+      state[d] = (major == 10 && minor == 0) ? 1 : 2;
+      if (state[d] == 1) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+          uint64_t thr = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+      }
     }
-    pool_set[*dev] = true;
+    if (state[d] == 2)
+      return fail(QT_ENODEV, "device %d is sm_%d; this library is built for sm_100a only", d, arch[d]);
   }
   return QT_OK;
 }
@@ -165,21 +173,32 @@ int transform_device_impl(bool inverse, const double* x1, const double* x2, doub
 }
 
 // RAII device buffer + stream for the host-buffer entry points.
+// Per-thread, per-device non-blocking stream for the host-buffer entry
+// points (created once: stream creation costs more than a small T-product).
+cudaStream_t thread_stream(int device) {
+  thread_local cudaStream_t streams[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  return streams[device];
+}
+
+// Device switch + stream for the host-buffer entry points (restores the
+// caller's device on exit).
 struct HostCall {
   cudaStream_t st = nullptr;
   int prev = -1;
   ~HostCall() {
-    if (st) cudaStreamDestroy(st);
     if (prev >= 0) cudaSetDevice(prev);
   }
   int begin(int device) {
     cudaError_t e = cudaGetDevice(&prev);
     if (e != cudaSuccess) { prev = -1; return cuda_fail(e, "cudaGetDevice"); }
-    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    if (device != prev && (e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     int dev = 0;
     int rc = current_device(&dev);
     if (rc) return rc;
-    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+    st = thread_stream(dev);
+    if (!st) return fail(QT_ECUDA, "cannot create a stream on device %d", dev);
     return QT_OK;
   }
 };
