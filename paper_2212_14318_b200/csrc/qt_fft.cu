@@ -515,10 +515,10 @@ cudaError_t launch_fft2(const TubeBatch& batch, const FftGeom& G, const double2*
   while (logT > 0 && (uint64_t(1) << (logT - 1)) >= maxtubes) --logT;           // tiny jobs
   while (logT > 3 && (maxtubes >> logT) * (uint64_t)njobs * groups < 296) --logT;  // >= 2 CTAs/SM
   const size_t smem = sizeof(double2) * ((size_t)L << logT);
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(tube_fft2_kernel<R0, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+  static std::mutex mu;
+  static uint64_t done = 0;
+  cudaError_t attr = once_per_device(mu, done, [] {
+    return cudaFuncSetAttribute(tube_fft2_kernel<R0, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
   });
   if (attr != cudaSuccess) return attr;
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;

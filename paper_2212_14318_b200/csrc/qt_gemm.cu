@@ -345,11 +345,11 @@ template <class C>
 cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2, double2* ch1,
                        double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc,
                        uint64_t bslice, uint64_t cslice, cudaStream_t stream) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(paired_spectral_gemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)C::SMEM_BYTES);
+  static std::mutex mu;
+  static uint64_t done = 0;
+  const cudaError_t attr_err = once_per_device(mu, done, [] {
+    return cudaFuncSetAttribute(paired_spectral_gemm_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
   const uint64_t npairs = p / 2 + 1;
@@ -389,16 +389,16 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
                                     cudaStream_t stream) {
   auto kern = paired_small_persistent_kernel<C>;
   const size_t smem = 2 * (size_t)C::STAGE_ELEMS * 16;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int per_sm = 1, sms = 148;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NTHREADS, smem);
+  static std::mutex mu;
+  static uint64_t done = 0;
+  static int per_sm = 1, sms = 148;  // identical on every B200
+  const cudaError_t attr_err = once_per_device(mu, done, [&] {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NTHREADS, smem);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return e;
   });
   if (attr_err != cudaSuccess) return attr_err;
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);

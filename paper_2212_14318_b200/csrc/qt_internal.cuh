@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 namespace qtb {
@@ -85,6 +86,20 @@ int qt3_read_device(const char* path, double* t1, double* t2, uint64_t m, uint64
                     cudaStream_t stream, std::string* err);
 int qt3_write_device(const char* path, const double* t1, const double* t2, uint64_t m, uint64_t n, uint64_t p,
                      cudaStream_t stream, std::string* err);
+
+// Kernel attributes (e.g. the dynamic shared-memory opt-in) are per device:
+// run `fn` once for every device a launcher is used on (thread-safe).
+template <class F>
+cudaError_t once_per_device(std::mutex& mu, uint64_t& done_mask, F fn) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && ((done_mask >> dev) & 1ull)) return cudaSuccess;
+  e = fn();
+  if (e == cudaSuccess && dev < 64) done_mask |= 1ull << dev;
+  return e;
+}
 
 // Launch accounting (qt_kernel_launches).
 void count_launches(uint64_t k);

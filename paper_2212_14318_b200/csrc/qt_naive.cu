@@ -135,10 +135,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 template <class C>
 cudaError_t launch_naive_cfg(const double2* a1, const double2* a2, const double2* b1, const double2* b2, double2* c1,
                              double2* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, cudaStream_t stream) {
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(naive_tprod_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static std::mutex mu;
+  static uint64_t done = 0;
+  const cudaError_t attr = once_per_device(mu, done, [] {
+    return cudaFuncSetAttribute(naive_tprod_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)C::SMEM_BYTES);
   });
   if (attr != cudaSuccess) return attr;
