@@ -73,6 +73,8 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the N>1 row-sharded chunked-broadcast pipeline even on one GPU (no broadcast)")
     return ap.parse_args()
 
 
@@ -267,10 +269,11 @@ def run_ours(args, cfg):
     rows = hi - lo
     # N = 1: pinned host inputs (the e2e leg copies from them); N > 1: every
     # rank regenerates A (sequential generator) and keeps its slab, rank 0 owns B
-    a, b, _ = host_inputs(cfg, pinned=(world == 1), need_b=(world == 1 or rank == 0))
+    sharded_mode = world > 1 or args.sharded
+    a, b, _ = host_inputs(cfg, pinned=not sharded_mode, need_b=(world == 1 or rank == 0))
     l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     big = (cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s)) > 2 * 126e6
-    if world == 1:
+    if not sharded_mode:
         # device-resident inputs; one step = the product entry point qt_tprod_f64_device
         da1 = torch.from_numpy(a.t1.view(np.float64)).to(dev)
         da2 = torch.from_numpy(a.t2.view(np.float64)).to(dev)
@@ -305,6 +308,9 @@ def run_ours(args, cfg):
 
         def bcast(t):
             return dist.broadcast(t, 0, async_op=True)
+
+        if world == 1:
+            bcast = None
 
         def step():
             sharded.step(broadcast=bcast)
@@ -344,7 +350,7 @@ def run_ours(args, cfg):
 
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
     # (full-B stage kernels; with N > 1 ranks the rank-0-shaped K2 on its slab)
-    if world > 1:  # full B for the stage kernels: assemble rank 0's chunks (zeros elsewhere)
+    if sharded_mode:  # full B for the stage kernels: assemble rank 0's chunks (zeros elsewhere)
         db1 = torch.zeros((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
         db2 = torch.zeros_like(db1)
         if rank == 0:
@@ -422,7 +428,7 @@ def run_ours(args, cfg):
 
     # ---- end to end: host buffers in, host buffers out, copies inside the timed region ----
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if not sharded_mode and args.e2e_steps > 0:
         c1p = torch.empty((cfg.p, cfg.m, 2 * cfg.s), dtype=torch.float64, pin_memory=True)
         c2p = torch.empty_like(c1p, pin_memory=True)
 
@@ -441,7 +447,7 @@ def run_ours(args, cfg):
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
                "api": "qt_tprod_f64_host (pinned host buffers)"}
-    elif world > 1 and args.e2e_steps > 0:
+    elif sharded_mode and args.e2e_steps > 0:
         pin_c = torch.empty(sharded.c.shape, dtype=torch.float64, pin_memory=True)
 
         def e2e_step():  # per rank: A slab (+ B on rank 0) H2D, broadcast + pipeline, C slab D2H
@@ -453,12 +459,14 @@ def run_ours(args, cfg):
             torch.cuda.synchronize()
 
         e2e_step()
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
         t = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
         e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
@@ -467,7 +475,7 @@ def run_ours(args, cfg):
                       "qt_* device pipeline, pinned C slab D2H; max over ranks"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded_mode and not args.no_cpu_baseline:
         import oracle as O
         if O.ref_available():
             threads = os.cpu_count() or 1
@@ -482,7 +490,8 @@ def run_ours(args, cfg):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                       "parallelism": f"rows{world}" + ("+bcastB" if world > 1 else ""),
+                       "parallelism": f"rows{world}" + ("+bcastB(chunked)" if world > 1 else "")
+                       + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
                        "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
                        "flops_eff_per_step": cfg.flops_eff},
             "roofline": roof,
