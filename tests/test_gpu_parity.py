@@ -332,3 +332,33 @@ def test_multi_driver_before_torch_import_keeps_torch_importable():
             "import torch; assert torch.cuda.is_available(); print('ok')\n") % ROOT_DIR
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_concurrent_host_calls_are_reentrant_and_bitwise():
+    """the drop-in must be reentrant.  Several host threads call
+    tprod_fast at once (per-thread streams, stream-ordered workspace, shared
+    pinned arena and twiddle cache); each result equals its sequential twin."""
+    import threading
+    shapes = [(40, 24, 30, 16), (300, 64, 200, 32), (16, 16, 16, 4096), (5, 4, 3, 7), (260, 70, 130, 64),
+              (33, 17, 40, 12)]
+    ins = [(qt.gen_random_tensor(m, n, p, 10 + i), qt.gen_random_tensor(n, s, p, 20 + i))
+           for i, (m, n, s, p) in enumerate(shapes)]
+    want = [qt.tprod_fast(a, b) for a, b in ins]
+    got = [None] * len(ins)
+    errors = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = qt.tprod_fast(*ins[i])
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(ins))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for w, g in zip(want, got):
+        assert bits_equal(w.t1, g.t1) and bits_equal(w.t2, g.t2)
