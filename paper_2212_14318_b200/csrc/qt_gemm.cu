@@ -264,23 +264,35 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     *col0 = (t / ntm) * C::BN;
     return pair_args(ah1, ah2, bh1, bh2, ch1, ch2, k, (p - k) % p, amn, (size_t)bslice, (size_t)cslice);
   };
+  constexpr int D = C::STAGES;  // ring depth: items prefetched D - 1 ahead
+  const long long G = gridDim.x;
   long long w = blockIdx.x;
   if (w >= items) return;
-  int r0, c0;
-  PairArgs P = item_args(w, &r0, &c0);
-  load_stage<C, false>(smem, P, 0, r0, c0, m, n, s, ldb);
-  cp_async_commit();
-  for (int it = 0; w < items; ++it, w += gridDim.x) {
-    const long long wn_ = w + gridDim.x;
-    int nr0 = 0, nc0 = 0;
-    if (wn_ < items) {
-      const PairArgs Pn = item_args(wn_, &nr0, &nc0);
-      load_stage<C, false>(smem + ((it + 1) & 1) * C::STAGE_ELEMS, Pn, 0, nr0, nc0, m, n, s, ldb);
+#pragma unroll
+  for (int d = 0; d < D - 1; ++d) {
+    const long long wd = w + d * G;
+    if (wd < items) {
+      int lr, lc;
+      const PairArgs Pd = item_args(wd, &lr, &lc);
+      load_stage<C, false>(smem + d * C::STAGE_ELEMS, Pd, 0, lr, lc, m, n, s, ldb);
     }
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int it = 0; w < items; ++it, w += G) {
+    {
+      const long long wp = w + (D - 1) * G;
+      if (wp < items) {
+        int lr, lc;
+        const PairArgs Pp = item_args(wp, &lr, &lc);
+        load_stage<C, false>(smem + ((it + D - 1) % D) * C::STAGE_ELEMS, Pp, 0, lr, lc, m, n, s, ldb);
+      }
+      cp_async_commit();
+    }
+    cp_async_wait<D - 1>();
     __syncthreads();
-    const double2* sa = smem + (it & 1) * C::STAGE_ELEMS;
+    int r0, c0;
+    const PairArgs P = item_args(w, &r0, &c0);
+    const double2* sa = smem + (it % D) * C::STAGE_ELEMS;
     if constexpr (C::GAUSS) {
       double T[12][C::RB][2];
 #pragma unroll
@@ -298,10 +310,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
       mma_stage<C, false>(sa, sa + 4 * C::A_PLANE, acc, wm, wn, g, q);
       store_tile<C, false>(P, acc, r0, c0, m, s, ldc, wm, wn, g, q);
     }
-    __syncthreads();  // buffer (it & 1) is refilled by the next iteration's prefetch
-    if (wn_ < items) {
-      P = item_args(wn_, &r0, &c0);
-    }
+    __syncthreads();  // buffer (it % D) is refilled by a later iteration's prefetch
   }
   cp_async_wait<0>();
 }
@@ -388,7 +397,7 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                     cudaStream_t stream) {
   auto kern = paired_small_persistent_kernel<C>;
-  const size_t smem = 2 * (size_t)C::STAGE_ELEMS * 16;
+  const size_t smem = (size_t)C::STAGES * C::STAGE_ELEMS * 16;
   static std::mutex mu;
   static uint64_t done = 0;
   static int per_sm = 1, sms = 148;  // identical on every B200
