@@ -173,7 +173,6 @@ int transform_device_impl(bool inverse, const double* x1, const double* x2, doub
   return QT_OK;
 }
 
-// RAII device buffer + stream for the host-buffer entry points.
 // Per-thread, per-device non-blocking stream for the host-buffer entry
 // points (created once: stream creation costs more than a small T-product).
 cudaStream_t thread_stream(int device) {
