@@ -114,6 +114,25 @@ int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
                                       uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                       void* stream);
 
+/* Stage-2 algorithm for a product of this shape: QT_GEMM_DMMA (FP64 DMMA
+ * tensor cores, mma.sync m8n8k4) or QT_GEMM_INT8_EXACT (exact integer
+ * evaluation on the int8 tcgen05 tensor cores: 16 modular int8 GEMMs + CRT,
+ * fp64-accurate).  Depends on (n, s) only and on
+ * $QTB_OZAKI (0 never, 1 auto, 2 whenever n allows).  A caller that splits one
+ * product into row slabs or column chunks passes the full-shape choice to
+ * qt_spectral_product_f64_device_ld_algo so every piece uses the same
+ * arithmetic (bitwise-identical results). */
+#define QT_GEMM_AUTO (-1)
+#define QT_GEMM_DMMA 0
+#define QT_GEMM_INT8_EXACT 1
+int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p);
+int qt_spectral_product_f64_device_ld_algo(const double* ahat1, const double* ahat2,
+                                           const double* bhat1, const double* bhat2,
+                                           double* chat1, double* chat2,
+                                           uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                           uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
+                                           int algo, void* stream);
+
 /* Definitional product tprod_naive = fold(bcirc(A) . unfold(B))
  * (tproduct.hpp:23-25, tproduct.cpp:49-53) without materialising bcirc:
  * C_k = sum_r A_{(k-r) mod p} (.) B_r on FP64 DMMA.  16 m n s p^2 real

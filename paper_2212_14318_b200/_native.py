@@ -31,6 +31,8 @@ SIGNATURES = {
     "qt_qifft3_conj_f64_device": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),
     "qt_spectral_product_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_spectral_product_f64_device_ld": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [_vp]),
+    "qt_spectral_product_f64_device_ld_algo": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [ctypes.c_int, _vp]),
+    "qt_gemm_algo": (ctypes.c_int, [_u64] * 4),
     "qt_tprod_naive_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_tprod_naive_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),
     "qt_tprod_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),

@@ -441,6 +441,7 @@ static int tprod_host_tiled(const double* a1, const double* a2, const double* b1
     return QT_OK;
   };
   uint64_t unit = 0;
+  const int algo = choose_gemm_algo(n, s);  // one algorithm for every tile of the product
   auto compute_tile = [&](uint64_t i, uint64_t j) -> int {
     const int t = (int)(unit % 3);
     ++unit;
@@ -448,7 +449,7 @@ static int tprod_host_tiled(const double* a1, const double* a2, const double* b1
     const uint64_t rows = rows_of(i), cols = cols_of(j);
     if ((e = launch_spectral_gemm((const double2*)ah_slab(Ah1, i), (const double2*)ah_slab(Ah2, i),
                                   (const double2*)bh_chunk(Bh1, j), (const double2*)bh_chunk(Bh2, j),
-                                  (double2*)T[t][0], (double2*)T[t][1], rows, n, cols, p, scomp)) != cudaSuccess)
+                                  (double2*)T[t][0], (double2*)T[t][1], rows, n, cols, p, scomp, algo)) != cudaSuccess)
       return cuda_fail(e, "K2 paired spectral GEMM");
     TubeBatch ic{};
     add_inverse(ic, T[t][0], T[t][1], T[t][0], T[t][1], rows * cols, p);
@@ -496,20 +497,181 @@ static int tprod_host_tiled(const double* a1, const double* a2, const double* b1
   return cleanup(QT_OK);
 }
 
-int qt_spectral_product_f64_device_ld(const double* ah1, const double* ah2, const double* bh1, const double* bh2,
-                                      double* ch1, double* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                                      uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream) {
+// Host path for products that take the int8 (Ozaki) K2 (qt_ozaki.cu).  Its
+// residues of B̂ are the expensive, reusable half, so instead of (row x column)
+// tiles it streams ROW SLABS against a resident B':
+//   phase 1: B copied in (chunks on the copy-in stream), one K1, B' residues for
+//            every frequency (overlapping slab 0's upload);
+//   phase 2: per A row slab: copy-in -> K1 -> A' residues + int8 GEMMs + CRT ->
+//            K3 -> copy-out of the slab's rows, slabs double-buffered so the
+//            copy-in of slab i+1 and the copy-out of slab i-1 run under slab i.
+// Every element goes through the same exact integer product as the device
+// path, so the result is bitwise identical to it (finite inputs).
+static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const double* b1, const double* b2,
+                                  double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                  uint64_t R, HostCall& hc) {
+  const size_t cx = sizeof(double2);
+  const uint64_t NI = (m + R - 1) / R;
+  const size_t bpl = n * s * p * cx;       // B (and B̂) per plane
+  const size_t stA = R * n * p * cx;       // A slab per plane
+  const size_t stC = R * s * p * cx;       // C slab per plane
+  cudaError_t e;
+  int dev = 0;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&]() {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) evs.push_back(ev);
+    return ev;
+  };
+  char* d = nullptr;
+  OzakiB B;
+  auto a256 = [](size_t x) { return (x + 255) / 256 * 256; };
+  // B staging (2 planes) + B̂ (2) + A staging (2 x 2) + Â slab (2 x 2) + C slab (2 x 2) + flag
+  const size_t total = 2 * a256(bpl) * 2 + 4 * a256(stA) * 2 + 4 * a256(stC) + 256;
+  auto cleanup = [&](int code) {
+    for (cudaStream_t x : {sin, scomp, sout})
+      if (x) cudaStreamSynchronize(x);
+    if (B.res) ozaki_release(B, hc.st);
+    if (d) cudaFreeAsync(d, hc.st);
+    cudaError_t se = cudaStreamSynchronize(hc.st);
+    for (cudaStream_t x : {sin, scomp, sout})
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    if (!code && se != cudaSuccess) return cuda_fail(se, "tprod_fast (host) sync");
+    return code;
+  };
+  for (cudaStream_t* x : {&sin, &scomp, &sout})
+    if ((e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking)) != cudaSuccess) return cleanup(cuda_fail(e, "stream"));
+  if ((e = cudaMallocAsync((void**)&d, total, hc.st)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMallocAsync(host call)"));
+  {
+    cudaEvent_t ready = mkev();
+    cudaEventRecord(ready, hc.st);
+    for (cudaStream_t x : {sin, scomp, sout}) cudaStreamWaitEvent(x, ready, 0);
+  }
+  char* cur = d;
+  auto take = [&](size_t bytes) { char* r = cur; cur += a256(bytes); return (double*)r; };
+  double* Bs1 = take(bpl);
+  double* Bs2 = take(bpl);
+  double* Bh1 = take(bpl);
+  double* Bh2 = take(bpl);
+  double* SA[2][2] = {{take(stA), take(stA)}, {take(stA), take(stA)}};
+  double* AH[2][2] = {{take(stA), take(stA)}, {take(stA), take(stA)}};
+  double* CS[2][2] = {{take(stC), take(stC)}, {take(stC), take(stC)}};
+  int* flag = (int*)take(sizeof(int));
+  PhaseTrace tr(hc.st);
+
+  // phase 1: B in ~8 chunks per plane, then K1 and the B' residues
+  if ((e = cudaMemsetAsync(flag, 0, sizeof(int), scomp)) != cudaSuccess) return cleanup(cuda_fail(e, "memset"));
+  const size_t bchunk = std::max<size_t>(size_t(64) << 20, (bpl + 7) / 8);
+  for (int plane = 0; plane < 2; ++plane)
+    for (size_t off = 0; off < bpl; off += bchunk)
+      if ((e = cudaMemcpyAsync((char*)(plane ? Bs2 : Bs1) + off, (const char*)(plane ? b2 : b1) + off,
+                               std::min(bchunk, bpl - off), cudaMemcpyHostToDevice, sin)) != cudaSuccess)
+        return cleanup(cuda_fail(e, "H2D B"));
+  {
+    cudaEvent_t in = mkev();
+    cudaEventRecord(in, sin);
+    cudaStreamWaitEvent(scomp, in, 0);
+  }
+  tr.mark("B uploaded", sin);
+  {
+    TubeBatch fb{};
+    add_forward(fb, Bs1, Bs2, Bh1, Bh2, n * s);
+    if ((e = launch_tube_fft(fb, (int)p, scomp, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (B)"));
+  }
+  if ((e = ozaki_prepare_b((const double2*)Bh1, (const double2*)Bh2, R, n, s, p, s, n * s, flag, true, &B, scomp)) !=
+      cudaSuccess)
+    return cleanup(cuda_fail(e, "K2 B residues"));
+  tr.mark("B' residues ready", scomp);
+
+  // phase 2: A row slabs
+  cudaEvent_t sa_free[2] = {nullptr, nullptr}, cs_free[2] = {nullptr, nullptr};
+  for (uint64_t i = 0; i < NI; ++i) {
+    const int b = (int)(i & 1);
+    const uint64_t rows = std::min<uint64_t>(R, m - i * R);
+    if (sa_free[b]) cudaStreamWaitEvent(sin, sa_free[b], 0);
+    const size_t apitch = m * n * cx, awidth = rows * n * cx;
+    if ((e = cudaMemcpy2DAsync(SA[b][0], awidth, a1 + 2 * i * R * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)) ||
+        (e = cudaMemcpy2DAsync(SA[b][1], awidth, a2 + 2 * i * R * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)))
+      return cleanup(cuda_fail(e, "H2D A slab"));
+    cudaEvent_t in = mkev();
+    cudaEventRecord(in, sin);
+    cudaStreamWaitEvent(scomp, in, 0);
+    TubeBatch fb{};
+    add_forward(fb, SA[b][0], SA[b][1], AH[b][0], AH[b][1], rows * n);
+    if ((e = launch_tube_fft(fb, (int)p, scomp, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K1 tube FFT (A)"));
+    sa_free[b] = mkev();
+    cudaEventRecord(sa_free[b], scomp);
+    if (cs_free[b]) cudaStreamWaitEvent(scomp, cs_free[b], 0);
+    const double2 *ah1 = (const double2*)AH[b][0], *ah2 = (const double2*)AH[b][1];
+    double2 *cc1 = (double2*)CS[b][0], *cc2 = (double2*)CS[b][1];
+    if ((e = ozaki_multiply(B, ah1, ah2, (const double2*)Bh1, (const double2*)Bh2, rows, cc1, cc2, s, rows * s, flag,
+                            scomp)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "K2 int8 GEMM"));
+    // non-finite inputs: the fp64 DMMA kernels recompute the slab (no-op otherwise)
+    if ((e = dmma_spectral_gemm(ah1, ah2, (const double2*)Bh1, (const double2*)Bh2, cc1, cc2, rows, n, s, p, s, s,
+                                n * s, rows * s, scomp, flag)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "K2 fallback"));
+    TubeBatch ic{};
+    add_inverse(ic, CS[b][0], CS[b][1], CS[b][0], CS[b][1], rows * s, p);
+    if ((e = launch_tube_fft(ic, (int)p, scomp, dev)) != cudaSuccess) return cleanup(cuda_fail(e, "K3 inverse tube FFT"));
+    cudaEvent_t done = mkev();
+    cudaEventRecord(done, scomp);
+    cudaStreamWaitEvent(sout, done, 0);
+    const size_t cpitch = m * s * cx, cwidth = rows * s * cx;
+    if ((e = cudaMemcpy2DAsync(c1 + 2 * i * R * s, cpitch, CS[b][0], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)) ||
+        (e = cudaMemcpy2DAsync(c2 + 2 * i * R * s, cpitch, CS[b][1], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)))
+      return cleanup(cuda_fail(e, "D2H C slab"));
+    cs_free[b] = mkev();
+    cudaEventRecord(cs_free[b], sout);
+    tr.mark("slab " + std::to_string(i) + " computed", scomp);
+  }
+  tr.mark("all slabs downloaded", sout);
+  for (cudaStream_t x : {sin, scomp, sout}) {
+    cudaEvent_t fin = mkev();
+    cudaEventRecord(fin, x);
+    cudaStreamWaitEvent(hc.st, fin, 0);
+  }
+  tr.dump();
+  return cleanup(QT_OK);
+}
+
+int qt_spectral_product_f64_device_ld_algo(const double* ah1, const double* ah2, const double* bh1,
+                                           const double* bh2, double* ch1, double* ch2, uint64_t m, uint64_t n,
+                                           uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc, uint64_t bslice,
+                                           uint64_t cslice, int algo, void* stream) {
   t_err.clear();
   int rc = check_dims(m, n, s, p, "spectral_product");
   if (rc) return rc;
   if (ldb < s || ldc < s || bslice < n * ldb || cslice < m * ldc || ldb > kIntMax || ldc > kIntMax)
     return fail(QT_EINVAL, "spectral_product: leading dimensions smaller than the matrices");
+  if (algo != QT_GEMM_AUTO && algo != QT_GEMM_DMMA && algo != QT_GEMM_INT8_EXACT)
+    return fail(QT_EINVAL, "spectral_product: unknown algorithm");
+  if (algo == QT_GEMM_INT8_EXACT && (n % 32 != 0 || n > 8192))
+    return fail(QT_EINVAL, "spectral_product: the int8 path needs n % 32 == 0 and n <= 8192");
   int dev = 0;
   if ((rc = current_device(&dev))) return rc;
   cudaError_t e = launch_spectral_gemm_ld((const double2*)ah1, (const double2*)ah2, (const double2*)bh1,
                                           (const double2*)bh2, (double2*)ch1, (double2*)ch2, m, n, s, p, ldb, ldc,
-                                          bslice, cslice, (cudaStream_t)stream);
+                                          bslice, cslice, (cudaStream_t)stream, algo);
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "K2 paired spectral GEMM");
+}
+
+int qt_spectral_product_f64_device_ld(const double* ah1, const double* ah2, const double* bh1, const double* bh2,
+                                      double* ch1, double* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                      uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream) {
+  return qt_spectral_product_f64_device_ld_algo(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice,
+                                                QT_GEMM_AUTO, stream);
+}
+
+int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
+  (void)m;
+  (void)p;
+  return choose_gemm_algo(n, s);
 }
 
 static int tprod_host_impl(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
@@ -518,6 +680,12 @@ static int tprod_host_impl(const double* a1, const double* a2, const double* b1,
   const size_t ab = m * n * p * sizeof(double2), bb = n * s * p * sizeof(double2), cb = m * s * p * sizeof(double2);
   // Large problems stream (row slab x column chunk) tiles: ~8 slabs of >= 64
   // rows and ~8 chunks of >= 64 columns (a multiple of the GEMM tile).
+  // Products on the int8 K2 stream row slabs against resident B' residues.
+  if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20) && choose_gemm_algo(n, s) == kAlgoOzaki) {
+    uint64_t R = std::max<uint64_t>(64, (m + 7) / 8);
+    R = (R + 63) / 64 * 64;
+    return tprod_host_slabs_ozaki(a1, a2, b1, b2, c1, c2, m, n, s, p, R, hc);
+  }
   if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20)) {
     uint64_t R = std::max<uint64_t>(64, (m + 7) / 8);
     R = (R + 63) / 64 * 64;

@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_small_persistent_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                    const double2* __restrict__ bh1, const double2* __restrict__ bh2,
                                    double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
-                                   int ldb, int ldc, long long bslice, long long cslice) {
+                                   int ldb, int ldc, long long bslice, long long cslice, const int* only_if) {
+  if (only_if != nullptr && *only_if == 0) return;  // Ozaki path succeeded (qt_ozaki.cu)
   extern __shared__ double2 smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -327,7 +328,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_spectral_gemm_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                 const double2* __restrict__ bh1, const double2* __restrict__ bh2,
                                 double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
-                                int pair0, int ldb, int ldc, long long bslice, long long cslice) {
+                                int pair0, int ldb, int ldc, long long bslice, long long cslice, const int* only_if) {
+  if (only_if != nullptr && *only_if == 0) return;  // Ozaki path succeeded (qt_ozaki.cu)
   const int k = pair0 + blockIdx.y;
   const int sg = (p - k) % p;
   const int ntm = (m + C::BM - 1) / C::BM, ntn = (s + C::BN - 1) / C::BN;
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 template <class C>
 cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2, double2* ch1,
                        double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc,
-                       uint64_t bslice, uint64_t cslice, cudaStream_t stream) {
+                       uint64_t bslice, uint64_t cslice, cudaStream_t stream, const int* only_if = nullptr) {
   static std::mutex mu;
   static uint64_t done = 0;
   const cudaError_t attr_err = once_per_device(mu, done, [] {
@@ -372,7 +374,7 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
     dim3 grid((unsigned)tiles, chunk);
     paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(
         ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)k0, (int)ldb, (int)ldc, (long long)bslice,
-        (long long)cslice);
+        (long long)cslice, only_if);
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -395,7 +397,7 @@ template <class C>
 cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, const int* only_if = nullptr) {
   auto kern = paired_small_persistent_kernel<C>;
   const size_t smem = (size_t)C::STAGES * C::STAGE_ELEMS * 16;
   static std::mutex mu;
@@ -414,39 +416,67 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
   const uint64_t items = (p / 2 + 1) * tiles;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)std::max(1, per_sm) * sms);
   kern<<<(unsigned)grid, C::NTHREADS, smem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p,
-                                                       (int)ldb, (int)ldc, (long long)bslice, (long long)cslice);
+                                                       (int)ldb, (int)ldc, (long long)bslice, (long long)cslice,
+                                                       only_if);
   count_launches(1);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
-                                    double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                                    uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream) {
-  if (m == 0 || s == 0 || p == 0) return cudaSuccess;
+// DMMA (fp64 tensor-core) paired product; with only_if != nullptr every CTA
+// exits at once unless *only_if != 0 (the Ozaki path's non-finite fallback).
+cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                               double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                               uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
+                               const int* only_if) {
   // Small slices (m, s <= 32): the 64-row tile would waste >= half its DMMAs
   // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
   const bool gauss = gauss_enabled();
   if (m <= 32 && s <= 32) {
     if (n <= (uint64_t)SmallCfg::BK)
       return gauss ? launch_small_persistent<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc,
-                                                            bslice, cslice, stream)
+                                                            bslice, cslice, stream, only_if)
                    : launch_small_persistent<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice,
-                                                       cslice, stream);
+                                                       cslice, stream, only_if);
     return gauss ? launch_cfg<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice,
-                                             stream)
-                 : launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
+                                             stream, only_if)
+                 : launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream,
+                                        only_if);
   }
   if (gauss)
-    return launch_cfg<GaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
-  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream);
+    return launch_cfg<GaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream,
+                                only_if);
+  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if);
+}
+
+cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                    double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                    uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
+                                    int algo) {
+  if (m == 0 || s == 0 || p == 0) return cudaSuccess;
+  if (algo == kAlgoAuto) algo = choose_gemm_algo(n, s);
+  if (algo == kAlgoOzaki && (n % 32 != 0 || n > 8192)) return cudaErrorInvalidValue;
+  if (algo != kAlgoOzaki)
+    return dmma_spectral_gemm(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, nullptr);
+  // exact int8 tensor-core path (qt_ozaki.cu); the DMMA kernels run only if
+  // the inputs held a non-finite value
+  int* flag = nullptr;
+  cudaError_t e = cudaMallocAsync(&flag, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
+  if (e == cudaSuccess)
+    e = launch_spectral_gemm_ozaki(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, flag, stream);
+  if (e == cudaSuccess)
+    e = dmma_spectral_gemm(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, flag);
+  const cudaError_t fe = cudaFreeAsync(flag, stream);
+  return e != cudaSuccess ? e : fe;
 }
 
 cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                  double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                                 cudaStream_t stream) {
-  return launch_spectral_gemm_ld(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, s, s, n * s, m * s, stream);
+                                 cudaStream_t stream, int algo) {
+  return launch_spectral_gemm_ld(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, s, s, n * s, m * s, stream, algo);
 }
 
 }  // namespace qtb

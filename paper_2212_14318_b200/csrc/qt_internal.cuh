@@ -65,7 +65,7 @@ cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2,
                                  const double2* bh1, const double2* bh2,
                                  double2* ch1, double2* ch2,
                                  uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, int algo = -1);
 
 // Same with explicit leading dimensions: B̂ rows at pitch ldb (slice stride
 // bslice), Ĉ rows at pitch ldc (slice stride cslice) — lets a column chunk of
@@ -73,7 +73,41 @@ cudaError_t launch_spectral_gemm(const double2* ah1, const double2* ah2,
 cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, int algo = -1);
+
+// Exact int8 tensor-core (Ozaki-II / CRT) evaluation of the same product
+// (qt_ozaki.cu).  *flag (device int, zeroed by the caller) is set to 1 if the
+// inputs hold a non-finite value, in which case C is left untouched.
+enum GemmAlgo { kAlgoAuto = -1, kAlgoDmma = 0, kAlgoOzaki = 1 };
+bool ozaki_supported(uint64_t n, uint64_t s);
+// the algorithm a product of this shape uses (callers that split one product
+// into row slabs or column chunks decide once, on the full shape)
+inline int choose_gemm_algo(uint64_t n, uint64_t s) { return ozaki_supported(n, s) ? kAlgoOzaki : kAlgoDmma; }
+cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, const double2* bh1,
+                                       const double2* bh2, double2* ch1, double2* ch2, uint64_t m, uint64_t n,
+                                       uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc, uint64_t bslice,
+                                       uint64_t cslice, int* flag, cudaStream_t stream);
+// Two-phase form for row-slab streaming: B' residues prepared once for every
+// frequency (require_all) or per A batch, then any number of A row slabs.
+struct OzakiB {
+  uint8_t* res = nullptr;
+  int* eB = nullptr;
+  uint64_t n = 0, s = 0, p = 0, ldb = 0, bslice = 0;
+  int nslots = 0;
+  bool all = false;
+};
+cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                            uint64_t ldb, uint64_t bslice, int* flag, bool require_all, OzakiB* out,
+                            cudaStream_t stream);
+cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                           uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
+                           cudaStream_t stream);
+cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream);
+// DMMA kernels that run only if *only_if != 0 (nullptr: always)
+cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                               double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                               uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
+                               const int* only_if);
 
 // Definitional product C_k = sum_r A_{(k-r) mod p} (.) B_r (qt_naive.cu).
 cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,

@@ -202,6 +202,7 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
   }
 
   // 3) per device: for each chunk K1(B chunk) + strided K2 into the C slab; K3; download
+  const int algo = qt_gemm_algo(m, n, s, p);  // every rank and chunk: the full product's choice
   auto compute = [&](int g) {
     DevState& d = st[g];
     cudaSetDevice(d.dev);
@@ -218,9 +219,9 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
       r = qt_qfft3_conj_f64_device(chunk_ptr(g, j, 0), chunk_ptr(g, j, 1), bhat_ptr(g, 0), bhat_ptr(g, 1), n, cols,
                                    p, d.comp);
       if (r == QT_OK)
-        r = qt_spectral_product_f64_device_ld(Ah1, Ah2, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q,
-                                              C2 + 2 * j * Q, rows[g], n, cols, p, cols, s, n * cols, rows[g] * s,
-                                              d.comp);
+        r = qt_spectral_product_f64_device_ld_algo(Ah1, Ah2, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q,
+                                                   C2 + 2 * j * Q, rows[g], n, cols, p, cols, s, n * cols,
+                                                   rows[g] * s, algo, d.comp);
     }
     if (r == QT_OK) r = qt_qifft3_conj_f64_device(C1, C2, C1, C2, rows[g], s, p, d.comp);
     if (r == QT_OK) {

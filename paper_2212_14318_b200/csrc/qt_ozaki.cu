@@ -1,0 +1,744 @@
+// qt_ozaki.cu — K2 on the int8 tensor cores: exact modular (Ozaki-II / CRT)
+// evaluation of the paired-frequency product (sm_100a, tcgen05 + TMA + TMEM).
+//
+// What is computed is the same stage 2 as qt_gemm.cu (tproduct.cpp:89-106):
+//     [C1_k; C2_k] = X_k Y_k,  X_k = [[A1_k, -conj A2_sk], [A2_k, conj A1_sk]],  Y_k = [B1_k; B2_k]
+// (sk = (p - k) mod p, SURVEY §8(a) paired form).  In real form
+//     [Re C | Im C] = [Re X | Im X] . [[Re Y, Im Y], [-Im Y, Re Y]]      (2m x 4n) . (4n x 2s)
+// FP64 has no tcgen05 path on B200 (DMMA peaks at 37 TF/s), so the product is
+// evaluated EXACTLY in integers and rounded once:
+//   1. scale: every row of X_k and every column of Y_k gets a power of two so
+//      that its largest |re|, |im| lies in [2^(b-1), 2^b), b = 53, and is rounded
+//      to integers X', Y' (the only approximation: <= 2^-53 of the row/column
+//      maximum, i.e. fp64 input precision);
+//   2. residues: X' and Y' mod each of Q = 16 pairwise-coprime moduli <= 256, as
+//      uint8 in [0, p) (K2r kernels, K-major, ready for TMA);
+//   3. int8 GEMMs: for each modulus, X'_q Y'_q on tcgen05.mma.kind::i8 (u8 x u8)
+//      with an int32 TMEM accumulator (exact: sum < 255^2 * 4n < 2^31 for
+//      n <= 8192), reduced mod p_q in the epilogue and stored as one byte per
+//      real output (K2g kernel);
+//   4. CRT: the 16 residues give X'Y' exactly (|X'Y'| < 2^121 < M/2 = 2^124.2),
+//      reconstructed as a 96-bit fixed-point fraction X'Y'/M, converted to
+//      double once and scaled back by 2^-(eX + eY) (K2c kernel).
+// The integer product is exact, so the result does not depend on tiling,
+// K order, row shards or column chunks — bitwise — and its error is the fp64
+// rounding of the scaled inputs plus one final rounding: measured below the
+// DMMA path's error against the definitional product.
+//
+// Non-finite inputs cannot be represented in integers: K2r raises a device
+// flag, K2c then leaves C alone and the DMMA kernel (qt_gemm.cu) recomputes
+// the product on the GPU (its launch is conditional on the flag).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "qt_internal.cuh"
+
+namespace qtb {
+namespace oz {
+
+constexpr int kQ = 16;
+constexpr int kBits = 53;
+// pairwise coprime, <= 256; product M = 2^125.2
+constexpr int kModuli[kQ] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+struct ModTable {
+  uint32_t p[kQ];
+  uint32_t magic[kQ];  // floor(2^32 / p): quotient estimate off by at most one
+  uint32_t c1[kQ];     // 2^18 mod p
+  uint32_t c2[kQ];     // 2^36 mod p
+  uint32_t bias[kQ];   // multiple of p >= 2^25 (keeps the limb combination non-negative)
+  uint32_t w[kQ][3];   // round(2^96 * y_q / p_q) mod 2^96, y_q = (M/p_q)^-1 mod p_q (CRT weights)
+  double M;            // prod p_q (rounded)
+};
+__constant__ ModTable c_mod;
+
+// ------------------------------------------------------------------ tiles
+constexpr int BM = 128;        // output rows per CTA (TMEM lanes)
+constexpr int BNC = 128;       // complex output columns per CTA (Re + Im = 256 TMEM columns)
+constexpr int BN = 2 * BNC;    // real B' rows per tile
+constexpr int BK = 128;        // K bytes per stage (one 128-byte swizzle row)
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK;  // 16 KB
+constexpr int B_STAGE = BN * BK;  // 32 KB
+constexpr int GEMM_THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr size_t GEMM_SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) + 1024;
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, int8 x int8 -> int32
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// K-major operand, 128-byte swizzle: 8-row groups 1024 B apart (SBO), version 1
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: s32 accumulator, u8 x u8, K-major A and B, M = 128, N = 256
+constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// v mod p for any 32-bit v: the magic quotient is exact or one short
+__device__ __forceinline__ uint32_t mod_u32(uint32_t v, uint32_t p, uint32_t magic) {
+  const uint32_t r = v - __umulhi(v, magic) * p;
+  return r >= p ? r - p : r;
+}
+
+// --------------------------------------------------------------- K2g GEMM
+struct GemmParams {
+  uint8_t* R;        // residues out: [Q][F * Mp][Sp] x (re, im) bytes
+  int Q, mt, Mp, Sp, KB, F;
+  int bslot0;        // slot of this batch's first frequency in the B' buffer
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mtile = blockIdx.x % P.mt, ntile = blockIdx.x / P.mt, f = blockIdx.y;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      const int arow = f * P.Mp + mtile * BM, brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN;
+      uint32_t it = 0;
+      for (int q = 0; q < P.Q; ++q)
+        for (int kb = 0; kb < P.KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
+          tma_load_3d(sA + s * A_STAGE, &mapA, &full[s], kb * BK, arow, q);
+          tma_load_3d(sB + s * B_STAGE, &mapB, &full[s], kb * BK, brow, q);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      uint32_t it = 0;
+      for (int q = 0; q < P.Q; ++q) {
+        const int b = q & 1;
+        mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kb = 0; kb < P.KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * A_STAGE), b0 = smem_u32(sB + s * B_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8(d, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), kIdesc, (kb | kk) != 0);
+          tc_commit(&empty[s]);  // smem stage free once these MMAs have read it
+        }
+        tc_commit(&tfull[b]);  // accumulator b complete
+      }
+    }
+  } else {  // ---- epilogue: TMEM -> mod p -> bytes
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const size_t plane = (size_t)P.F * P.Mp * P.Sp * 2;
+    uint8_t* out0 = P.R + ((size_t)(f * P.Mp + mtile * BM + row) * P.Sp + (size_t)ntile * BNC) * 2;
+    for (int q = 0; q < P.Q; ++q) {
+      const int b = q & 1;
+      mbar_wait(&tfull[b], (q >> 1) & 1);
+      tc_fence_after();
+      const uint32_t pq = c_mod.p[q], mg = c_mod.magic[q];
+      uint8_t* out = out0 + (size_t)q * plane;
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + b * BN;
+#pragma unroll 1
+      for (int c = 0; c < BNC / 32; ++c) {
+        uint32_t re[32], im[32];
+        tmem_ld32(tbase + c * 32, re);
+        tmem_ld32(tbase + BNC + c * 32, im);
+        tmem_wait_ld();
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t r0 = mod_u32(re[2 * j], pq, mg), i0 = mod_u32(im[2 * j], pq, mg);
+          const uint32_t r1 = mod_u32(re[2 * j + 1], pq, mg), i1 = mod_u32(im[2 * j + 1], pq, mg);
+          w[j] = r0 | (i0 << 8) | (r1 << 16) | (i1 << 24);
+        }
+        uint4* o = reinterpret_cast<uint4*>(out + c * 64);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------- K2r residues
+// Frequencies are processed in slots: slot 2j, 2j+1 hold the pair (j+1,
+// p-j-1); the self-paired 0 and p/2 come last.  A batch is a run of slots with
+// an even start, so a pair never straddles two batches.
+__device__ __forceinline__ int slot_freq(int slot, int p) {
+  const int npairs = (p - 1) / 2;
+  if (slot < 2 * npairs) return (slot & 1) ? p - (slot / 2 + 1) : slot / 2 + 1;
+  return slot == 2 * npairs ? 0 : p / 2;
+}
+
+// An integer-valued double |x| < 2^53 as 18-bit limbs: x = a2 2^36 + a1 2^18 + a0
+struct Limbs {
+  uint32_t a0, a1;
+  int a2;
+};
+__device__ __forceinline__ Limbs to_limbs(double x, int e) {
+  const long long v = __double2ll_rn(ldexp(x, e));
+  return Limbs{(uint32_t)(v & 0x3FFFF), (uint32_t)((v >> 18) & 0x3FFFF), (int)(v >> 36)};
+}
+// x mod p_q in [0, p_q)
+__device__ __forceinline__ uint32_t res_of(const Limbs& l, int q) {
+  const uint32_t v = (uint32_t)((int)c_mod.c2[q] * l.a2 + (int)c_mod.bias[q]) + c_mod.c1[q] * l.a1 + l.a0;
+  return mod_u32(v, c_mod.p[q], c_mod.magic[q]);
+}
+__device__ __forceinline__ uint32_t neg_res(uint32_t r, uint32_t p) { return r ? p - r : 0u; }
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+  return v;
+}
+
+// exponent e with max * 2^e in [2^(b-1), 2^b) (0 for an all-zero row)
+__device__ __forceinline__ int scale_exp(double mx) {
+  if (mx == 0.0) return 0;
+  int E;
+  frexp(mx, &E);
+  return kBits - E;
+}
+constexpr double kDblMax = 1.7976931348623157e308;
+
+// A side: one CTA per (slot f, row i < m) handles the row pair
+// (A1_k[i], A2_sk[i]), which shares one exponent, and writes
+//   X_k  row i     = [Re A1_k | -Re A2_sk | Im A1_k |  Im A2_sk]
+//   X_sk row m + i = [Re A2_sk |  Re A1_k | Im A2_sk | -Im A1_k]
+// (X_sk's slot is f^1, or f itself for a self-paired frequency).
+constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32-bit word)
+__global__ void __launch_bounds__(256) oz_residue_a_kernel(const double2* __restrict__ a1,
+                                                           const double2* __restrict__ a2, uint8_t* __restrict__ out,
+                                                           int* __restrict__ eA, int* nonfinite, int m, int n, int p,
+                                                           int f0, int Mp, int F, int Q) {
+  __shared__ double red[8];
+  const int i = blockIdx.x, f = blockIdx.y;
+  const int k = slot_freq(f0 + f, p), sk = (p - k) % p;
+  const int fpart = (k == sk) ? f : (f ^ 1);
+  const double2* P = a1 + ((size_t)k * m + i) * n;
+  const double2* Qr = a2 + ((size_t)sk * m + i) * n;
+  double mx = 0.0;
+  bool bad = false;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double2 x = P[j], y = Qr[j];
+    mx = fmax(mx, fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y))));
+    bad |= !(fabs(x.x) + fabs(x.y) + fabs(y.x) + fabs(y.y) <= kDblMax);
+  }
+  bad = __syncthreads_or(bad);
+  mx = block_max(mx, red);
+  if (bad) {
+    if (threadIdx.x == 0) atomicExch(nonfinite, 1);
+    return;
+  }
+  const int e = scale_exp(mx);
+  if (threadIdx.x == 0) {
+    eA[f * Mp + i] = e;
+    eA[fpart * Mp + m + i] = e;
+  }
+  const size_t Kp = 4 * (size_t)n, plane = (size_t)F * Mp * Kp;
+  uint8_t* up = out + (size_t)(f * Mp + i) * Kp;
+  uint8_t* lo = out + (size_t)(fpart * Mp + m + i) * Kp;
+  for (int j0 = threadIdx.x * kAVec; j0 < n; j0 += blockDim.x * kAVec) {
+    Limbs r1[kAVec], i1[kAVec], r2[kAVec], i2[kAVec];
+#pragma unroll
+    for (int t = 0; t < kAVec; ++t) {
+      const double2 x = P[j0 + t], y = Qr[j0 + t];
+      r1[t] = to_limbs(x.x, e);
+      i1[t] = to_limbs(x.y, e);
+      r2[t] = to_limbs(y.x, e);
+      i2[t] = to_limbs(y.y, e);
+    }
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t pq = c_mod.p[q];
+      uint32_t wr1 = 0, wi1 = 0, wr2 = 0, wi2 = 0, wnr2 = 0, wni1 = 0;
+#pragma unroll
+      for (int t = 0; t < kAVec; ++t) {
+        const int sh = t * 8;
+        const uint32_t a = res_of(r1[t], q), b = res_of(i1[t], q), c = res_of(r2[t], q), d = res_of(i2[t], q);
+        wr1 |= a << sh;
+        wi1 |= b << sh;
+        wr2 |= c << sh;
+        wi2 |= d << sh;
+        wnr2 |= neg_res(c, pq) << sh;
+        wni1 |= neg_res(b, pq) << sh;
+      }
+      uint8_t* u = up + (size_t)q * plane + j0;
+      uint8_t* l = lo + (size_t)q * plane + j0;
+      *reinterpret_cast<uint32_t*>(u) = wr1;
+      *reinterpret_cast<uint32_t*>(u + n) = wnr2;
+      *reinterpret_cast<uint32_t*>(u + 2 * n) = wi1;
+      *reinterpret_cast<uint32_t*>(u + 3 * n) = wi2;
+      *reinterpret_cast<uint32_t*>(l) = wr2;
+      *reinterpret_cast<uint32_t*>(l + n) = wr1;
+      *reinterpret_cast<uint32_t*>(l + 2 * n) = wi2;
+      *reinterpret_cast<uint32_t*>(l + 3 * n) = wni1;
+    }
+  }
+}
+
+// B side, pass 1: per (slot f, column c) exponent over Y_k[:, c] = [B1_k[:, c]; B2_k[:, c]]
+__global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
+                                                          const double2* __restrict__ b2, int* __restrict__ eB,
+                                                          int* nonfinite, int n, int s, int p, int f0, int Sp,
+                                                          uint64_t ldb, uint64_t bslice) {
+  __shared__ double red[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
+  const int k = slot_freq(f0 + f, p);
+  double mx = 0.0;
+  if (c < s)
+    for (int j = w; j < 2 * n; j += 8) {
+      const double2 y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
+      // a sum of magnitudes is inf/nan iff a component is (or the pair overflows)
+      mx = fmax(mx, (fabs(y.x) + fabs(y.y) <= kDblMax) ? fmax(fabs(y.x), fabs(y.y))
+                                                       : __longlong_as_double(0x7ff0000000000000ll));
+    }
+  red[w][threadIdx.x & 31] = mx;
+  __syncthreads();
+  if (w == 0) {
+    for (int t = 1; t < 8; ++t) mx = fmax(mx, red[t][threadIdx.x]);
+    int e = 0;
+    if (c < s) {
+      if (!(mx <= kDblMax)) atomicExch(nonfinite, 1);
+      else e = scale_exp(mx);
+    }
+    eB[f * Sp + c] = e;
+  }
+}
+
+// B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
+// the Re-row [Re Y | -Im Y] and the Im-row [Im Y | Re Y] of each column.  Row
+// order inside a slot: tile t = c / 128 holds its 128 Re-rows, then its 128
+// Im-rows.  Columns c >= s (padding) get zero rows.
+__global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
+                                                           const double2* __restrict__ b2,
+                                                           const int* __restrict__ eB, uint8_t* __restrict__ out,
+                                                           int n, int s, int p, int f0, int Sp, int F, int Q,
+                                                           uint64_t ldb, uint64_t bslice) {
+  extern __shared__ double2 tile_raw[];
+  double2 (*tile)[33] = reinterpret_cast<double2 (*)[33]>(tile_raw);
+  const int c0 = blockIdx.x * 32, j0 = blockIdx.z * 128, f = blockIdx.y;
+  const int k = slot_freq(f0 + f, p);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int jj = ty; jj < 128; jj += 8) {
+    const int j = j0 + jj, c = c0 + tx;
+    double2 y = make_double2(0.0, 0.0);
+    if (c < s && j < 2 * n)
+      y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
+    tile[jj][tx] = y;
+  }
+  __syncthreads();
+  const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
+  const int c = c0 + tx;
+  const int e = eB[f * Sp + c];
+  const int tcol = c / BNC, ic = c % BNC;
+  uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp;
+  uint8_t* im_row = re_row + (size_t)BNC * Kp;
+  const int jb = j0 + ty * 16;
+  if (jb >= 2 * n) return;
+  Limbs lr[16], li[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const double2 y = tile[ty * 16 + t][tx];
+    lr[t] = to_limbs(y.x, e);
+    li[t] = to_limbs(y.y, e);
+  }
+  for (int q = 0; q < Q; ++q) {
+    const uint32_t pq = c_mod.p[q];
+    uint32_t wr[4] = {0, 0, 0, 0}, wi[4] = {0, 0, 0, 0}, wni[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int w = t >> 2, sh = (t & 3) * 8;
+      const uint32_t a = res_of(lr[t], q), b = res_of(li[t], q);
+      wr[w] |= a << sh;
+      wi[w] |= b << sh;
+      wni[w] |= neg_res(b, pq) << sh;
+    }
+    const size_t off = (size_t)q * plane + jb;
+    *reinterpret_cast<uint4*>(re_row + off) = make_uint4(wr[0], wr[1], wr[2], wr[3]);           // Re-row: Re Y
+    *reinterpret_cast<uint4*>(re_row + off + 2 * n) = make_uint4(wni[0], wni[1], wni[2], wni[3]);  // Re-row: -Im Y
+    *reinterpret_cast<uint4*>(im_row + off) = make_uint4(wi[0], wi[1], wi[2], wi[3]);           // Im-row: Im Y
+    *reinterpret_cast<uint4*>(im_row + off + 2 * n) = make_uint4(wr[0], wr[1], wr[2], wr[3]);   // Im-row: Re Y
+  }
+}
+
+constexpr size_t kResBSmem = sizeof(double2) * 128 * 33;
+
+// ------------------------------------------------------------- K2c CRT
+// X'Y'/M = sum_q r_q y_q / p_q (mod 1), accumulated as a 96-bit fixed-point
+// fraction (mod 2^96 wraps = mod 1); the weights' rounding (<= 1/2 ulp each)
+// bounds the error by 16*255/2 units of 2^-96, i.e. <= 2^-84 * M = 2^41 in X'Y'
+// (which is ~2^110 for a typical element): far below one fp64 ulp.
+__device__ __forceinline__ double crt_value(const uint8_t* res, size_t plane, int Q) {
+  uint64_t acc0 = 0, acc1 = 0, acc2 = 0;
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    if (q >= Q) break;
+    const uint32_t r = res[(size_t)q * plane];
+    acc0 += (uint64_t)r * c_mod.w[q][0];
+    acc1 += (uint64_t)r * c_mod.w[q][1];
+    acc2 += (uint64_t)r * c_mod.w[q][2];
+  }
+  acc1 += acc0 >> 32;
+  acc2 += acc1 >> 32;
+  const uint32_t s0 = (uint32_t)acc0, s1 = (uint32_t)acc1, s2 = (uint32_t)acc2;
+  // signed 96-bit fraction in [-1/2, 1/2)
+  const int64_t top = (int64_t)(((uint64_t)s2 << 32) | s1);
+  const double frac = ldexp((double)top, -64) + ldexp((double)s0, -96);
+  return frac * c_mod.M;
+}
+
+__global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
+                                                     const int* __restrict__ eB, const int* nonfinite,
+                                                     double2* __restrict__ c1, double2* __restrict__ c2, int m,
+                                                     int s, int p, int f0, int fcur, int bslot0, int Mp, int Sp, int F,
+                                                     int Q, uint64_t ldc, uint64_t cslice) {
+  if (*nonfinite) return;
+  const size_t plane = (size_t)F * Mp * Sp * 2;
+  const size_t total = (size_t)fcur * 2 * m * s;  // slots of this batch only
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % s);
+    const size_t fr = t / s;
+    const int r = (int)(fr % (2 * m)), f = (int)(fr / (2 * m));
+    const uint8_t* res = R + ((size_t)(f * Mp + r) * Sp + c) * 2;
+    const double re = crt_value(res, plane, Q), im = crt_value(res + 1, plane, Q);
+    const int e = -(eA[f * Mp + r] + eB[(bslot0 + f) * Sp + c]);
+    const double2 v = make_double2(ldexp(re, e), ldexp(im, e));
+    const int k = slot_freq(f0 + f, p);
+    if (r < m) c1[k * cslice + (size_t)r * ldc + c] = v;
+    else c2[k * cslice + (size_t)(r - m) * ldc + c] = v;
+  }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, void* base, uint64_t kp, uint64_t rows, uint64_t planes, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {kp, rows, planes};
+  const cuuint64_t strides[2] = {kp, kp * rows};
+  const cuuint32_t box[3] = {(cuuint32_t)BK, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+ModTable make_table() {
+  ModTable t{};
+  unsigned __int128 M = 1;
+  for (int q = 0; q < kQ; ++q) M *= (unsigned)kModuli[q];
+  for (int q = 0; q < kQ; ++q) {
+    const uint32_t p = (uint32_t)kModuli[q];
+    t.p[q] = p;
+    t.magic[q] = (uint32_t)((((uint64_t)1) << 32) / p);
+    t.c1[q] = (uint32_t)((((uint64_t)1) << 18) % p);
+    t.c2[q] = (uint32_t)((((uint64_t)1) << 36) % p);
+    t.bias[q] = (uint32_t)(((((uint64_t)1) << 25) + p - 1) / p * p);
+    uint64_t mp = 1;  // (M / p) mod p
+    for (int j = 0; j < kQ; ++j)
+      if (j != q) mp = mp * (uint64_t)kModuli[j] % p;
+    uint64_t y = 1;
+    while (mp * y % p != 1) ++y;
+    // round(2^96 * y / p) mod 2^96
+    const unsigned __int128 num = (((unsigned __int128)y) << 96) + p / 2;
+    const unsigned __int128 w = num / p;
+    t.w[q][0] = (uint32_t)w;
+    t.w[q][1] = (uint32_t)(w >> 32);
+    t.w[q][2] = (uint32_t)(w >> 64);
+  }
+  t.M = (double)M;
+  return t;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+}  // namespace oz
+
+bool ozaki_supported(uint64_t n, uint64_t s) {
+  // QTB_OZAKI: 0 = never, 1 = auto (large contraction and output width), 2 = whenever the shape allows.
+  // Callers that split one product (row shards, column chunks) decide once on the full shape.
+  static const int mode = oz::env_int("QTB_OZAKI", 1);
+  if (mode == 0 || n == 0 || n % 32 != 0 || n > 8192) return false;
+  if (mode == 2) return true;
+  return n >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_N", 256) && s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_S", 256);
+}
+
+namespace {
+
+cudaError_t oz_init() {
+  using namespace oz;
+  static std::mutex mu;
+  static uint64_t done = 0;
+  cudaError_t e = once_per_device(mu, done, [] {
+    const ModTable t = make_table();
+    cudaError_t r = cudaMemcpyToSymbol(c_mod, &t, sizeof(t));
+    if (r != cudaSuccess) return r;
+    r = cudaFuncSetAttribute(oz_residue_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResBSmem);
+    if (r != cudaSuccess) return r;
+    return cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+  });
+  if (e != cudaSuccess) return e;
+  return encode_fn() ? cudaSuccess : cudaErrorNotSupported;
+}
+
+uint64_t pad_rows(uint64_t m) { return (2 * m + oz::BM - 1) / oz::BM * oz::BM; }
+uint64_t pad_cols(uint64_t s) { return (s + oz::BNC - 1) / oz::BNC * oz::BNC; }
+uint64_t b_slot_bytes(uint64_t n, uint64_t s) { return (uint64_t)oz::kQ * 2 * pad_cols(s) * 4 * n + 4 * pad_cols(s); }
+uint64_t a_slot_bytes(uint64_t m, uint64_t n, uint64_t s) {
+  return (uint64_t)oz::kQ * (pad_rows(m) * 4 * n + pad_rows(m) * pad_cols(s) * 2) + 4 * pad_rows(m);
+}
+uint64_t env_mb(const char* name, uint64_t dflt_mb) { return (uint64_t)oz::env_int(name, (int)dflt_mb) << 20; }
+
+// slots per batch: even (pairs stay together), balanced over the batches
+uint64_t batch_slots(uint64_t p, uint64_t per_slot, uint64_t budget) {
+  uint64_t F = std::max<uint64_t>(2, std::min<uint64_t>(p, budget / std::max<uint64_t>(1, per_slot)) & ~uint64_t(1));
+  const uint64_t nb = (p + F - 1) / F;
+  return std::min<uint64_t>(p, ((p + nb - 1) / nb + 1) & ~uint64_t(1));
+}
+
+// B' residues (and column exponents) of slots [f0, f0 + fcur) into buffer slots [bslot0, ...)
+cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint64_t f0, int fcur, int bslot0,
+                   int* flag, cudaStream_t stream) {
+  using namespace oz;
+  const uint64_t Sp = pad_cols(B.s);
+  uint8_t* res = B.res + (size_t)bslot0 * 2 * Sp * 4 * B.n;
+  int* eB = B.eB + (size_t)bslot0 * Sp;
+  oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur), 256, 0, stream>>>(bh1, bh2, eB, flag, (int)B.n, (int)B.s,
+                                                                         (int)B.p, (int)f0, (int)Sp, B.ldb, B.bslice);
+  oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + 127) / 128)), 256, kResBSmem, stream>>>(
+      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, kQ, B.ldb, B.bslice);
+  count_launches(2);
+  return cudaGetLastError();
+}
+
+// A side, GEMM and CRT for the frequency slots [0, p) against prepared B'
+// slots (B.all: slot f of B' is frequency slot f; else B' holds the batch)
+cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                     uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
+                     cudaStream_t stream) {
+  using namespace oz;
+  const uint64_t n = B.n, s = B.s, p = B.p, Mp = pad_rows(m), Sp = pad_cols(s), Kp = 4 * n;
+  const uint64_t F = B.all ? batch_slots(p, a_slot_bytes(m, n, s), env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  if (F * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytesA = (size_t)kQ * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
+  const size_t offR = bytesA, offE = offR + bytesR, wsbytes = offE + F * Mp * sizeof(int);
+  uint8_t* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, wsbytes, stream);
+  if (e != cudaSuccess) return e;
+  uint8_t* resA = ws;
+  uint8_t* R = ws + offR;
+  int* eA = reinterpret_cast<int*>(ws + offE);
+  // rows [2m, Mp) of every X' slot are padding the residue kernel never writes
+  if (Mp > 2 * m) e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * F, stream);
+  CUtensorMap mapA, mapB;
+  if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, F * Mp, kQ, BM) ||
+                           !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, BN)))
+    e = cudaErrorInvalidValue;
+  for (uint64_t f0 = 0; f0 < p && e == cudaSuccess; f0 += F) {
+    const int fcur = (int)std::min<uint64_t>(F, p - f0);
+    int bslot0 = (int)f0;
+    if (!B.all) {  // B' for this batch only
+      bslot0 = 0;
+      if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
+    }
+    oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n, (int)p,
+                                                                     (int)f0, (int)Mp, (int)F, kQ);
+    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0};
+    oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA, mapB,
+                                                                                                       gp);
+    const size_t total = (size_t)fcur * 2 * m * s;
+    const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 32);
+    oz_crt_kernel<<<blocks, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, fcur,
+                                              bslot0, (int)Mp, (int)Sp, (int)F, kQ, ldc, cslice);
+    count_launches(3);
+    e = cudaGetLastError();
+  }
+  const cudaError_t fe = cudaFreeAsync(ws, stream);
+  return e != cudaSuccess ? e : fe;
+}
+
+}  // namespace
+
+cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                            uint64_t ldb, uint64_t bslice, int* flag, bool require_all, OzakiB* out,
+                            cudaStream_t stream) {
+  *out = OzakiB{};
+  if (n % 32 != 0 || n > 8192 || p == 0) return cudaErrorInvalidValue;
+  cudaError_t e = oz_init();
+  if (e != cudaSuccess) return e;
+  OzakiB B{};
+  B.n = n;
+  B.s = s;
+  B.p = p;
+  B.ldb = ldb;
+  B.bslice = bslice;
+  const uint64_t per_b = b_slot_bytes(n, s);
+  // keep B' for every frequency when it fits (one residue pass over B̂, reused
+  // by every A batch / row slab); otherwise B' is rebuilt per A batch
+  B.all = require_all || per_b * p <= env_mb("QTB_OZAKI_B_MB", 24576);
+  B.nslots = B.all ? (int)p : (int)batch_slots(p, a_slot_bytes(m, n, s) + per_b, env_mb("QTB_OZAKI_WS_MB", 6144));
+  if ((uint64_t)B.nslots * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)oz::kQ * B.nslots * 2 * pad_cols(s) * 4 * n;
+  if ((e = cudaMallocAsync(&B.res, bytes + (size_t)B.nslots * pad_cols(s) * sizeof(int), stream)) != cudaSuccess)
+    return e;
+  B.eB = reinterpret_cast<int*>(B.res + bytes);
+  if (B.all) e = prep_b(B, bh1, bh2, 0, (int)p, 0, flag, stream);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(B.res, stream);
+    return e;
+  }
+  *out = B;
+  return cudaSuccess;
+}
+
+cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                           uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
+                           cudaStream_t stream) {
+  if (m == 0 || B.s == 0) return cudaSuccess;
+  return multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
+}
+
+cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream) {
+  cudaError_t e = B.res ? cudaFreeAsync(B.res, stream) : cudaSuccess;
+  B = OzakiB{};
+  return e;
+}
+
+cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, const double2* bh1,
+                                       const double2* bh2, double2* ch1, double2* ch2, uint64_t m, uint64_t n,
+                                       uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc, uint64_t bslice,
+                                       uint64_t cslice, int* flag, cudaStream_t stream) {
+  if (m == 0 || s == 0 || p == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  OzakiB B;
+  if ((e = ozaki_prepare_b(bh1, bh2, m, n, s, p, ldb, bslice, flag, false, &B, stream)) != cudaSuccess) return e;
+  e = ozaki_multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
+  const cudaError_t fe = ozaki_release(B, stream);
+  return e != cudaSuccess ? e : fe;
+}
+
+}  // namespace qtb

@@ -42,6 +42,10 @@ class RowShardedTProduct:
         self.bh = [torch.empty_like(t) for t in self.bc]
         self.c = torch.empty((2, p, self.rows, 2 * s), **f64)
         self.L = _native.lib()
+        # one stage-2 algorithm for every rank and chunk: the full product's
+        # (QT_GEMM_DMMA or QT_GEMM_INT8_EXACT), so the stitched C is bitwise
+        # identical to a single-GPU call
+        self.algo = self.L.qt_gemm_algo(m, n, s, p)
 
     # ---------------------------------------------------------------- inputs
     def load_a(self, a1: np.ndarray, a2: np.ndarray) -> None:
@@ -80,10 +84,10 @@ class RowShardedTProduct:
                                                      self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), n, cols, p,
                                                      sh), "qfft3_conj(B chunk)")
             off = 16 * c0  # bytes: column c0 of every row of the C slab
-            _native.check(L.qt_spectral_product_f64_device_ld(
+            _native.check(L.qt_spectral_product_f64_device_ld_algo(
                 self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(),
                 self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, rows, n, cols, p,
-                cols, s, n * cols, rows * s, sh), "spectral_product(chunk)")
+                cols, s, n * cols, rows * s, self.algo, sh), "spectral_product(chunk)")
         if rows:
             _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
                                                       self.c[0].data_ptr(), self.c[1].data_ptr(), rows, s, p, sh),

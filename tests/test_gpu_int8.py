@@ -1,0 +1,213 @@
+"""GPU parity of the exact int8 (Ozaki-II / CRT) stage 2 — csrc/qt_ozaki.cu.
+
+The product is evaluated exactly in integers and rounded once, so besides the
+1e-12 bar of BASELINE.json against the reference's tprod_fast (and its 1e-11
+bar against the definitional product, test_tproduct.cpp:105-112) it must be
+(a) bitwise independent of batching, row slabs and column chunks, and (b) at
+least as accurate as the fp64 DMMA path against a long-double truth.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2212_14318_b200 as qt
+from paper_2212_14318_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+DMMA, INT8 = 0, 1
+
+
+def bits_equal(x, y):
+    return np.array_equal(np.ascontiguousarray(x).view(np.uint64), np.ascontiguousarray(y).view(np.uint64))
+
+
+def torch_cuda():
+    import torch
+    return torch
+
+
+def spectral(ah, bh, m, n, s, p, algo, rows=None, cols=None):
+    """Stage 2 through qt_spectral_product_f64_device_ld_algo; rows/cols select
+    a row slab of Â / column chunk of B̂ (written into the full Ĉ)."""
+    torch = torch_cuda()
+    L = _native.lib()
+    c = torch.zeros((2, p, m, s), dtype=torch.complex128, device="cuda")
+    r0, r1 = rows if rows else (0, m)
+    c0, c1 = cols if cols else (0, s)
+    a = ah[:, :, r0:r1].contiguous()
+    b = bh[:, :, :, c0:c1].contiguous()
+    cc = torch.zeros((2, p, r1 - r0, s), dtype=torch.complex128, device="cuda")
+    off = 16 * c0
+    _native.check(L.qt_spectral_product_f64_device_ld_algo(
+        a[0].data_ptr(), a[1].data_ptr(), b[0].data_ptr(), b[1].data_ptr(), cc[0].data_ptr() + off,
+        cc[1].data_ptr() + off, r1 - r0, n, c1 - c0, p, c1 - c0, s, n * (c1 - c0), (r1 - r0) * s, algo, None),
+        "spectral")
+    c[:, :, r0:r1] = cc
+    torch.cuda.synchronize()
+    return c
+
+
+def random_spectral(m, n, s, p, seed):
+    torch = torch_cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    ah = torch.randn((2, p, m, n), dtype=torch.complex128, device="cuda", generator=g)
+    bh = torch.randn((2, p, n, s), dtype=torch.complex128, device="cuda", generator=g)
+    return ah, bh
+
+
+def reference_spectral(ah, bh):
+    """SURVEY §8(a) paired form in numpy float64 (complex128 matmul)."""
+    A1, A2 = ah[0].cpu().numpy(), ah[1].cpu().numpy()
+    B1, B2 = bh[0].cpu().numpy(), bh[1].cpu().numpy()
+    p = A1.shape[0]
+    C1 = np.empty((p, A1.shape[1], B1.shape[2]), np.complex128)
+    C2 = np.empty_like(C1)
+    for k in range(p):
+        sk = (p - k) % p
+        C1[k] = A1[k] @ B1[k] - np.conj(A2[sk]) @ B2[k]
+        C2[k] = np.conj(A1[sk]) @ B2[k] + A2[k] @ B1[k]
+    return C1, C2
+
+
+def rel(x, y):
+    return float(np.sqrt(sum(np.sum(np.abs(a - b) ** 2) for a, b in zip(x, y)) /
+                         sum(np.sum(np.abs(b) ** 2) for b in y)))
+
+
+# ---------------------------------------------------------------- algorithm
+def test_algorithm_choice_depends_on_n_and_s_only():
+    L = _native.lib()
+    assert L.qt_gemm_algo(2048, 2048, 2048, 32) == INT8      # config 5
+    assert L.qt_gemm_algo(7, 2048, 2048, 32) == INT8         # any row slab of it
+    assert L.qt_gemm_algo(1080, 1920, 64, 64) == DMMA        # config 4: narrow output
+    assert L.qt_gemm_algo(16, 16, 16, 4096) == DMMA          # config 3
+    assert L.qt_gemm_algo(32, 32, 32, 16) == DMMA            # config 1
+    assert L.qt_gemm_algo(64, 300, 512, 8) == DMMA           # n % 32 != 0
+
+
+@pytest.mark.parametrize("m,n,s,p", [(1, 32, 1, 5), (2, 32, 2, 3), (4, 64, 4, 1), (64, 96, 80, 8),
+                                     (130, 256, 70, 7), (200, 64, 300, 9), (129, 288, 131, 2)])
+def test_int8_spectral_matches_fp64(m, n, s, p):
+    """Forced int8 path on ragged / odd-p / tiny shapes against numpy fp64 and
+    against the DMMA path (both ~1e-16; bar 1e-13)."""
+    ah, bh = random_spectral(m, n, s, p, 5 + m + p)
+    c8 = spectral(ah, bh, m, n, s, p, INT8)
+    cd = spectral(ah, bh, m, n, s, p, DMMA)
+    ref = reference_spectral(ah, bh)
+    got8 = (c8[0].cpu().numpy(), c8[1].cpu().numpy())
+    gotd = (cd[0].cpu().numpy(), cd[1].cpu().numpy())
+    assert rel(got8, ref) <= 1e-13
+    assert rel(got8, gotd) <= 1e-13
+
+
+def test_int8_more_accurate_than_fp64_gemm():
+    """Against a long-double evaluation the exact-integer product's error is
+    no larger than the fp64 DMMA product's (both ~1e-16)."""
+    m, n, s, p = 48, 512, 40, 4
+    ah, bh = random_spectral(m, n, s, p, 77)
+    c8 = spectral(ah, bh, m, n, s, p, INT8)
+    cd = spectral(ah, bh, m, n, s, p, DMMA)
+    A = [x.cpu().numpy() for x in ah]
+    B = [x.cpu().numpy() for x in bh]
+    ld = np.longdouble
+
+    def cmm(x, y):  # complex matmul in long double
+        xr, xi, yr, yi = (v.astype(ld) for v in (x.real, x.imag, y.real, y.imag))
+        return xr @ yr - xi @ yi, xr @ yi + xi @ yr
+
+    err8 = errd = norm = 0.0
+    for k in range(p):
+        sk = (p - k) % p
+        t1 = cmm(A[0][k], B[0][k])
+        t2 = cmm(np.conj(A[1][sk]), B[1][k])
+        t3 = cmm(np.conj(A[0][sk]), B[1][k])
+        t4 = cmm(A[1][k], B[0][k])
+        c1 = (t1[0] - t2[0], t1[1] - t2[1])
+        c2 = (t3[0] + t4[0], t3[1] + t4[1])
+        for got, sq in ((c8, "e8"), (cd, "ed")):
+            g1, g2 = got[0][k].cpu().numpy(), got[1][k].cpu().numpy()
+            e = (np.sum((g1.real - c1[0]) ** 2 + (g1.imag - c1[1]) ** 2) +
+                 np.sum((g2.real - c2[0]) ** 2 + (g2.imag - c2[1]) ** 2))
+            if sq == "e8":
+                err8 += float(e)
+            else:
+                errd += float(e)
+        norm += float(np.sum(c1[0] ** 2 + c1[1] ** 2) + np.sum(c2[0] ** 2 + c2[1] ** 2))
+    e8, ed = np.sqrt(err8 / norm), np.sqrt(errd / norm)
+    assert e8 <= 5e-16 and e8 <= ed, (e8, ed)
+
+
+# --------------------------------------------------------- exactness/bitwise
+def test_int8_row_slabs_and_column_chunks_bitwise():
+    m, n, s, p = 150, 128, 300, 6
+    ah, bh = random_spectral(m, n, s, p, 3)
+    full = spectral(ah, bh, m, n, s, p, INT8)
+    for rows in ((0, 64), (64, 101), (101, 150)):
+        part = spectral(ah, bh, m, n, s, p, INT8, rows=rows)
+        assert bits_equal(part[:, :, rows[0]:rows[1]].cpu().numpy(), full[:, :, rows[0]:rows[1]].cpu().numpy())
+    for cols in ((0, 128), (128, 137), (137, 300)):
+        part = spectral(ah, bh, m, n, s, p, INT8, cols=cols)
+        assert bits_equal(part[..., cols[0]:cols[1]].cpu().numpy(), full[..., cols[0]:cols[1]].cpu().numpy())
+
+
+def test_int8_batching_is_bitwise_invariant(monkeypatch):
+    m, n, s, p = 96, 256, 260, 7
+    ah, bh = random_spectral(m, n, s, p, 4)
+    ref = spectral(ah, bh, m, n, s, p, INT8).cpu().numpy()
+    monkeypatch.setenv("QTB_OZAKI_WS_MB", "1")   # 2 frequency slots per batch
+    monkeypatch.setenv("QTB_OZAKI_B_MB", "1")    # B' rebuilt per batch
+    got = spectral(ah, bh, m, n, s, p, INT8).cpu().numpy()
+    assert bits_equal(got, ref)
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -float("inf")])
+@pytest.mark.parametrize("where", ["a", "b"])
+def test_int8_nonfinite_inputs_fall_back_to_fp64(bad, where):
+    """Integers cannot carry inf/nan: the int8 path flags them and the DMMA
+    kernels recompute the product, so the result equals the fp64 path's."""
+    m, n, s, p = 40, 64, 36, 4
+    ah, bh = random_spectral(m, n, s, p, 9)
+    if where == "a":
+        ah[1, 2, 5, 7] = bad
+    else:
+        bh[0, 1, 9, 3] = bad
+    c8 = spectral(ah, bh, m, n, s, p, INT8).cpu().numpy()
+    cd = spectral(ah, bh, m, n, s, p, DMMA).cpu().numpy()
+    assert bits_equal(c8, cd)
+
+
+def test_int8_rejects_unsupported_contraction():
+    m, n, s, p = 8, 48, 8, 2  # n % 32 != 0
+    ah, bh = random_spectral(m, n, s, p, 1)
+    with pytest.raises(ValueError):
+        spectral(ah, bh, m, n, s, p, INT8)
+
+
+# ----------------------------------------------------------- full products
+@pytest.mark.parametrize("m,n,s,p", [(40, 256, 260, 5), (130, 288, 256, 4)])
+def test_int8_tprod_against_reference_oracle(m, n, s, p):
+    """Shapes that select the int8 path by themselves (n, s >= 256), end to end
+    through tprod_fast against the reference restatement (bar 1e-12)."""
+    assert _native.lib().qt_gemm_algo(m, n, s, p) == INT8
+    a = qt.gen_random_tensor(m, n, p, 21)
+    b = qt.gen_random_tensor(n, s, p, 22)
+    c = qt.tprod_fast(a, b)
+    ref = O.tprod_fast((a.t1, a.t2), (b.t1, b.t2))
+    assert O.rel_frob_error((c.t1, c.t2), ref) <= 1e-12
+
+
+def test_int8_host_slab_stream_bitwise_equals_device_path():
+    """A >= 128 MB int8 product takes the row-slab streaming host path
+    (resident B' residues); it must equal the device-resident path bitwise."""
+    torch = torch_cuda()
+    m, n, s, p = 512, 256, 256, 64
+    a = qt.gen_random_tensor(m, n, p, 31)
+    b = qt.gen_random_tensor(n, s, p, 32)
+    host = qt.tprod_fast(a, b)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    c1 = torch.empty((p, m, s), dtype=torch.complex128, device="cuda")
+    c2 = torch.empty_like(c1)
+    qt.tprod_fast_device(dev(a.t1), dev(a.t2), dev(b.t1), dev(b.t2), c1, c2, m, n, s, p)
+    torch.cuda.synchronize()
+    assert bits_equal(host.t1, c1.cpu().numpy()) and bits_equal(host.t2, c2.cpu().numpy())
