@@ -273,17 +273,25 @@ __device__ __forceinline__ int slot_freq(int slot, int p) {
   return slot == 2 * npairs ? 0 : p / 2;
 }
 
-// An integer-valued double |x| < 2^53 as 18-bit limbs: x = a2 2^36 + a1 2^18 + a0
+// x * 2^e, exact for the finite values scaled here (one multiply in range)
+__device__ __forceinline__ double scale2(double x, int e) {
+  if (e >= -1022 && e <= 1023) return x * __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(x, e);
+}
+
+// An integer-valued double |x| <= 2^53 as 18-bit limbs: x = a2 2^36 + a1 2^18 + a0
 struct Limbs {
   uint32_t a0, a1;
   int a2;
 };
 __device__ __forceinline__ Limbs to_limbs(double x, int e) {
-  const long long v = __double2ll_rn(ldexp(x, e));
+  const long long v = __double2ll_rn(scale2(x, e));
   return Limbs{(uint32_t)(v & 0x3FFFF), (uint32_t)((v >> 18) & 0x3FFFF), (int)(v >> 36)};
 }
-// x mod p_q in [0, p_q)
+// x mod p_q in [0, p_q); q is a compile-time index after unrolling, so the
+// table entries are constant-bank operands
 __device__ __forceinline__ uint32_t res_of(const Limbs& l, int q) {
+  if (q == 0) return l.a0 & 0xffu;  // p_0 = 256: the low byte (two's complement)
   const uint32_t v = (uint32_t)((int)c_mod.c2[q] * l.a2 + (int)c_mod.bias[q]) + c_mod.c1[q] * l.a1 + l.a0;
   return mod_u32(v, c_mod.p[q], c_mod.magic[q]);
 }
@@ -300,14 +308,14 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return v;
 }
 
-// exponent e with max * 2^e in [2^(b-1), 2^b) (0 for an all-zero row)
-__device__ __forceinline__ int scale_exp(double mx) {
-  if (mx == 0.0) return 0;
+// binary exponent E of a finite nonzero max (max < 2^E, max >= 2^(E-1))
+__device__ __forceinline__ int exp_of(double mx) {
   int E;
   frexp(mx, &E);
-  return kBits - E;
+  return E;
 }
 constexpr double kDblMax = 1.7976931348623157e308;
+constexpr int kNoExp = (int)0xC0C0C0C0;  // column of zeros (cudaMemset byte 0xC0); below every exponent
 
 // A side: one CTA per (slot f, row i < m) handles the row pair
 // (A1_k[i], A2_sk[i]), which shares one exponent, and writes
@@ -315,10 +323,10 @@ constexpr double kDblMax = 1.7976931348623157e308;
 //   X_sk row m + i = [Re A2_sk |  Re A1_k | Im A2_sk | -Im A1_k]
 // (X_sk's slot is f^1, or f itself for a self-paired frequency).
 constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32-bit word)
-__global__ void __launch_bounds__(256) oz_residue_a_kernel(const double2* __restrict__ a1,
+__global__ void __launch_bounds__(256, 3) oz_residue_a_kernel(const double2* __restrict__ a1,
                                                            const double2* __restrict__ a2, uint8_t* __restrict__ out,
                                                            int* __restrict__ eA, int* nonfinite, int m, int n, int p,
-                                                           int f0, int Mp, int F, int Q) {
+                                                           int f0, int Mp, int F) {
   __shared__ double red[8];
   const int i = blockIdx.x, f = blockIdx.y;
   const int k = slot_freq(f0 + f, p), sk = (p - k) % p;
@@ -338,7 +346,7 @@ __global__ void __launch_bounds__(256) oz_residue_a_kernel(const double2* __rest
     if (threadIdx.x == 0) atomicExch(nonfinite, 1);
     return;
   }
-  const int e = scale_exp(mx);
+  const int e = mx == 0.0 ? 0 : kBits - exp_of(mx);
   if (threadIdx.x == 0) {
     eA[f * Mp + i] = e;
     eA[fpart * Mp + m + i] = e;
@@ -356,7 +364,8 @@ __global__ void __launch_bounds__(256) oz_residue_a_kernel(const double2* __rest
       r2[t] = to_limbs(y.x, e);
       i2[t] = to_limbs(y.y, e);
     }
-    for (int q = 0; q < Q; ++q) {
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
       uint32_t wr1 = 0, wi1 = 0, wr2 = 0, wi2 = 0, wnr2 = 0, wni1 = 0;
 #pragma unroll
@@ -384,7 +393,9 @@ __global__ void __launch_bounds__(256) oz_residue_a_kernel(const double2* __rest
   }
 }
 
-// B side, pass 1: per (slot f, column c) exponent over Y_k[:, c] = [B1_k[:, c]; B2_k[:, c]]
+// B side, pass 1: per (slot f, column c) the binary exponent of the max over
+// Y_k[:, c] = [B1_k[:, c]; B2_k[:, c]], by atomicMax over row blocks of 256
+// (eB pre-filled with kNoExp; monotone, so the order of the atomics is moot)
 __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
                                                           const double2* __restrict__ b2, int* __restrict__ eB,
                                                           int* nonfinite, int n, int s, int p, int f0, int Sp,
@@ -392,9 +403,10 @@ __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restr
   __shared__ double red[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
   const int k = slot_freq(f0 + f, p);
+  const int jend = min(2 * n, (int)(blockIdx.z + 1) * 256);
   double mx = 0.0;
   if (c < s)
-    for (int j = w; j < 2 * n; j += 8) {
+    for (int j = blockIdx.z * 256 + w; j < jend; j += 8) {
       const double2 y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
       // a sum of magnitudes is inf/nan iff a component is (or the pair overflows)
       mx = fmax(mx, (fabs(y.x) + fabs(y.y) <= kDblMax) ? fmax(fabs(y.x), fabs(y.y))
@@ -402,116 +414,120 @@ __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restr
     }
   red[w][threadIdx.x & 31] = mx;
   __syncthreads();
-  if (w == 0) {
+  if (w == 0 && c < s) {
     for (int t = 1; t < 8; ++t) mx = fmax(mx, red[t][threadIdx.x]);
-    int e = 0;
-    if (c < s) {
-      if (!(mx <= kDblMax)) atomicExch(nonfinite, 1);
-      else e = scale_exp(mx);
-    }
-    eB[f * Sp + c] = e;
+    if (!(mx <= kDblMax)) atomicExch(nonfinite, 1);
+    else if (mx != 0.0) atomicMax(&eB[f * Sp + c], exp_of(mx));
   }
 }
 
 // B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
 // the Re-row [Re Y | -Im Y] and the Im-row [Im Y | Re Y] of each column.  Row
 // order inside a slot: tile t = c / 128 holds its 128 Re-rows, then its 128
-// Im-rows.  Columns c >= s (padding) get zero rows.
+// Im-rows.  Columns c >= s (padding) get zero rows.  The 128 x 32 block is
+// transposed through shared memory (column-major, row j at j + j/8 so both the
+// column-wise fill and the 4-consecutive-rows-per-lane reads are conflict
+// free); each warp then writes 128 contiguous bytes of a B' row per store.
+constexpr int kBRows = 128;
+constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 145 double2 per column
+constexpr size_t kResBSmem = sizeof(double2) * 32 * kBStride;
 __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2,
                                                            const int* __restrict__ eB, uint8_t* __restrict__ out,
-                                                           int n, int s, int p, int f0, int Sp, int F, int Q,
-                                                           uint64_t ldb, uint64_t bslice) {
-  extern __shared__ double2 tile_raw[];
-  double2 (*tile)[33] = reinterpret_cast<double2 (*)[33]>(tile_raw);
-  const int c0 = blockIdx.x * 32, j0 = blockIdx.z * 128, f = blockIdx.y;
+                                                           int n, int s, int p, int f0, int Sp, int F, uint64_t ldb,
+                                                           uint64_t bslice) {
+  extern __shared__ double2 tile[];  // [32][kBStride]
+  const int c0 = blockIdx.x * 32, j0 = blockIdx.z * kBRows, f = blockIdx.y;
   const int k = slot_freq(f0 + f, p);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int jj = ty; jj < 128; jj += 8) {
+  for (int jj = ty; jj < kBRows; jj += 8) {
     const int j = j0 + jj, c = c0 + tx;
     double2 y = make_double2(0.0, 0.0);
     if (c < s && j < 2 * n)
       y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
-    tile[jj][tx] = y;
+    tile[tx * kBStride + jj + (jj >> 3)] = y;
   }
   __syncthreads();
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
-  const int c = c0 + tx;
-  const int e = eB[f * Sp + c];
-  const int tcol = c / BNC, ic = c % BNC;
-  uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp;
-  uint8_t* im_row = re_row + (size_t)BNC * Kp;
-  const int jb = j0 + ty * 16;
+  const int jl = 4 * tx, jb = j0 + jl;  // this lane's 4 consecutive rows
   if (jb >= 2 * n) return;
-  Limbs lr[16], li[16];
+  for (int cc = ty; cc < 32; cc += 8) {
+    const int c = c0 + cc;
+    const int E = eB[f * Sp + c];
+    const int e = E == kNoExp ? 0 : kBits - E;
+    const int tcol = c / BNC, ic = c % BNC;
+    uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp + jb;
+    uint8_t* im_row = re_row + (size_t)BNC * Kp;
+    Limbs lr[4], li[4];
 #pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    const double2 y = tile[ty * 16 + t][tx];
-    lr[t] = to_limbs(y.x, e);
-    li[t] = to_limbs(y.y, e);
-  }
-  for (int q = 0; q < Q; ++q) {
-    const uint32_t pq = c_mod.p[q];
-    uint32_t wr[4] = {0, 0, 0, 0}, wi[4] = {0, 0, 0, 0}, wni[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const int w = t >> 2, sh = (t & 3) * 8;
-      const uint32_t a = res_of(lr[t], q), b = res_of(li[t], q);
-      wr[w] |= a << sh;
-      wi[w] |= b << sh;
-      wni[w] |= neg_res(b, pq) << sh;
+    for (int t = 0; t < 4; ++t) {
+      const double2 y = tile[cc * kBStride + jl + t + ((jl + t) >> 3)];
+      lr[t] = to_limbs(y.x, e);
+      li[t] = to_limbs(y.y, e);
     }
-    const size_t off = (size_t)q * plane + jb;
-    *reinterpret_cast<uint4*>(re_row + off) = make_uint4(wr[0], wr[1], wr[2], wr[3]);           // Re-row: Re Y
-    *reinterpret_cast<uint4*>(re_row + off + 2 * n) = make_uint4(wni[0], wni[1], wni[2], wni[3]);  // Re-row: -Im Y
-    *reinterpret_cast<uint4*>(im_row + off) = make_uint4(wi[0], wi[1], wi[2], wi[3]);           // Im-row: Im Y
-    *reinterpret_cast<uint4*>(im_row + off + 2 * n) = make_uint4(wr[0], wr[1], wr[2], wr[3]);   // Im-row: Re Y
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const uint32_t pq = c_mod.p[q];
+      uint32_t wr = 0, wi = 0, wni = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t a = res_of(lr[t], q), b = res_of(li[t], q);
+        wr |= a << (8 * t);
+        wi |= b << (8 * t);
+        wni |= neg_res(b, pq) << (8 * t);
+      }
+      const size_t off = (size_t)q * plane;
+      *reinterpret_cast<uint32_t*>(re_row + off) = wr;           // Re-row: Re Y
+      *reinterpret_cast<uint32_t*>(re_row + off + 2 * n) = wni;  // Re-row: -Im Y
+      *reinterpret_cast<uint32_t*>(im_row + off) = wi;           // Im-row: Im Y
+      *reinterpret_cast<uint32_t*>(im_row + off + 2 * n) = wr;   // Im-row: Re Y
+    }
   }
 }
-
-constexpr size_t kResBSmem = sizeof(double2) * 128 * 33;
 
 // ------------------------------------------------------------- K2c CRT
 // X'Y'/M = sum_q r_q y_q / p_q (mod 1), accumulated as a 96-bit fixed-point
 // fraction (mod 2^96 wraps = mod 1); the weights' rounding (<= 1/2 ulp each)
 // bounds the error by 16*255/2 units of 2^-96, i.e. <= 2^-84 * M = 2^41 in X'Y'
 // (which is ~2^110 for a typical element): far below one fp64 ulp.
-__device__ __forceinline__ double crt_value(const uint8_t* res, size_t plane, int Q) {
-  uint64_t acc0 = 0, acc1 = 0, acc2 = 0;
-#pragma unroll
-  for (int q = 0; q < kQ; ++q) {
-    if (q >= Q) break;
-    const uint32_t r = res[(size_t)q * plane];
-    acc0 += (uint64_t)r * c_mod.w[q][0];
-    acc1 += (uint64_t)r * c_mod.w[q][1];
-    acc2 += (uint64_t)r * c_mod.w[q][2];
-  }
+__device__ __forceinline__ double crt_finish(uint64_t acc0, uint64_t acc1, uint64_t acc2, int e) {
   acc1 += acc0 >> 32;
   acc2 += acc1 >> 32;
-  const uint32_t s0 = (uint32_t)acc0, s1 = (uint32_t)acc1, s2 = (uint32_t)acc2;
-  // signed 96-bit fraction in [-1/2, 1/2)
-  const int64_t top = (int64_t)(((uint64_t)s2 << 32) | s1);
-  const double frac = ldexp((double)top, -64) + ldexp((double)s0, -96);
-  return frac * c_mod.M;
+  // signed 96-bit fraction in [-1/2, 1/2), then times M 2^e
+  const int64_t top = (int64_t)(((uint64_t)(uint32_t)acc2 << 32) | (uint32_t)acc1);
+  const double frac = (double)top + (double)(uint32_t)acc0 * 2.3283064365386963e-10;  // (top + s0 2^-32), units 2^-64
+  return scale2(frac * c_mod.M, e - 64);
 }
 
+// one thread per complex element of output rows r (slot f, row r of [C1; C2])
 __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
                                                      const int* __restrict__ eB, const int* nonfinite,
                                                      double2* __restrict__ c1, double2* __restrict__ c2, int m,
-                                                     int s, int p, int f0, int fcur, int bslot0, int Mp, int Sp, int F,
-                                                     int Q, uint64_t ldc, uint64_t cslice) {
+                                                     int s, int p, int f0, int bslot0, int Mp, int Sp, int F,
+                                                     uint64_t ldc, uint64_t cslice) {
   if (*nonfinite) return;
-  const size_t plane = (size_t)F * Mp * Sp * 2;
-  const size_t total = (size_t)fcur * 2 * m * s;  // slots of this batch only
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t % s);
-    const size_t fr = t / s;
-    const int r = (int)(fr % (2 * m)), f = (int)(fr / (2 * m));
-    const uint8_t* res = R + ((size_t)(f * Mp + r) * Sp + c) * 2;
-    const double re = crt_value(res, plane, Q), im = crt_value(res + 1, plane, Q);
-    const int e = -(eA[f * Mp + r] + eB[(bslot0 + f) * Sp + c]);
-    const double2 v = make_double2(ldexp(re, e), ldexp(im, e));
-    const int k = slot_freq(f0 + f, p);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = blockIdx.z;
+  if (c >= s) return;
+  const int Eb = eB[(bslot0 + f) * Sp + c];
+  const int eb = Eb == kNoExp ? 0 : kBits - Eb;
+  const int k = slot_freq(f0 + f, p);
+  const size_t plane = (size_t)F * Mp * Sp;  // uchar2 elements
+  for (int r = blockIdx.y; r < 2 * m; r += gridDim.y) {
+    const uchar2* res = reinterpret_cast<const uchar2*>(R) + (size_t)(f * Mp + r) * Sp + c;
+    uint64_t x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const uchar2 v = res[(size_t)q * plane];
+      x0 += (uint64_t)v.x * c_mod.w[q][0];
+      x1 += (uint64_t)v.x * c_mod.w[q][1];
+      x2 += (uint64_t)v.x * c_mod.w[q][2];
+      y0 += (uint64_t)v.y * c_mod.w[q][0];
+      y1 += (uint64_t)v.y * c_mod.w[q][1];
+      y2 += (uint64_t)v.y * c_mod.w[q][2];
+    }
+    const int e = -(eA[f * Mp + r] + eb);
+    const double2 v = make_double2(crt_finish(x0, x1, x2, e), crt_finish(y0, y1, y2, e));
     if (r < m) c1[k * cslice + (size_t)r * ldc + c] = v;
     else c2[k * cslice + (size_t)(r - m) * ldc + c] = v;
   }
@@ -626,10 +642,13 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   const uint64_t Sp = pad_cols(B.s);
   uint8_t* res = B.res + (size_t)bslot0 * 2 * Sp * 4 * B.n;
   int* eB = B.eB + (size_t)bslot0 * Sp;
-  oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur), 256, 0, stream>>>(bh1, bh2, eB, flag, (int)B.n, (int)B.s,
-                                                                         (int)B.p, (int)f0, (int)Sp, B.ldb, B.bslice);
-  oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + 127) / 128)), 256, kResBSmem, stream>>>(
-      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, kQ, B.ldb, B.bslice);
+  cudaError_t e = cudaMemsetAsync(eB, 0xC0, (size_t)fcur * Sp * sizeof(int), stream);  // kNoExp
+  if (e != cudaSuccess) return e;
+  oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + 255) / 256)), 256, 0, stream>>>(
+      bh1, bh2, eB, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, B.ldb, B.bslice);
+  oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
+                        stream>>>(
+      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice);
   count_launches(2);
   return cudaGetLastError();
 }
@@ -665,14 +684,13 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
       if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
     }
     oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n, (int)p,
-                                                                     (int)f0, (int)Mp, (int)F, kQ);
+                                                                     (int)f0, (int)Mp, (int)F);
     GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0};
     oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA, mapB,
                                                                                                        gp);
-    const size_t total = (size_t)fcur * 2 * m * s;
-    const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 32);
-    oz_crt_kernel<<<blocks, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, fcur,
-                                              bslot0, (int)Mp, (int)Sp, (int)F, kQ, ldc, cslice);
+    const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
+    oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, bslot0,
+                                             (int)Mp, (int)Sp, (int)F, ldc, cslice);
     count_launches(3);
     e = cudaGetLastError();
   }
