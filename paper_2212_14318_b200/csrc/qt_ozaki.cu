@@ -263,6 +263,167 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+// ----------------------------------------------- K2g GEMM, CTA pair (2SM)
+// The same product on tcgen05.mma.cta_group::2: a cluster of two CTAs on a
+// TPC computes a 256 x 256 tile (M = 256 rows of X', N = 128 complex output
+// columns).  Each CTA stages its own 128 rows of A and HALF of the 256 B' rows,
+// so per SM the L2->SMEM operand traffic per MMA drops from 12 KB to 8 KB; the
+// even CTA issues the MMAs (its descriptors address the same offsets in the
+// odd CTA's shared memory) into both CTAs' TMEM.  Barriers: TMA bytes of both
+// CTAs land on the even CTA's full[s]; MMA commits multicast to both CTAs'
+// empty[s] / tfull[b]; both epilogues arrive on the even CTA's tempty[b].
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the even CTA's copy
+constexpr int STAGES2 = 6;
+constexpr int B2_STAGE = (BN / 2) * BK;  // 16 KB: this CTA's half of the B' tile
+constexpr size_t GEMM2_SMEM = (size_t)STAGES2 * (A_STAGE + B2_STAGE) + 1024;
+constexpr uint32_t kIdesc2 = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    oz_gemm2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                    GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A_STAGE;
+  __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int pair = blockIdx.x >> 1;
+  const int mt2 = P.mt / 2;  // 256-row tiles
+  const int mtile2 = pair % mt2, ntile = pair / mt2, f = blockIdx.y;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote use
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs)
+      const int arow = f * P.Mp + mtile2 * 256 + rank * BM;
+      const int brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN + rank * (BN / 2);
+      uint32_t it = 0;
+      for (int q = 0; q < P.Q; ++q)
+        for (int kb = 0; kb < P.KB; ++kb, ++it) {
+          const int s = it % STAGES2;
+          mbar_wait(&empty[s], ((it / STAGES2) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_STAGE + B2_STAGE));
+          tma_load_3d_2sm(sA + s * A_STAGE, &mapA, &full[s], kb * BK, arow, q);
+          tma_load_3d_2sm(sB + s * B2_STAGE, &mapB, &full[s], kb * BK, brow, q);
+        }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {  // ---- MMA issuer (even CTA)
+      uint32_t it = 0;
+      for (int q = 0; q < P.Q; ++q) {
+        const int b = q & 1;
+        mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * BN;
+        for (int kb = 0; kb < P.KB; ++kb, ++it) {
+          const int s = it % STAGES2;
+          mbar_wait(&full[s], (it / STAGES2) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * A_STAGE), b0 = smem_u32(sB + s * B2_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8_2sm(d, smem_desc_sw128(a0 + kk * 32), smem_desc_sw128(b0 + kk * 32), kIdesc2, (kb | kk) != 0);
+          tc_commit_2sm(&empty[s]);
+        }
+        tc_commit_2sm(&tfull[b]);
+      }
+    }
+  } else {  // ---- epilogue (both CTAs, own TMEM rows)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const size_t plane = (size_t)P.F * P.Mp * P.Sp * 2;
+    uint8_t* out0 = P.R + ((size_t)(f * P.Mp + mtile2 * 256 + rank * BM + row) * P.Sp + (size_t)ntile * BNC) * 2;
+    for (int q = 0; q < P.Q; ++q) {
+      const int b = q & 1;
+      mbar_wait(&tfull[b], (q >> 1) & 1);
+      tc_fence_after();
+      const uint32_t pq = c_mod.p[q], mg = c_mod.magic[q];
+      uint8_t* out = out0 + (size_t)q * plane;
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + b * BN;
+#pragma unroll 1
+      for (int c = 0; c < BNC / 32; ++c) {
+        uint32_t re[32], im[32];
+        tmem_ld32(tbase + c * 32, re);
+        tmem_ld32(tbase + BNC + c * 32, im);
+        tmem_wait_ld();
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t r0 = mod_u32(re[2 * j], pq, mg), i0 = mod_u32(im[2 * j], pq, mg);
+          const uint32_t r1 = mod_u32(re[2 * j + 1], pq, mg), i1 = mod_u32(im[2 * j + 1], pq, mg);
+          w[j] = r0 | (i0 << 8) | (r1 << 16) | (i1 << 24);
+        }
+        uint4* o = reinterpret_cast<uint4*>(out + c * 64);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(&tempty[b]) & kPeerMask)
+                     : "memory");
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // ------------------------------------------------------- K2r residues
 // Frequencies are processed in slots: slot 2j, 2j+1 hold the pair (j+1,
 // p-j-1); the self-paired 0 and p/2 come last.  A batch is a run of slots with
@@ -594,12 +755,17 @@ int env_int(const char* name, int dflt) {
 }  // namespace oz
 
 bool ozaki_supported(uint64_t n, uint64_t s) {
-  // QTB_OZAKI: 0 = never, 1 = auto (large contraction and output width), 2 = whenever the shape allows.
-  // Callers that split one product (row shards, column chunks) decide once on the full shape.
+  // QTB_OZAKI: 0 = never, 1 = auto, 2 = whenever the shape allows.  Auto takes
+  // the int8 path where it measured faster than DMMA on B200 (tools/oz_sweep.py:
+  // 256^3 0.86x, n = 1920 s = 64 0.61x, s = 128 1.10x, 512^3 1.68x, 2048^3
+  // 3.3x): the 16 residue GEMMs need enough columns to amortise the residues
+  // of A.  Callers that split one product (row slabs, column chunks) decide
+  // once on the full shape; m never enters (row shards agree by construction).
   static const int mode = oz::env_int("QTB_OZAKI", 1);
   if (mode == 0 || n == 0 || n % 32 != 0 || n > 8192) return false;
   if (mode == 2) return true;
-  return n >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_N", 256) && s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_S", 256);
+  return n >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_N", 256) && s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_S", 128) &&
+         n * s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_NS", 1 << 17);
 }
 
 namespace {
@@ -614,13 +780,23 @@ cudaError_t oz_init() {
     if (r != cudaSuccess) return r;
     r = cudaFuncSetAttribute(oz_residue_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResBSmem);
     if (r != cudaSuccess) return r;
+    r = cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
+    if (r != cudaSuccess) return r;
     return cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
   });
   if (e != cudaSuccess) return e;
   return encode_fn() ? cudaSuccess : cudaErrorNotSupported;
 }
 
-uint64_t pad_rows(uint64_t m) { return (2 * m + oz::BM - 1) / oz::BM * oz::BM; }
+bool use_pair() {
+  static const bool on = oz::env_int("QTB_OZAKI_2SM", 1) != 0;
+  return on;
+}
+// X' rows per slot: a multiple of the 256-row pair tile (128 for the 1-CTA kernel)
+uint64_t pad_rows(uint64_t m) {
+  const uint64_t t = use_pair() ? 256 : oz::BM;
+  return (2 * m + t - 1) / t * t;
+}
 uint64_t pad_cols(uint64_t s) { return (s + oz::BNC - 1) / oz::BNC * oz::BNC; }
 uint64_t b_slot_bytes(uint64_t n, uint64_t s) { return (uint64_t)oz::kQ * 2 * pad_cols(s) * 4 * n + 4 * pad_cols(s); }
 uint64_t a_slot_bytes(uint64_t m, uint64_t n, uint64_t s) {
@@ -674,7 +850,7 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
   if (Mp > 2 * m) e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * F, stream);
   CUtensorMap mapA, mapB;
   if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, F * Mp, kQ, BM) ||
-                           !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, BN)))
+                           !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, use_pair() ? BN / 2 : BN)))
     e = cudaErrorInvalidValue;
   for (uint64_t f0 = 0; f0 < p && e == cudaSuccess; f0 += F) {
     const int fcur = (int)std::min<uint64_t>(F, p - f0);
@@ -686,8 +862,12 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
     oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n, (int)p,
                                                                      (int)f0, (int)Mp, (int)F);
     GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0};
-    oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA, mapB,
-                                                                                                       gp);
+    if (use_pair())
+      oz_gemm2_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM2_SMEM, stream>>>(
+          mapA, mapB, gp);
+    else
+      oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA,
+                                                                                                         mapB, gp);
     const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
     oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, bslot0,
                                              (int)Mp, (int)Sp, (int)F, ldc, cslice);

@@ -81,6 +81,7 @@ def test_algorithm_choice_depends_on_n_and_s_only():
     assert L.qt_gemm_algo(2048, 2048, 2048, 32) == INT8      # config 5
     assert L.qt_gemm_algo(7, 2048, 2048, 32) == INT8         # any row slab of it
     assert L.qt_gemm_algo(1080, 1920, 64, 64) == DMMA        # config 4: narrow output
+    assert L.qt_gemm_algo(256, 256, 256, 64) == DMMA         # config 2: too small to amortise
     assert L.qt_gemm_algo(16, 16, 16, 4096) == DMMA          # config 3
     assert L.qt_gemm_algo(32, 32, 32, 16) == DMMA            # config 1
     assert L.qt_gemm_algo(64, 300, 512, 8) == DMMA           # n % 32 != 0
@@ -185,7 +186,7 @@ def test_int8_rejects_unsupported_contraction():
 
 
 # ----------------------------------------------------------- full products
-@pytest.mark.parametrize("m,n,s,p", [(40, 256, 260, 5), (130, 288, 256, 4)])
+@pytest.mark.parametrize("m,n,s,p", [(40, 256, 520, 5), (130, 288, 512, 4)])
 def test_int8_tprod_against_reference_oracle(m, n, s, p):
     """Shapes that select the int8 path by themselves (n, s >= 256), end to end
     through tprod_fast against the reference restatement (bar 1e-12)."""
@@ -201,7 +202,7 @@ def test_int8_host_slab_stream_bitwise_equals_device_path():
     """A >= 128 MB int8 product takes the row-slab streaming host path
     (resident B' residues); it must equal the device-resident path bitwise."""
     torch = torch_cuda()
-    m, n, s, p = 512, 256, 256, 64
+    m, n, s, p = 256, 256, 512, 64
     a = qt.gen_random_tensor(m, n, p, 31)
     b = qt.gen_random_tensor(n, s, p, 32)
     host = qt.tprod_fast(a, b)
