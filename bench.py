@@ -4,8 +4,10 @@
 Workload: BASELINE.json configs[4], the 1/2/4/8-GPU scaling case
 (m = n = s = 2048, p = 32, components U[-1,1) from the reference generator),
 override with --config {1..5}.  One step = one full T-product C = A *_T B
-(K1 tube FFT of A and B -> K2 paired-frequency DMMA GEMM -> K3 inverse tube
-FFT) over inputs already resident in HBM.  With N ranks (torchrun) the rows
+(K1 tube FFT of A and B -> K2 paired-frequency GEMM -> K3 inverse tube FFT)
+over inputs already resident in HBM.  K2 runs as the exact int8 tcgen05
+product (Ozaki-II, csrc/qt_ozaki.cu) for wide products (configs 5 and larger)
+and on the fp64 DMMA tensor cores otherwise (qt_gemm_algo).  With N ranks (torchrun) the rows
 of A and C are sharded in slabs of ceil(m/N) and B is broadcast from rank 0
 with NCCL inside the timed step (strong scaling: total work fixed).
 
@@ -20,6 +22,7 @@ same workload.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -383,6 +386,23 @@ def run_ours(args, cfg):
     ifft_ms = timed(lambda: L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
                                                         dc2.data_ptr(), rows, cfg.s, cfg.p, sh), max(3, args.steps))
     del ah, bh
+    # ---- per-kernel device time of the stage-2 GEMM kernel itself (library
+    # CUDA events on the launching stream, qt_prof_*), over a few extra steps
+    algo = L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p)   # 0 = fp64 DMMA, 1 = exact int8 (tcgen05)
+    nprof = max(2, args.steps)
+    L.qt_prof_enable(1)
+    for _ in range(nprof):
+        if not big:
+            l2_flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    L.qt_prof_enable(0)
+    prof = {}
+    for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_crt"):
+        t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
+        qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
+        if n_l.value:
+            prof[tag] = {"ms_per_step": t_ms.value / nprof, "launches_per_step": n_l.value / nprof}
     # keep the GPU under the same load for >= 1 s of clock samples
     # (iteration count from the max-over-ranks step time: identical on every rank)
     for _ in range(min(2000, int(math.ceil(1000.0 / max(ms, 1e-3))))):
@@ -398,31 +418,59 @@ def run_ours(args, cfg):
     gemm_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s) + cfg.bytes_tensor(rows, cfg.s)
     gemm_ai = 32.0 * rows * cfg.n * cfg.s * cfg.p / gemm_bytes
     ridge = PEAK_FP64_DMMA_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    algo = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
-            else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
-    if gemm_ai >= ridge:
-        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": gemm_tf,
-                "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": gemm_tf / PEAK_FP64_DMMA_TFLOPS,
+    algo_txt = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
+                else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
+    if algo == 1 and "k2_int8_gemm" in prof:
+        # exact int8 path: 16 modular GEMMs of the real-embedded (2m x 4n) . (4n x 2s) product per frequency
+        k_ms = prof["k2_int8_gemm"]["ms_per_step"]
+        ops = 2.0 * 16 * (2 * rows) * (4 * cfg.n) * (2 * cfg.s) * cfg.p
+        ach = ops / (k_ms * 1e-3) / 1e12
+        peak_i8 = 2.0 * peaks["bf16_tflops"]
+        roof = {"kernel": "K2 int8 modular GEMM oz_gemm2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)",
+                "bound": "tensor", "achieved": ach, "peak": peak_i8, "unit": "TFLOP/s", "frac": ach / peak_i8,
+                "op_type": "int8 x int8 -> int32 tensor ops (multiply-add = 2), i.e. TOPS",
+                "peak_source": f"2 x {peak_src} bf16_tflops (MEASURED_PEAKS.json); int8:bf16 dense = 4.5:2.25 "
+                               "PFLOP/s nominal",
+                "algorithmic": "2 * 16 moduli * (2m)(4n)(2s) * p int8 ops per step (= 512 m n s p), "
+                               "launched in frequency batches",
+                "algorithm": "exact Ozaki-II: 53-bit scaled integers, 16 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
+                "kernel_ms": k_ms, "launches_per_step": prof["k2_int8_gemm"]["launches_per_step"],
+                "share_of_step": k_ms / ms,
+                "fp64_equivalent_tflops": 32.0 * rows * cfg.n * cfg.s * cfg.p / (k_ms * 1e-3) / 1e12,
+                "traffic": None}
+        traffic, traffic_src = ncu_traffic(cfg, "K2_int8_gemm", rows)
+        roof["algorithmic_bytes"] = None
+    elif gemm_ai >= ridge:
+        k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
+        ktf = 32.0 * rows * cfg.n * cfg.s * cfg.p / (k_ms * 1e-3) / 1e12
+        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": ktf,
+                "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ktf / PEAK_FP64_DMMA_TFLOPS,
                 "peak_source": "measured fp64 DMMA burst (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no fp64",
                 "algorithmic": "32*m*n*s*p flops per launch (SURVEY 8d F_gemm, the reference's 16 m n s p "
                                "multiplications + additions)",
-                "algorithm": algo, "executed_tflops": exec_tf, "executed_frac": exec_tf / PEAK_FP64_DMMA_TFLOPS,
-                "kernel_ms": gemm_ms, "share_of_step": gemm_ms / ms, "traffic": None}
+                "algorithm": algo_txt, "executed_tflops": ktf * (0.75 if gauss else 1.0),
+                "executed_frac": ktf * (0.75 if gauss else 1.0) / PEAK_FP64_DMMA_TFLOPS,
+                "kernel_ms": k_ms, "share_of_step": k_ms / ms, "traffic": None}
+        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+        roof["algorithmic_bytes"] = gemm_bytes
     else:
-        gb = gemm_bytes / (gemm_ms * 1e-3) / 1e9
+        k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
+        gb = gemm_bytes / (k_ms * 1e-3) / 1e9
         roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "hbm", "achieved": gb,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"],
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
-                "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "algorithm": algo,
-                "kernel_ms": gemm_ms, "share_of_step": gemm_ms / ms, "traffic": None}
-    traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+                "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "algorithm": algo_txt,
+                "kernel_ms": k_ms, "share_of_step": k_ms / ms, "traffic": None}
+        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+        roof["algorithmic_bytes"] = gemm_bytes
     roof["traffic"] = traffic
     roof["traffic_source"] = traffic_src
-    roof["algorithmic_bytes"] = gemm_bytes
+    roof["kernel_times_ms_per_step"] = {k: v["ms_per_step"] for k, v in prof.items()}
     stages = {
         "K1_fft_A": {"ms": fftA_ms, "GB_s": fftA_gbs, "frac_hbm": fftA_gbs / peaks["hbm_gbs"]},
         "K2_gemm": {"ms": gemm_ms, "TFLOP_s": gemm_tf, "frac_fp64": gemm_tf / PEAK_FP64_DMMA_TFLOPS,
-                    "executed_TFLOP_s": exec_tf},
+                    "algorithm": "exact int8 (Ozaki-II, tcgen05)" if algo == 1 else "fp64 DMMA",
+                    **({} if algo == 1 else {"executed_TFLOP_s": exec_tf})},
         "K3_ifft_C": {"ms": ifft_ms, "GB_s": ifft_gbs, "frac_hbm": ifft_gbs / peaks["hbm_gbs"]},
     }
 

@@ -66,6 +66,15 @@ const char* qt_last_error(void);
  * (all devices).  Used by bench.py to report gpu_launches. */
 uint64_t qt_kernel_launches(void);
 
+/* Per-kernel device timing (CUDA events recorded on the launching stream
+ * around each launch of a tagged kernel), for bench.py's roofline.  Off by
+ * default; qt_prof_read synchronizes on the recorded events, returns the
+ * summed milliseconds and launch count of one tag and clears it.  Tags:
+ * "fft" (K1/K3 tube FFTs), "k2_dmma" (fp64 DMMA GEMM), "k2_int8_gemm"
+ * (tcgen05 int8 modular GEMM), "k2_int8_residues", "k2_int8_crt". */
+void qt_prof_enable(int on);
+int qt_prof_read(const char* tag, double* ms, uint64_t* launches);
+
 /* ---- device-resident entry points (all pointers are device pointers) ---
  * stream is a cudaStream_t (NULL = legacy default stream).  Work is enqueued
  * on the stream; the call returns without synchronising.                  */

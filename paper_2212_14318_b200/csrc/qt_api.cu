@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -216,6 +217,28 @@ int d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
 
 void count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
+}  // namespace
+
+bool prof_on() { return g_prof.load(std::memory_order_relaxed); }
+
+ProfScope::ProfScope(const char* t, cudaStream_t s) : tag(t), st(s) {
+  if (prof_on() && cudaEventCreate(&e0) == cudaSuccess) cudaEventRecord(e0, st);
+}
+
+void ProfScope::stop() {
+  if (!e0) return;
+  cudaEvent_t e1 = nullptr;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_ev[tag].emplace_back(e0, e1);
+  e0 = nullptr;
+}
+
 }  // namespace qtb
 
 using namespace qtb;
@@ -227,6 +250,33 @@ int qt_abi_version(void) { return QT_B200_ABI_VERSION; }
 const char* qt_last_error(void) { return t_err.c_str(); }
 
 uint64_t qt_kernel_launches(void) { return g_launches.load(); }
+
+void qt_prof_enable(int on) { g_prof.store(on != 0); }
+
+int qt_prof_read(const char* tag, double* ms, uint64_t* launches) {
+  t_err.clear();
+  if (!tag || !ms || !launches) return fail(QT_EINVAL, "qt_prof_read: null argument");
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    auto it = g_prof_ev.find(tag);
+    if (it != g_prof_ev.end()) evs.swap(it->second);
+  }
+  double total = 0.0;
+  int rc = QT_OK;
+  for (auto& [a, b] : evs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, a, b);
+    if (e != cudaSuccess && rc == QT_OK) rc = cuda_fail(e, "qt_prof_read");
+    total += t;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  *ms = total;
+  *launches = evs.size();
+  return rc;
+}
 
 int qt_tprod_f64_device(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                         double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream) {

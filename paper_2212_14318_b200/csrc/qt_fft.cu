@@ -523,7 +523,9 @@ cudaError_t launch_fft2(const TubeBatch& batch, const FftGeom& G, const double2*
   if (attr != cudaSuccess) return attr;
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
   dim3 grid((unsigned)tiles, njobs, groups);
+  ProfScope ps("fft", stream);
   tube_fft2_kernel<R0, R1><<<grid, kFftThreads, smem, stream>>>(batch, G, tw, logT);
+  ps.stop();
   count_launches(1);
   return cudaGetLastError();
 }
@@ -539,7 +541,9 @@ cudaError_t launch_pass(const TubeBatch& batch, const FftPlan& pl, const FftGeom
   }
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
   dim3 grid((unsigned)tiles, batch.njobs, groups);
+  ProfScope ps("fft", stream);
   tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
+  ps.stop();
   count_launches(1);
   return cudaGetLastError();
 }
@@ -644,9 +648,11 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
       double2* dst = (last && !bounce) ? J.out : bufs[s & 1];
       const uint64_t tot = (uint64_t)p * J.ntubes;
       const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, 148ull * 16);
+      ProfScope ps("fft", stream);
       tube_fft_global_stage_kernel<<<blocks, 256, 0, stream>>>(src, dst, J.ntubes, p, Ns, plan.radix[s], tw,
                                                                first ? J.conj_in : 0, last ? J.conj_out : 0,
                                                                last ? J.scale : 1.0);
+      ps.stop();
       count_launches(1);
       if (bounce) {
         cudaError_t ce = cudaMemcpyAsync(J.out, dst, bytes, cudaMemcpyDeviceToDevice, stream);

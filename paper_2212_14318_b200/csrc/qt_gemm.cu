@@ -372,9 +372,11 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
   for (uint64_t k0 = 0; k0 < npairs; k0 += 65535) {
     const unsigned chunk = (unsigned)std::min<uint64_t>(65535, npairs - k0);
     dim3 grid((unsigned)tiles, chunk);
+    ProfScope ps(only_if ? "k2_dmma_guard" : "k2_dmma", stream);
     paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(
         ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)k0, (int)ldb, (int)ldc, (long long)bslice,
         (long long)cslice, only_if);
+    ps.stop();
     count_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -415,9 +417,11 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
   const uint64_t items = (p / 2 + 1) * tiles;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)std::max(1, per_sm) * sms);
+  ProfScope ps(only_if ? "k2_dmma_guard" : "k2_dmma", stream);
   kern<<<(unsigned)grid, C::NTHREADS, smem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p,
                                                        (int)ldb, (int)ldc, (long long)bslice, (long long)cslice,
                                                        only_if);
+  ps.stop();
   count_launches(1);
   return cudaGetLastError();
 }

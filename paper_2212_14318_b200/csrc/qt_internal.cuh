@@ -138,4 +138,16 @@ cudaError_t once_per_device(std::mutex& mu, uint64_t& done_mask, F fn) {
 // Launch accounting (qt_kernel_launches).
 void count_launches(uint64_t k);
 
+// Per-kernel event timing (qt_prof_enable / qt_prof_read): a ProfScope
+// records a start event on construction and a stop event in stop(); both are
+// no-ops unless profiling is on.
+bool prof_on();
+struct ProfScope {
+  const char* tag;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(const char* t, cudaStream_t s);
+  void stop();
+};
+
 }  // namespace qtb

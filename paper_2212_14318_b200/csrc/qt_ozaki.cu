@@ -151,6 +151,7 @@ struct GemmParams {
   uint8_t* R;        // residues out: [Q][F * Mp][Sp] x (re, im) bytes
   int Q, mt, Mp, Sp, KB, F;
   int bslot0;        // slot of this batch's first frequency in the B' buffer
+  int nt, fcur;      // n tiles, slots in this batch (persistent pair kernel)
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -319,9 +320,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t rank;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int pair = blockIdx.x >> 1;
+  // persistent: cluster c takes work items c, c + nclusters, ... in the order
+  // (slot, modulus, n tile, m tile), so the clusters in flight share one
+  // (slot, modulus) plane of X' and Y' (~67 MB at config 5): each operand
+  // byte comes from DRAM about once instead of once per wave
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int mt2 = P.mt / 2;  // 256-row tiles
-  const int mtile2 = pair % mt2, ntile = pair / mt2, f = blockIdx.y;
+  const int tiles = mt2 * P.nt;
+  const int nitems = P.fcur * P.Q * tiles;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES2; ++s) {
@@ -347,10 +353,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer (both CTAs)
-      const int arow = f * P.Mp + mtile2 * 256 + rank * BM;
-      const int brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN + rank * (BN / 2);
       uint32_t it = 0;
-      for (int q = 0; q < P.Q; ++q)
+      for (int item = cl; item < nitems; item += ncl) {
+        const int t = item % tiles, fq = item / tiles, q = fq % P.Q, f = fq / P.Q;
+        const int mtile2 = t % mt2, ntile = t / mt2;
+        const int arow = f * P.Mp + mtile2 * 256 + rank * BM;
+        const int brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN + rank * (BN / 2);
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
           const int s = it % STAGES2;
           mbar_wait(&empty[s], ((it / STAGES2) & 1) ^ 1);
@@ -358,13 +366,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tma_load_3d_2sm(sA + s * A_STAGE, &mapA, &full[s], kb * BK, arow, q);
           tma_load_3d_2sm(sB + s * B2_STAGE, &mapB, &full[s], kb * BK, brow, q);
         }
+      }
     }
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {  // ---- MMA issuer (even CTA)
       uint32_t it = 0;
-      for (int q = 0; q < P.Q; ++q) {
-        const int b = q & 1;
-        mbar_wait(&tempty[b], ((q >> 1) & 1) ^ 1);
+      for (int item = cl, li = 0; item < nitems; item += ncl, ++li) {
+        const int b = li & 1;
+        mbar_wait(&tempty[b], ((li >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + b * BN;
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
@@ -384,13 +393,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const size_t plane = (size_t)P.F * P.Mp * P.Sp * 2;
-    uint8_t* out0 = P.R + ((size_t)(f * P.Mp + mtile2 * 256 + rank * BM + row) * P.Sp + (size_t)ntile * BNC) * 2;
-    for (int q = 0; q < P.Q; ++q) {
-      const int b = q & 1;
-      mbar_wait(&tfull[b], (q >> 1) & 1);
+    for (int item = cl, li = 0; item < nitems; item += ncl, ++li) {
+      const int t = item % tiles, fq = item / tiles, q = fq % P.Q, f = fq / P.Q;
+      const int mtile2 = t % mt2, ntile = t / mt2;
+      const int b = li & 1;
+      mbar_wait(&tfull[b], (li >> 1) & 1);
       tc_fence_after();
       const uint32_t pq = c_mod.p[q], mg = c_mod.magic[q];
-      uint8_t* out = out0 + (size_t)q * plane;
+      uint8_t* out = P.R + (size_t)q * plane +
+                     ((size_t)(f * P.Mp + mtile2 * 256 + rank * BM + row) * P.Sp + (size_t)ntile * BNC) * 2;
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + b * BN;
 #pragma unroll 1
       for (int c = 0; c < BNC / 32; ++c) {
@@ -788,6 +799,13 @@ cudaError_t oz_init() {
   return encode_fn() ? cudaSuccess : cudaErrorNotSupported;
 }
 
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    return n;
+  return 148;
+}
+
 bool use_pair() {
   static const bool on = oz::env_int("QTB_OZAKI_2SM", 1) != 0;
   return on;
@@ -820,11 +838,13 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   int* eB = B.eB + (size_t)bslot0 * Sp;
   cudaError_t e = cudaMemsetAsync(eB, 0xC0, (size_t)fcur * Sp * sizeof(int), stream);  // kNoExp
   if (e != cudaSuccess) return e;
+  ProfScope ps("k2_int8_residues", stream);
   oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + 255) / 256)), 256, 0, stream>>>(
       bh1, bh2, eB, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, B.ldb, B.bslice);
   oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
                         stream>>>(
       bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice);
+  ps.stop();
   count_launches(2);
   return cudaGetLastError();
 }
@@ -859,18 +879,26 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
       bslot0 = 0;
       if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
     }
+    ProfScope pr("k2_int8_residues", stream);
     oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n, (int)p,
                                                                      (int)f0, (int)Mp, (int)F);
-    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0};
-    if (use_pair())
-      oz_gemm2_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM2_SMEM, stream>>>(
-          mapA, mapB, gp);
+    pr.stop();
+    ProfScope pg("k2_int8_gemm", stream);
+    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0, (int)(Sp / BNC), fcur};
+    if (use_pair()) {
+      const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
+      const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
+      oz_gemm2_kernel<<<2 * clusters, GEMM_THREADS, GEMM2_SMEM, stream>>>(mapA, mapB, gp);
+    }
     else
       oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA,
                                                                                                          mapB, gp);
+    pg.stop();
     const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
+    ProfScope pc("k2_int8_crt", stream);
     oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, bslot0,
                                              (int)Mp, (int)Sp, (int)F, ldc, cslice);
+    pc.stop();
     count_launches(3);
     e = cudaGetLastError();
   }

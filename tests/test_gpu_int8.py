@@ -188,7 +188,7 @@ def test_int8_rejects_unsupported_contraction():
 # ----------------------------------------------------------- full products
 @pytest.mark.parametrize("m,n,s,p", [(40, 256, 520, 5), (130, 288, 512, 4)])
 def test_int8_tprod_against_reference_oracle(m, n, s, p):
-    """Shapes that select the int8 path by themselves (n, s >= 256), end to end
+    """Shapes that select the int8 path by themselves (n >= 256, n s >= 2^17), end to end
     through tprod_fast against the reference restatement (bar 1e-12)."""
     assert _native.lib().qt_gemm_algo(m, n, s, p) == INT8
     a = qt.gen_random_tensor(m, n, p, 21)
