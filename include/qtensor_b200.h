@@ -142,6 +142,19 @@ int qt_spectral_product_f64_device_ld_algo(const double* ahat1, const double* ah
                                            uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                            int algo, void* stream);
 
+/* Exact-int8 stage 2 against a fixed Â, for callers that feed B̂ in column
+ * chunks (the chunked multi-GPU pipeline): the 16 modular residues of Â are
+ * built once by qt_int8_plan_create and reused by every
+ * qt_int8_plan_multiply (same strides as qt_spectral_product_f64_device_ld;
+ * Â must stay valid until qt_int8_plan_destroy).  Bitwise identical to one
+ * qt_spectral_product_f64_device_ld_algo(..., QT_GEMM_INT8_EXACT) call on the
+ * whole B̂.  Requires n % 32 == 0 and n <= 8192. */
+int qt_int8_plan_create(const double* ahat1, const double* ahat2, uint64_t m, uint64_t n, uint64_t p,
+                        void* stream, void** plan);
+int qt_int8_plan_multiply(void* plan, const double* bhat1, const double* bhat2, double* chat1, double* chat2,
+                          uint64_t s, uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream);
+int qt_int8_plan_destroy(void* plan, void* stream);
+
 /* Definitional product tprod_naive = fold(bcirc(A) . unfold(B))
  * (tproduct.hpp:23-25, tproduct.cpp:49-53) without materialising bcirc:
  * C_k = sum_r A_{(k-r) mod p} (.) B_r on FP64 DMMA.  16 m n s p^2 real

@@ -718,6 +718,86 @@ int qt_spectral_product_f64_device_ld(const double* ah1, const double* ah2, cons
                                                 QT_GEMM_AUTO, stream);
 }
 
+namespace {
+struct Int8Plan {
+  OzakiA A;
+  const double2* ah1 = nullptr;
+  const double2* ah2 = nullptr;
+  int* flags = nullptr;  // [0] non-finite in Â (from create), [1] per multiply (Â or B̂ chunk)
+  int device = 0;
+};
+}  // namespace
+
+int qt_int8_plan_create(const double* ah1, const double* ah2, uint64_t m, uint64_t n, uint64_t p, void* stream,
+                        void** plan) {
+  t_err.clear();
+  if (!plan) return fail(QT_EINVAL, "int8 plan: null plan pointer");
+  *plan = nullptr;
+  int rc = check_dims(m, n, 1, p, "int8 plan");
+  if (rc) return rc;
+  if (m == 0 || n == 0 || n % 32 != 0 || n > 8192)
+    return fail(QT_EINVAL, "int8 plan: needs m > 0 and n %% 32 == 0, 0 < n <= 8192");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  Int8Plan* P = new Int8Plan;
+  P->ah1 = (const double2*)ah1;
+  P->ah2 = (const double2*)ah2;
+  P->device = dev;
+  cudaError_t e = cudaMallocAsync(&P->flags, 2 * sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(P->flags, 0, 2 * sizeof(int), st);
+  if (e == cudaSuccess) e = ozaki_prepare_a(P->ah1, P->ah2, m, n, p, P->flags, &P->A, st);
+  if (e != cudaSuccess) {
+    if (P->flags) cudaFreeAsync(P->flags, st);
+    delete P;
+    return cuda_fail(e, "int8 plan: residues of A");
+  }
+  *plan = P;
+  return QT_OK;
+}
+
+int qt_int8_plan_multiply(void* plan, const double* bh1, const double* bh2, double* ch1, double* ch2, uint64_t s,
+                          uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream) {
+  t_err.clear();
+  Int8Plan* P = (Int8Plan*)plan;
+  if (!P) return fail(QT_EINVAL, "int8 plan: null plan");
+  const uint64_t m = P->A.m, n = P->A.n, p = P->A.p;
+  int rc = check_dims(m, n, s, p, "int8 plan multiply");
+  if (rc) return rc;
+  if (s == 0) return QT_OK;
+  if (ldb < s || ldc < s || bslice < n * ldb || cslice < m * ldc || ldb > kIntMax || ldc > kIntMax)
+    return fail(QT_EINVAL, "int8 plan multiply: leading dimensions smaller than the matrices");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* flag = P->flags + 1;
+  cudaError_t e = cudaMemcpyAsync(flag, P->flags, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  OzakiB B;
+  if (e == cudaSuccess)
+    e = ozaki_prepare_b((const double2*)bh1, (const double2*)bh2, m, n, s, p, ldb, bslice, flag, true, &B, st);
+  if (e == cudaSuccess)
+    e = ozaki_multiply_prepared(P->A, B, (double2*)ch1, (double2*)ch2, ldc, cslice, flag, st);
+  if (B.res) {
+    const cudaError_t fe = ozaki_release(B, st);
+    if (e == cudaSuccess) e = fe;
+  }
+  // non-finite inputs: the fp64 DMMA kernels recompute this chunk (no-op otherwise)
+  if (e == cudaSuccess)
+    e = dmma_spectral_gemm(P->ah1, P->ah2, (const double2*)bh1, (const double2*)bh2, (double2*)ch1, (double2*)ch2,
+                           m, n, s, p, ldb, ldc, bslice, cslice, st, flag);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 plan multiply");
+}
+
+int qt_int8_plan_destroy(void* plan, void* stream) {
+  t_err.clear();
+  Int8Plan* P = (Int8Plan*)plan;
+  if (!P) return QT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = ozaki_release_a(P->A, st);
+  const cudaError_t fe = cudaFreeAsync(P->flags, st);
+  delete P;
+  if (e == cudaSuccess) e = fe;
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 plan destroy");
+}
+
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
   (void)m;
   (void)p;

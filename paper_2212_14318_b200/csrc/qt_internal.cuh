@@ -103,6 +103,18 @@ cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, co
                            uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
                            cudaStream_t stream);
 cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream);
+// X' residues of every frequency, prepared once and reused against many B'
+// (column chunks of B: the chunked multi-GPU pipeline, the e2e wavefront)
+struct OzakiA {
+  uint8_t* res = nullptr;
+  int* eA = nullptr;
+  uint64_t m = 0, n = 0, p = 0;
+};
+cudaError_t ozaki_prepare_a(const double2* ah1, const double2* ah2, uint64_t m, uint64_t n, uint64_t p, int* flag,
+                            OzakiA* out, cudaStream_t stream);
+cudaError_t ozaki_multiply_prepared(const OzakiA& A, OzakiB& B, double2* ch1, double2* ch2, uint64_t ldc,
+                                    uint64_t cslice, int* flag, cudaStream_t stream);
+cudaError_t ozaki_release_a(OzakiA& A, cudaStream_t stream);
 // DMMA kernels that run only if *only_if != 0 (nullptr: always)
 cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,

@@ -213,15 +213,25 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     double* C1 = (double*)(base + 4 * ab);
     double* C2 = (double*)(base + 4 * ab + cb);
     int& r = d.rc;
+    void* plan = nullptr;  // exact int8 stage 2: Â slab residues built once, reused by every chunk
+    if (r == QT_OK && algo == QT_GEMM_INT8_EXACT && rows[g] > 0)
+      r = qt_int8_plan_create(Ah1, Ah2, rows[g], n, p, d.comp, &plan);
     for (uint64_t j = 0; j < NJ && r == QT_OK; ++j) {
       const uint64_t cols = chunk_cols(j);
       cudaStreamWaitEvent(d.comp, arrived[g][j], 0);
       r = qt_qfft3_conj_f64_device(chunk_ptr(g, j, 0), chunk_ptr(g, j, 1), bhat_ptr(g, 0), bhat_ptr(g, 1), n, cols,
                                    p, d.comp);
-      if (r == QT_OK)
+      if (r == QT_OK && plan)
+        r = qt_int8_plan_multiply(plan, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q, C2 + 2 * j * Q, cols, cols, s,
+                                  n * cols, rows[g] * s, d.comp);
+      else if (r == QT_OK)
         r = qt_spectral_product_f64_device_ld_algo(Ah1, Ah2, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q,
                                                    C2 + 2 * j * Q, rows[g], n, cols, p, cols, s, n * cols,
                                                    rows[g] * s, algo, d.comp);
+    }
+    if (plan) {
+      const int dr = qt_int8_plan_destroy(plan, d.comp);
+      if (r == QT_OK) r = dr;
     }
     if (r == QT_OK) r = qt_qifft3_conj_f64_device(C1, C2, C1, C2, rows[g], s, p, d.comp);
     if (r == QT_OK) {

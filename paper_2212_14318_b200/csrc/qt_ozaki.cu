@@ -152,6 +152,7 @@ struct GemmParams {
   int Q, mt, Mp, Sp, KB, F;
   int bslot0;        // slot of this batch's first frequency in the B' buffer
   int nt, fcur;      // n tiles, slots in this batch (persistent pair kernel)
+  int aslot0;        // slot of this batch's first frequency in the X' buffer
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      const int arow = f * P.Mp + mtile * BM, brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN;
+      const int arow = (P.aslot0 + f) * P.Mp + mtile * BM, brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN;
       uint32_t it = 0;
       for (int q = 0; q < P.Q; ++q)
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
@@ -357,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       for (int item = cl; item < nitems; item += ncl) {
         const int t = item % tiles, fq = item / tiles, q = fq % P.Q, f = fq / P.Q;
         const int mtile2 = t % mt2, ntile = t / mt2;
-        const int arow = f * P.Mp + mtile2 * 256 + rank * BM;
+        const int arow = (P.aslot0 + f) * P.Mp + mtile2 * 256 + rank * BM;
         const int brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN + rank * (BN / 2);
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
           const int s = it % STAGES2;
@@ -849,27 +850,46 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   return cudaGetLastError();
 }
 
-// A side, GEMM and CRT for the frequency slots [0, p) against prepared B'
-// slots (B.all: slot f of B' is frequency slot f; else B' holds the batch)
-cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
-                     uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
-                     cudaStream_t stream) {
+// X' residues (and row exponents) of every frequency slot of A into A.res
+cudaError_t prep_a(const OzakiA& A, const double2* ah1, const double2* ah2, int* flag, cudaStream_t stream) {
+  using namespace oz;
+  const uint64_t Mp = pad_rows(A.m), Kp = 4 * A.n;
+  cudaError_t e = cudaSuccess;
+  if (Mp > 2 * A.m)
+    e = cudaMemset2DAsync(A.res + 2 * A.m * Kp, Mp * Kp, 0, (Mp - 2 * A.m) * Kp, (size_t)kQ * A.p, stream);
+  if (e != cudaSuccess) return e;
+  ProfScope pr("k2_int8_residues", stream);
+  oz_residue_a_kernel<<<dim3((unsigned)A.m, (unsigned)A.p), 256, 0, stream>>>(
+      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p);
+  pr.stop();
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// GEMM and CRT for the frequency slots [0, p) against prepared B' slots
+// (B.all: slot f of B' is frequency slot f; else B' is rebuilt per batch) and
+// either prepared X' slots (A != nullptr) or X' built per batch from Â.
+cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1,
+                     const double2* bh2, uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice,
+                     int* flag, cudaStream_t stream) {
   using namespace oz;
   const uint64_t n = B.n, s = B.s, p = B.p, Mp = pad_rows(m), Sp = pad_cols(s), Kp = 4 * n;
-  const uint64_t F = B.all ? batch_slots(p, a_slot_bytes(m, n, s), env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
-  if (F * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytesA = (size_t)kQ * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
-  const size_t offR = bytesA, offE = offR + bytesR, wsbytes = offE + F * Mp * sizeof(int);
+  const uint64_t per_slot = A ? (uint64_t)kQ * Mp * Sp * 2 : a_slot_bytes(m, n, s);
+  const uint64_t F = B.all ? batch_slots(p, per_slot, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  if (F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytesA = A ? 0 : (size_t)kQ * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
+  const size_t offR = bytesA, offE = offR + bytesR, wsbytes = offE + (A ? 0 : F * Mp * sizeof(int));
   uint8_t* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, wsbytes, stream);
   if (e != cudaSuccess) return e;
-  uint8_t* resA = ws;
+  uint8_t* resA = A ? A->res : ws;
   uint8_t* R = ws + offR;
-  int* eA = reinterpret_cast<int*>(ws + offE);
+  int* eA = A ? A->eA : reinterpret_cast<int*>(ws + offE);
   // rows [2m, Mp) of every X' slot are padding the residue kernel never writes
-  if (Mp > 2 * m) e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * F, stream);
+  if (!A && Mp > 2 * m)
+    e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * F, stream);
   CUtensorMap mapA, mapB;
-  if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, F * Mp, kQ, BM) ||
+  if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, (A ? p : F) * Mp, kQ, BM) ||
                            !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, use_pair() ? BN / 2 : BN)))
     e = cudaErrorInvalidValue;
   for (uint64_t f0 = 0; f0 < p && e == cudaSuccess; f0 += F) {
@@ -879,27 +899,32 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
       bslot0 = 0;
       if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
     }
-    ProfScope pr("k2_int8_residues", stream);
-    oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n, (int)p,
-                                                                     (int)f0, (int)Mp, (int)F);
-    pr.stop();
+    const int aslot0 = A ? (int)f0 : 0;
+    if (!A) {
+      ProfScope pr("k2_int8_residues", stream);
+      oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n,
+                                                                       (int)p, (int)f0, (int)Mp, (int)F);
+      pr.stop();
+      count_launches(1);
+    }
     ProfScope pg("k2_int8_gemm", stream);
-    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0, (int)(Sp / BNC), fcur};
+    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0, (int)(Sp / BNC), fcur,
+                  aslot0};
     if (use_pair()) {
       const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
       const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
       oz_gemm2_kernel<<<2 * clusters, GEMM_THREADS, GEMM2_SMEM, stream>>>(mapA, mapB, gp);
-    }
-    else
+    } else {
       oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA,
                                                                                                          mapB, gp);
+    }
     pg.stop();
     const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
     ProfScope pc("k2_int8_crt", stream);
-    oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA, B.eB, flag, ch1, ch2, (int)m, (int)s, (int)p, (int)f0, bslot0,
-                                             (int)Mp, (int)Sp, (int)F, ldc, cslice);
+    oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA + (size_t)aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m, (int)s,
+                                             (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice);
     pc.stop();
-    count_launches(3);
+    count_launches(2);
     e = cudaGetLastError();
   }
   const cudaError_t fe = cudaFreeAsync(ws, stream);
@@ -944,7 +969,43 @@ cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, co
                            uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
                            cudaStream_t stream) {
   if (m == 0 || B.s == 0) return cudaSuccess;
-  return multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
+  return multiply(nullptr, B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
+}
+
+cudaError_t ozaki_prepare_a(const double2* ah1, const double2* ah2, uint64_t m, uint64_t n, uint64_t p, int* flag,
+                            OzakiA* out, cudaStream_t stream) {
+  *out = OzakiA{};
+  if (n % 32 != 0 || n > 8192 || p == 0 || m == 0) return cudaErrorInvalidValue;
+  cudaError_t e = oz_init();
+  if (e != cudaSuccess) return e;
+  OzakiA A;
+  A.m = m;
+  A.n = n;
+  A.p = p;
+  const uint64_t Mp = pad_rows(m);
+  if (p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)oz::kQ * p * Mp * 4 * n;
+  if ((e = cudaMallocAsync(&A.res, bytes + (size_t)p * Mp * sizeof(int), stream)) != cudaSuccess) return e;
+  A.eA = reinterpret_cast<int*>(A.res + bytes);
+  if ((e = prep_a(A, ah1, ah2, flag, stream)) != cudaSuccess) {
+    cudaFreeAsync(A.res, stream);
+    return e;
+  }
+  *out = A;
+  return cudaSuccess;
+}
+
+cudaError_t ozaki_multiply_prepared(const OzakiA& A, OzakiB& B, double2* ch1, double2* ch2, uint64_t ldc,
+                                    uint64_t cslice, int* flag, cudaStream_t stream) {
+  if (A.m == 0 || B.s == 0) return cudaSuccess;
+  if (A.n != B.n || A.p != B.p || !B.all) return cudaErrorInvalidValue;
+  return multiply(&A, B, nullptr, nullptr, nullptr, nullptr, A.m, ch1, ch2, ldc, cslice, flag, stream);
+}
+
+cudaError_t ozaki_release_a(OzakiA& A, cudaStream_t stream) {
+  cudaError_t e = A.res ? cudaFreeAsync(A.res, stream) : cudaSuccess;
+  A = OzakiA{};
+  return e;
 }
 
 cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream) {

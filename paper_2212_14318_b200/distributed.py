@@ -17,6 +17,8 @@ every world size and chunk count (tests/test_gpu_parity.py).
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _native, shard
@@ -74,6 +76,14 @@ class RowShardedTProduct:
             _native.check(L.qt_qfft3_conj_f64_device(self.a[0].data_ptr(), self.a[1].data_ptr(),
                                                      self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh),
                           "qfft3_conj(A slab)")
+        plan = None
+        if rows and self.algo == 1:
+            # exact int8 stage 2: the residues of this rank's Â slab are built
+            # once per step and reused by every B̂ chunk
+            h = ctypes.c_void_p()
+            _native.check(L.qt_int8_plan_create(self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh,
+                                                ctypes.byref(h)), "int8 plan")
+            plan = h
         for j, (c0, c1) in enumerate(self.chunks):
             if works is not None:
                 works[j].wait()  # compute stream waits for chunk j only
@@ -84,10 +94,17 @@ class RowShardedTProduct:
                                                      self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), n, cols, p,
                                                      sh), "qfft3_conj(B chunk)")
             off = 16 * c0  # bytes: column c0 of every row of the C slab
-            _native.check(L.qt_spectral_product_f64_device_ld_algo(
-                self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(),
-                self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, rows, n, cols, p,
-                cols, s, n * cols, rows * s, self.algo, sh), "spectral_product(chunk)")
+            if plan is not None:
+                _native.check(L.qt_int8_plan_multiply(
+                    plan, self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), self.c[0].data_ptr() + off,
+                    self.c[1].data_ptr() + off, cols, cols, s, n * cols, rows * s, sh), "int8 plan multiply")
+            else:
+                _native.check(L.qt_spectral_product_f64_device_ld_algo(
+                    self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(),
+                    self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, rows, n, cols, p,
+                    cols, s, n * cols, rows * s, self.algo, sh), "spectral_product(chunk)")
+        if plan is not None:
+            _native.check(L.qt_int8_plan_destroy(plan, sh), "int8 plan destroy")
         if rows:
             _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
                                                       self.c[0].data_ptr(), self.c[1].data_ptr(), rows, s, p, sh),

@@ -212,3 +212,64 @@ def test_int8_host_slab_stream_bitwise_equals_device_path():
     qt.tprod_fast_device(dev(a.t1), dev(a.t2), dev(b.t1), dev(b.t2), c1, c2, m, n, s, p)
     torch.cuda.synchronize()
     assert bits_equal(host.t1, c1.cpu().numpy()) and bits_equal(host.t2, c2.cpu().numpy())
+
+
+# ------------------------------------------------ chunked / sharded drivers
+@pytest.mark.parametrize("world,nchunks", [(1, 1), (1, 5), (3, 4)])
+def test_int8_row_sharded_chunked_pipeline_bitwise(world, nchunks):
+    """The N > 1 pipeline with the int8 stage 2 (one residue plan per rank,
+    reused by every B̂ column chunk) equals tprod_fast bitwise, rank by rank."""
+    import torch
+    from paper_2212_14318_b200.distributed import RowShardedTProduct
+    m, n, s, p = 150, 256, 520, 6
+    assert _native.lib().qt_gemm_algo(m, n, s, p) == INT8
+    a = qt.gen_random_tensor(m, n, p, 41)
+    b = qt.gen_random_tensor(n, s, p, 42)
+    want = qt.tprod_fast(a, b)
+    for r in range(world):
+        sh = RowShardedTProduct(m, n, s, p, r, world, "cuda:0", nchunks=nchunks)
+        assert sh.algo == INT8
+        sh.load_a(a.t1, a.t2)
+        sh.load_b(b.t1, b.t2)
+        sh.step()
+        torch.cuda.synchronize()
+        c1, c2 = sh.result()
+        assert bits_equal(c1, want.t1[:, sh.lo:sh.hi]) and bits_equal(c2, want.t2[:, sh.lo:sh.hi]), (world, r)
+
+
+def test_int8_multi_driver_single_device_bitwise():
+    m, n, s, p = 130, 256, 520, 4
+    a = qt.gen_random_tensor(m, n, p, 51)
+    b = qt.gen_random_tensor(n, s, p, 52)
+    c = qt.tprod_fast(a, b)
+    cm = qt.tprod_fast_multi(a, b, [0])
+    assert bits_equal(c.t1, cm.t1) and bits_equal(c.t2, cm.t2)
+
+
+def test_int8_plan_chunks_bitwise_and_nonfinite_chunk():
+    """qt_int8_plan_*: chunks of B̂ against one Â plan equal the one-shot int8
+    product bitwise; a chunk holding inf falls back to fp64 for that chunk
+    only (equal to the DMMA result there)."""
+    import ctypes
+    torch = torch_cuda()
+    L = _native.lib()
+    m, n, s, p = 70, 64, 300, 5
+    ah, bh = random_spectral(m, n, s, p, 12)
+    full = spectral(ah, bh, m, n, s, p, INT8)
+    plan = ctypes.c_void_p()
+    _native.check(L.qt_int8_plan_create(ah[0].data_ptr(), ah[1].data_ptr(), m, n, p, None, ctypes.byref(plan)), "plan")
+    c = torch.zeros((2, p, m, s), dtype=torch.complex128, device="cuda")
+    chunks = [(0, 128), (128, 131), (131, 300)]
+    bb = bh.clone()
+    bb[1, 2, 7, 200] = float("inf")  # in the last chunk
+    for c0, c1 in chunks:
+        b = bb[:, :, :, c0:c1].contiguous()
+        _native.check(L.qt_int8_plan_multiply(plan, b[0].data_ptr(), b[1].data_ptr(), c[0].data_ptr() + 16 * c0,
+                                              c[1].data_ptr() + 16 * c0, c1 - c0, c1 - c0, s, n * (c1 - c0), m * s,
+                                              None), "plan multiply")
+    _native.check(L.qt_int8_plan_destroy(plan, None), "plan destroy")
+    torch.cuda.synchronize()
+    got = c.cpu().numpy()
+    assert bits_equal(got[..., :131], full[..., :131].cpu().numpy())
+    dm = spectral(ah, bb, m, n, s, p, DMMA, cols=(131, 300)).cpu().numpy()
+    assert bits_equal(got[..., 131:], dm[..., 131:])
