@@ -471,6 +471,12 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
   e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
   if (e == cudaSuccess)
     e = launch_spectral_gemm_ozaki(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, flag, stream);
+  if (e == cudaErrorMemoryAllocation) {
+    // not enough free HBM for the residue workspace: the fp64 kernels
+    // recompute the whole product unconditionally (always correct)
+    cudaGetLastError();
+    e = cudaMemsetAsync(flag, 0xff, sizeof(int), stream);
+  }
   if (e == cudaSuccess)
     e = dmma_spectral_gemm(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, flag);
   const cudaError_t fe = cudaFreeAsync(flag, stream);
