@@ -51,6 +51,7 @@ constexpr int kModuli[kQ] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 2
 struct ModTable {
   uint32_t p[kQ];
   uint32_t magic[kQ];  // floor(2^32 / p): quotient estimate off by at most one
+  uint32_t magic37[kQ];  // ceil(2^37 / p): exact quotient umulhi(v, .) >> 5 for v < 2^28
   uint32_t c1[kQ];     // 2^18 mod p
   uint32_t c2[kQ];     // 2^36 mod p
   uint32_t bias[kQ];   // multiple of p >= 2^25 (keeps the limb combination non-negative)
@@ -465,8 +466,14 @@ __device__ __forceinline__ Limbs to_limbs(double x, int e) {
 // table entries are constant-bank operands
 __device__ __forceinline__ uint32_t res_of(const Limbs& l, int q) {
   if (q == 0) return l.a0 & 0xffu;  // p_0 = 256: the low byte (two's complement)
+  // v < 2^27 (c2 a2 + bias in [0, 2^26 + 256), c1 a1 < 2^26 - 2^19, a0 < 2^18): the
+  // Granlund-Montgomery quotient with a 37-bit reciprocal is exact (error < 2^-9 < 1/p)
   const uint32_t v = (uint32_t)((int)c_mod.c2[q] * l.a2 + (int)c_mod.bias[q]) + c_mod.c1[q] * l.a1 + l.a0;
-  return mod_u32(v, c_mod.p[q], c_mod.magic[q]);
+  return v - (__umulhi(v, c_mod.magic37[q]) >> 5) * c_mod.p[q];
+}
+// four bytes (each < 256) into one little-endian word (3 PRMT)
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
 __device__ __forceinline__ uint32_t neg_res(uint32_t r, uint32_t p) { return r ? p - r : 0u; }
 
@@ -540,18 +547,19 @@ __global__ void __launch_bounds__(256, 3) oz_residue_a_kernel(const double2* __r
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
-      uint32_t wr1 = 0, wi1 = 0, wr2 = 0, wi2 = 0, wnr2 = 0, wni1 = 0;
+      uint32_t a[kAVec], b[kAVec], c[kAVec], d[kAVec], nc[kAVec], nb[kAVec];
 #pragma unroll
       for (int t = 0; t < kAVec; ++t) {
-        const int sh = t * 8;
-        const uint32_t a = res_of(r1[t], q), b = res_of(i1[t], q), c = res_of(r2[t], q), d = res_of(i2[t], q);
-        wr1 |= a << sh;
-        wi1 |= b << sh;
-        wr2 |= c << sh;
-        wi2 |= d << sh;
-        wnr2 |= neg_res(c, pq) << sh;
-        wni1 |= neg_res(b, pq) << sh;
+        a[t] = res_of(r1[t], q);
+        b[t] = res_of(i1[t], q);
+        c[t] = res_of(r2[t], q);
+        d[t] = res_of(i2[t], q);
+        nc[t] = neg_res(c[t], pq);
+        nb[t] = neg_res(b[t], pq);
       }
+      const uint32_t wr1 = pack4(a[0], a[1], a[2], a[3]), wi1 = pack4(b[0], b[1], b[2], b[3]);
+      const uint32_t wr2 = pack4(c[0], c[1], c[2], c[3]), wi2 = pack4(d[0], d[1], d[2], d[3]);
+      const uint32_t wnr2 = pack4(nc[0], nc[1], nc[2], nc[3]), wni1 = pack4(nb[0], nb[1], nb[2], nb[3]);
       uint8_t* u = up + (size_t)q * plane + j0;
       uint8_t* l = lo + (size_t)q * plane + j0;
       *reinterpret_cast<uint32_t*>(u) = wr1;
@@ -641,14 +649,15 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
-      uint32_t wr = 0, wi = 0, wni = 0;
+      uint32_t a[4], b[4], nb[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const uint32_t a = res_of(lr[t], q), b = res_of(li[t], q);
-        wr |= a << (8 * t);
-        wi |= b << (8 * t);
-        wni |= neg_res(b, pq) << (8 * t);
+        a[t] = res_of(lr[t], q);
+        b[t] = res_of(li[t], q);
+        nb[t] = neg_res(b[t], pq);
       }
+      const uint32_t wr = pack4(a[0], a[1], a[2], a[3]), wi = pack4(b[0], b[1], b[2], b[3]);
+      const uint32_t wni = pack4(nb[0], nb[1], nb[2], nb[3]);
       const size_t off = (size_t)q * plane;
       *reinterpret_cast<uint32_t*>(re_row + off) = wr;           // Re-row: Re Y
       *reinterpret_cast<uint32_t*>(re_row + off + 2 * n) = wni;  // Re-row: -Im Y
@@ -740,6 +749,7 @@ ModTable make_table() {
     const uint32_t p = (uint32_t)kModuli[q];
     t.p[q] = p;
     t.magic[q] = (uint32_t)((((uint64_t)1) << 32) / p);
+    t.magic37[q] = (uint32_t)(((((uint64_t)1) << 37) + p - 1) / p);
     t.c1[q] = (uint32_t)((((uint64_t)1) << 18) % p);
     t.c2[q] = (uint32_t)((((uint64_t)1) << 36) % p);
     t.bias[q] = (uint32_t)(((((uint64_t)1) << 25) + p - 1) / p * p);
