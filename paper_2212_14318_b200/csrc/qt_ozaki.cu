@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "qt_internal.cuh"
 
@@ -885,41 +886,96 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   using namespace oz;
   const uint64_t n = B.n, s = B.s, p = B.p, Mp = pad_rows(m), Sp = pad_cols(s), Kp = 4 * n;
   const uint64_t per_slot = A ? (uint64_t)kQ * Mp * Sp * 2 : a_slot_bytes(m, n, s);
-  const uint64_t F = B.all ? batch_slots(p, per_slot, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
-  if (F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytesA = A ? 0 : (size_t)kQ * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
-  const size_t offR = bytesA, offE = offR + bytesR, wsbytes = offE + (A ? 0 : F * Mp * sizeof(int));
+  // with B' prepared for every frequency the frequency batches are software-
+  // pipelined over two streams: the X' residues of batch i+1 and the CRT of
+  // batch i run beside the int8 GEMM of batch i+1 / i (their CTAs fit next to
+  // the GEMM's on every SM: ~0 KB smem, <= 128 regs), with X' and R double-
+  // buffered.  Without B.all (B' rebuilt per batch) the batches run in order.
+  const bool pipe = B.all && env_int("QTB_OZAKI_PIPE", 1) != 0;
+  const uint64_t nbuf = pipe ? 2 : 1;
+  const uint64_t F = B.all ? batch_slots(p, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  const uint64_t nbatch = (p + F - 1) / F;
+  if (nbuf * F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytesA = A ? 0 : (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
+  const size_t offR = bytesA, offE = offR + nbuf * bytesR, wsbytes = offE + (A ? 0 : nbuf * F * Mp * sizeof(int));
   uint8_t* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, wsbytes, stream);
   if (e != cudaSuccess) return e;
   uint8_t* resA = A ? A->res : ws;
-  uint8_t* R = ws + offR;
   int* eA = A ? A->eA : reinterpret_cast<int*>(ws + offE);
+  const uint64_t aslots = A ? p : nbuf * F;  // slots in the X' buffer (its plane stride)
   // rows [2m, Mp) of every X' slot are padding the residue kernel never writes
   if (!A && Mp > 2 * m)
-    e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * F, stream);
+    e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * aslots, stream);
   CUtensorMap mapA, mapB;
-  if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, (A ? p : F) * Mp, kQ, BM) ||
+  if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, aslots * Mp, kQ, BM) ||
                            !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, use_pair() ? BN / 2 : BN)))
     e = cudaErrorInvalidValue;
-  for (uint64_t f0 = 0; f0 < p && e == cudaSuccess; f0 += F) {
-    const int fcur = (int)std::min<uint64_t>(F, p - f0);
+  cudaStream_t aux = stream;
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&]() {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) evs.push_back(ev);
+    return ev;
+  };
+  if (e == cudaSuccess && pipe && nbatch > 1) {
+    e = cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+      cudaEvent_t fork = mkev();
+      cudaEventRecord(fork, stream);
+      cudaStreamWaitEvent(aux, fork, 0);
+    } else {
+      aux = stream;
+    }
+  }
+  auto batch = [&](uint64_t i, uint64_t& f0, int& fcur) {
+    f0 = i * F;
+    fcur = (int)std::min<uint64_t>(F, p - f0);
+  };
+  auto residues = [&](uint64_t i, cudaStream_t st) {
+    uint64_t f0;
+    int fcur;
+    batch(i, f0, fcur);
+    const uint64_t b = i % nbuf;
+    ProfScope pr("k2_int8_residues", st);
+    oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp, eA + b * F * Mp,
+                                                                 flag, (int)m, (int)n, (int)p, (int)f0, (int)Mp,
+                                                                 (int)aslots);
+    pr.stop();
+    count_launches(1);
+  };
+  auto crt = [&](uint64_t i, cudaStream_t st) {
+    uint64_t f0;
+    int fcur;
+    batch(i, f0, fcur);
+    const uint64_t b = i % nbuf;
+    const int bslot0 = B.all ? (int)f0 : 0;
+    const uint64_t aslot0 = A ? f0 : b * F;
+    const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
+    ProfScope pc("k2_int8_crt", st);
+    oz_crt_kernel<<<cgrid, 256, 0, st>>>(ws + offR + b * bytesR, eA + aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m,
+                                         (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice);
+    pc.stop();
+    count_launches(1);
+  };
+  if (e == cudaSuccess && !A) residues(0, stream);
+  cudaEvent_t res_ready = nullptr, prev_gemm_done = nullptr;
+  for (uint64_t i = 0; i < nbatch && e == cudaSuccess; ++i) {
+    uint64_t f0;
+    int fcur;
+    batch(i, f0, fcur);
+    const uint64_t b = i % nbuf;
     int bslot0 = (int)f0;
-    if (!B.all) {  // B' for this batch only
+    if (!B.all) {  // B' for this batch only (sequential schedule)
       bslot0 = 0;
       if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
+      if (!A && i > 0) residues(i, stream);
     }
-    const int aslot0 = A ? (int)f0 : 0;
-    if (!A) {
-      ProfScope pr("k2_int8_residues", stream);
-      oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, stream>>>(ah1, ah2, resA, eA, flag, (int)m, (int)n,
-                                                                       (int)p, (int)f0, (int)Mp, (int)F);
-      pr.stop();
-      count_launches(1);
-    }
+    // X' of batch i (and, by stream order on aux, the CRT of batch i-2 that used R[b]) ready
+    if (res_ready) cudaStreamWaitEvent(stream, res_ready, 0);
     ProfScope pg("k2_int8_gemm", stream);
-    GemmParams gp{R, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0, (int)(Sp / BNC), fcur,
-                  aslot0};
+    GemmParams gp{ws + offR + b * bytesR, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0,
+                  (int)(Sp / BNC), fcur, (int)(A ? f0 : b * F)};
     if (use_pair()) {
       const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
       const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
@@ -929,15 +985,35 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
                                                                                                          mapB, gp);
     }
     pg.stop();
-    const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
-    ProfScope pc("k2_int8_crt", stream);
-    oz_crt_kernel<<<cgrid, 256, 0, stream>>>(R, eA + (size_t)aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m, (int)s,
-                                             (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice);
-    pc.stop();
-    count_launches(2);
+    count_launches(1);
+    if (aux != stream) {
+      cudaEvent_t gemm_done = mkev();
+      cudaEventRecord(gemm_done, stream);
+      // aux: X' residues of batch i+1 into the other buffer (free once GEMM i-1,
+      // which precedes GEMM i on the main stream, is done), then the CRT of batch i
+      if (!A && i + 1 < nbatch) {
+        if (prev_gemm_done) cudaStreamWaitEvent(aux, prev_gemm_done, 0);  // GEMM i-1 read this X' buffer
+        residues(i + 1, aux);
+      }
+      res_ready = mkev();
+      cudaEventRecord(res_ready, aux);
+      cudaStreamWaitEvent(aux, gemm_done, 0);
+      crt(i, aux);
+      prev_gemm_done = gemm_done;
+    } else {
+      crt(i, stream);
+      if (!A && B.all && i + 1 < nbatch) residues(i + 1, stream);
+    }
     e = cudaGetLastError();
   }
+  if (aux != stream) {
+    cudaEvent_t join = mkev();
+    cudaEventRecord(join, aux);
+    cudaStreamWaitEvent(stream, join, 0);
+  }
   const cudaError_t fe = cudaFreeAsync(ws, stream);
+  if (aux != stream) cudaStreamDestroy(aux);
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
   return e != cudaSuccess ? e : fe;
 }
 
