@@ -659,11 +659,12 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
       }
       const uint32_t wr = pack4(a[0], a[1], a[2], a[3]), wi = pack4(b[0], b[1], b[2], b[3]);
       const uint32_t wni = pack4(nb[0], nb[1], nb[2], nb[3]);
-      const size_t off = (size_t)q * plane;
-      *reinterpret_cast<uint32_t*>(re_row + off) = wr;           // Re-row: Re Y
-      *reinterpret_cast<uint32_t*>(re_row + off + 2 * n) = wni;  // Re-row: -Im Y
-      *reinterpret_cast<uint32_t*>(im_row + off) = wi;           // Im-row: Im Y
-      *reinterpret_cast<uint32_t*>(im_row + off + 2 * n) = wr;   // Im-row: Re Y
+      *reinterpret_cast<uint32_t*>(re_row) = wr;           // Re-row: Re Y
+      *reinterpret_cast<uint32_t*>(re_row + 2 * n) = wni;  // Re-row: -Im Y
+      *reinterpret_cast<uint32_t*>(im_row) = wi;           // Im-row: Im Y
+      *reinterpret_cast<uint32_t*>(im_row + 2 * n) = wr;   // Im-row: Re Y
+      re_row += plane;
+      im_row += plane;
     }
   }
 }
@@ -682,37 +683,61 @@ __device__ __forceinline__ double crt_finish(uint64_t acc0, uint64_t acc1, uint6
   return scale2(frac * c_mod.M, e - 64);
 }
 
-// one thread per complex element of output rows r (slot f, row r of [C1; C2])
+// one thread per 4 consecutive complex elements of output rows r (slot f, row
+// r of [C1; C2]): 16 x 8-byte residue loads (pointer bumped by one plane per
+// modulus), 3 multiply-adds per residue into 64-bit limb accumulators
+constexpr int kCrtVec = 4;
 __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
                                                      const int* __restrict__ eB, const int* nonfinite,
                                                      double2* __restrict__ c1, double2* __restrict__ c2, int m,
                                                      int s, int p, int f0, int bslot0, int Mp, int Sp, int F,
                                                      uint64_t ldc, uint64_t cslice) {
   if (*nonfinite) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cb = (blockIdx.x * blockDim.x + threadIdx.x) * kCrtVec;
   const int f = blockIdx.z;
-  if (c >= s) return;
-  const int Eb = eB[(bslot0 + f) * Sp + c];
-  const int eb = Eb == kNoExp ? 0 : kBits - Eb;
+  if (cb >= s) return;
+  int eb[kCrtVec];
+#pragma unroll
+  for (int t = 0; t < kCrtVec; ++t) {
+    const int Eb = eB[(bslot0 + f) * Sp + cb + t];  // padding columns hold kNoExp
+    eb[t] = Eb == kNoExp ? 0 : kBits - Eb;
+  }
   const int k = slot_freq(f0 + f, p);
-  const size_t plane = (size_t)F * Mp * Sp;  // uchar2 elements
+  const size_t plane = (size_t)F * Mp * Sp * 2;  // bytes
   for (int r = blockIdx.y; r < 2 * m; r += gridDim.y) {
-    const uchar2* res = reinterpret_cast<const uchar2*>(R) + (size_t)(f * Mp + r) * Sp + c;
-    uint64_t x0 = 0, x1 = 0, x2 = 0, y0 = 0, y1 = 0, y2 = 0;
+    const uint8_t* ptr = R + ((size_t)(f * Mp + r) * Sp + cb) * 2;
+    uint64_t acc[kCrtVec][2][3];
+#pragma unroll
+    for (int t = 0; t < kCrtVec; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[t][h][0] = acc[t][h][1] = acc[t][h][2] = 0;
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
-      const uchar2 v = res[(size_t)q * plane];
-      x0 += (uint64_t)v.x * c_mod.w[q][0];
-      x1 += (uint64_t)v.x * c_mod.w[q][1];
-      x2 += (uint64_t)v.x * c_mod.w[q][2];
-      y0 += (uint64_t)v.y * c_mod.w[q][0];
-      y1 += (uint64_t)v.y * c_mod.w[q][1];
-      y2 += (uint64_t)v.y * c_mod.w[q][2];
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(ptr));  // (re, im) bytes of 4 columns
+      ptr += plane;
+      const uint32_t w0 = c_mod.w[q][0], w1 = c_mod.w[q][1], w2 = c_mod.w[q][2];
+#pragma unroll
+      for (int t = 0; t < kCrtVec; ++t) {
+        const uint32_t word = t < 2 ? v.x : v.y;
+        const int sh = (t & 1) * 16;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t rr = (word >> (sh + 8 * h)) & 0xffu;
+          acc[t][h][0] += (uint64_t)rr * w0;
+          acc[t][h][1] += (uint64_t)rr * w1;
+          acc[t][h][2] += (uint64_t)rr * w2;
+        }
+      }
     }
-    const int e = -(eA[f * Mp + r] + eb);
-    const double2 v = make_double2(crt_finish(x0, x1, x2, e), crt_finish(y0, y1, y2, e));
-    if (r < m) c1[k * cslice + (size_t)r * ldc + c] = v;
-    else c2[k * cslice + (size_t)(r - m) * ldc + c] = v;
+    const int ea = eA[f * Mp + r];
+    double2* dst = (r < m) ? c1 + k * cslice + (size_t)r * ldc : c2 + k * cslice + (size_t)(r - m) * ldc;
+#pragma unroll
+    for (int t = 0; t < kCrtVec; ++t) {
+      if (cb + t >= s) break;
+      const int e = -(ea + eb[t]);
+      dst[cb + t] = make_double2(crt_finish(acc[t][0][0], acc[t][0][1], acc[t][0][2], e),
+                                 crt_finish(acc[t][1][0], acc[t][1][1], acc[t][1][2], e));
+    }
   }
 }
 
@@ -951,7 +976,8 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     const uint64_t b = i % nbuf;
     const int bslot0 = B.all ? (int)f0 : 0;
     const uint64_t aslot0 = A ? f0 : b * F;
-    const dim3 cgrid((unsigned)((s + 255) / 256), (unsigned)std::min<uint64_t>(2 * m, 65535), (unsigned)fcur);
+    const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 65535),
+                     (unsigned)fcur);
     ProfScope pc("k2_int8_crt", st);
     oz_crt_kernel<<<cgrid, 256, 0, st>>>(ws + offR + b * bytesR, eA + aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m,
                                          (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice);
