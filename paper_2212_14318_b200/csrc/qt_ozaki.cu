@@ -504,7 +504,7 @@ constexpr int kNoExp = (int)0xC0C0C0C0;  // column of zeros (cudaMemset byte 0xC
 //   X_sk row m + i = [Re A2_sk |  Re A1_k | Im A2_sk | -Im A1_k]
 // (X_sk's slot is f^1, or f itself for a self-paired frequency).
 constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32-bit word)
-__global__ void __launch_bounds__(256, 3) oz_residue_a_kernel(const double2* __restrict__ a1,
+__global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __restrict__ a1,
                                                            const double2* __restrict__ a2, uint8_t* __restrict__ out,
                                                            int* __restrict__ eA, int* nonfinite, int m, int n, int p,
                                                            int f0, int Mp, int F) {
@@ -535,42 +535,44 @@ __global__ void __launch_bounds__(256, 3) oz_residue_a_kernel(const double2* __r
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * Mp * Kp;
   uint8_t* up = out + (size_t)(f * Mp + i) * Kp;
   uint8_t* lo = out + (size_t)(fpart * Mp + m + i) * Kp;
-  for (int j0 = threadIdx.x * kAVec; j0 < n; j0 += blockDim.x * kAVec) {
-    Limbs r1[kAVec], i1[kAVec], r2[kAVec], i2[kAVec];
+  // work unit: 4 consecutive elements of ONE source row (P = A1_k[i] or Q = A2_sk[i]);
+  // each residue goes to two places (one per output row)
+  const int nq = n / kAVec;
+  for (int u = threadIdx.x; u < 2 * nq; u += blockDim.x) {
+    const bool isP = u < nq;
+    const int j0 = (isP ? u : u - nq) * kAVec;
+    const double2* src = isP ? P : Qr;
+    Limbs re[kAVec], im[kAVec];
 #pragma unroll
     for (int t = 0; t < kAVec; ++t) {
-      const double2 x = P[j0 + t], y = Qr[j0 + t];
-      r1[t] = to_limbs(x.x, e);
-      i1[t] = to_limbs(x.y, e);
-      r2[t] = to_limbs(y.x, e);
-      i2[t] = to_limbs(y.y, e);
+      const double2 x = src[j0 + t];
+      re[t] = to_limbs(x.x, e);
+      im[t] = to_limbs(x.y, e);
     }
+    // P: up[0n] = Re, lo[1n] = Re, up[2n] = Im, lo[3n] = -Im
+    // Q: lo[0n] = Re, up[1n] = -Re, lo[2n] = Im, up[3n] = Im
+    uint8_t* pa = (isP ? up : lo) + j0;             // Re, plain
+    uint8_t* pb = (isP ? lo + n : up + n) + j0;     // Re (P) / -Re (Q)
+    uint8_t* pc = (isP ? up : lo) + 2 * n + j0;     // Im, plain
+    uint8_t* pd = (isP ? lo : up) + 3 * n + j0;     // -Im (P) / Im (Q)
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
-      uint32_t a[kAVec], b[kAVec], c[kAVec], d[kAVec], nc[kAVec], nb[kAVec];
+      uint32_t a[kAVec], b[kAVec], na[kAVec], nb[kAVec];
 #pragma unroll
       for (int t = 0; t < kAVec; ++t) {
-        a[t] = res_of(r1[t], q);
-        b[t] = res_of(i1[t], q);
-        c[t] = res_of(r2[t], q);
-        d[t] = res_of(i2[t], q);
-        nc[t] = neg_res(c[t], pq);
+        a[t] = res_of(re[t], q);
+        b[t] = res_of(im[t], q);
+        na[t] = neg_res(a[t], pq);
         nb[t] = neg_res(b[t], pq);
       }
-      const uint32_t wr1 = pack4(a[0], a[1], a[2], a[3]), wi1 = pack4(b[0], b[1], b[2], b[3]);
-      const uint32_t wr2 = pack4(c[0], c[1], c[2], c[3]), wi2 = pack4(d[0], d[1], d[2], d[3]);
-      const uint32_t wnr2 = pack4(nc[0], nc[1], nc[2], nc[3]), wni1 = pack4(nb[0], nb[1], nb[2], nb[3]);
-      uint8_t* u = up + (size_t)q * plane + j0;
-      uint8_t* l = lo + (size_t)q * plane + j0;
-      *reinterpret_cast<uint32_t*>(u) = wr1;
-      *reinterpret_cast<uint32_t*>(u + n) = wnr2;
-      *reinterpret_cast<uint32_t*>(u + 2 * n) = wi1;
-      *reinterpret_cast<uint32_t*>(u + 3 * n) = wi2;
-      *reinterpret_cast<uint32_t*>(l) = wr2;
-      *reinterpret_cast<uint32_t*>(l + n) = wr1;
-      *reinterpret_cast<uint32_t*>(l + 2 * n) = wi2;
-      *reinterpret_cast<uint32_t*>(l + 3 * n) = wni1;
+      const uint32_t wa = pack4(a[0], a[1], a[2], a[3]), wb = pack4(b[0], b[1], b[2], b[3]);
+      const uint32_t wna = pack4(na[0], na[1], na[2], na[3]), wnb = pack4(nb[0], nb[1], nb[2], nb[3]);
+      const size_t off = (size_t)q * plane;
+      *reinterpret_cast<uint32_t*>(pa + off) = wa;
+      *reinterpret_cast<uint32_t*>(pb + off) = isP ? wa : wna;
+      *reinterpret_cast<uint32_t*>(pc + off) = wb;
+      *reinterpret_cast<uint32_t*>(pd + off) = isP ? wnb : wb;
     }
   }
 }
