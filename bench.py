@@ -8,8 +8,9 @@ override with --config {1..5}.  One step = one full T-product C = A *_T B
 over inputs already resident in HBM.  K2 runs as the exact int8 tcgen05
 product (Ozaki-II, csrc/qt_ozaki.cu) for wide products (configs 5 and larger)
 and on the fp64 DMMA tensor cores otherwise (qt_gemm_algo).  With N ranks (torchrun) the rows
-of A and C are sharded in slabs of ceil(m/N) and B is broadcast from rank 0
-with NCCL inside the timed step (strong scaling: total work fixed).
+of A and C are sharded in slabs of ceil(m/N) and B's column chunks are
+broadcast with NCCL from the ranks that own them inside the timed step
+(strong scaling: total work fixed).
 
 metric value = F_eff / step time, F_eff = 32 m n s p + 10 (mn + ns + ms) p log2 p
 (SURVEY §8(d)).  e2e = the same metric through the host-buffer C-ABI call
@@ -290,7 +291,7 @@ def run_ours(args, cfg):
                                        dc1.data_ptr(), dc2.data_ptr(), rows, cfg.n, cfg.s, cfg.p, sh)
             qt._native.check(rc, "tprod_fast")
     else:
-        # rows of A/C sharded; B broadcast from rank 0 in column chunks that
+        # rows of A/C sharded; B broadcast in column chunks (each from the rank that owns it) that
         # overlap K1/K2 (paper_2212_14318_b200/distributed.py)
         from paper_2212_14318_b200.distributed import RowShardedTProduct
         sharded = RowShardedTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
@@ -298,19 +299,19 @@ def run_ours(args, cfg):
         # pinned host copies for the e2e leg: this rank's A slab (+ B chunks on rank 0)
         pin_a = torch.empty(sharded.a.shape, dtype=torch.float64, pin_memory=True)
         pin_a.copy_(sharded.a)
-        pin_b = []
-        if rank == 0:
-            sharded.load_b(b.t1, b.t2)
-            for t in sharded.bc:
+        pin_b = []  # pinned copies of the B chunks this rank owns (and uploads)
+        sharded.load_b(b.t1, b.t2)
+        for j, t in enumerate(sharded.bc):
+            if sharded.owned(j):
                 pb = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
                 pb.copy_(t)
-                pin_b.append(pb)
+                pin_b.append((t, pb))
         del a, b
         da1, da2 = sharded.a[0], sharded.a[1]
         dc1, dc2 = sharded.c[0], sharded.c[1]
 
-        def bcast(t):
-            return dist.broadcast(t, 0, async_op=True)
+        def bcast(t, src):
+            return dist.broadcast(t, src, async_op=True)
 
         if world == 1:
             bcast = None
@@ -353,13 +354,12 @@ def run_ours(args, cfg):
 
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
     # (full-B stage kernels; with N > 1 ranks the rank-0-shaped K2 on its slab)
-    if sharded_mode:  # full B for the stage kernels: assemble rank 0's chunks (zeros elsewhere)
+    if sharded_mode:  # full B for the stage kernels: every rank holds every chunk after a step
         db1 = torch.zeros((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
         db2 = torch.zeros_like(db1)
-        if rank == 0:
-            for (c0, c1_), t in zip(sharded.chunks, sharded.bc):
-                db1[:, :, 2 * c0:2 * c1_].copy_(t[0])
-                db2[:, :, 2 * c0:2 * c1_].copy_(t[1])
+        for (c0, c1_), t in zip(sharded.chunks, sharded.bc):
+            db1[:, :, 2 * c0:2 * c1_].copy_(t[0])
+            db2[:, :, 2 * c0:2 * c1_].copy_(t[1])
     ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
     bh = torch.empty((2, cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
     qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
@@ -503,7 +503,7 @@ def run_ours(args, cfg):
 
         def e2e_step():  # per rank: A slab (+ B on rank 0) H2D, broadcast + pipeline, C slab D2H
             sharded.a.copy_(pin_a, non_blocking=True)
-            for t, pb in zip(sharded.bc, pin_b):
+            for t, pb in pin_b:
                 t.copy_(pb, non_blocking=True)
             sharded.step(broadcast=bcast)
             pin_c.copy_(sharded.c, non_blocking=True)
@@ -522,7 +522,7 @@ def run_ours(args, cfg):
         e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
-               "api": "per rank: pinned A slab (+ B on rank 0) H2D, chunked NCCL broadcast, "
+               "api": "per rank: pinned A slab + the B chunks it owns H2D, chunked NCCL broadcasts from the owners, "
                       "qt_* device pipeline, pinned C slab D2H; max over ranks"}
 
     cpu = None
@@ -541,7 +541,7 @@ def run_ours(args, cfg):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                       "parallelism": f"rows{world}" + ("+bcastB(chunked)" if world > 1 else "")
+                       "parallelism": f"rows{world}" + ("+bcastB(chunked, owner-rooted)" if world > 1 else "")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
                        "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
                        "flops_eff_per_step": cfg.flops_eff},

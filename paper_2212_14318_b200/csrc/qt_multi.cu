@@ -4,9 +4,9 @@
 // this is the B200-native scale-out of tprod_fast (tproduct.cpp:75-111):
 //   * rows of A and C are split into contiguous slabs of ceil(m/G) rows — row i
 //     of C depends only on row i of A and all of B, so slabs are independent;
-//   * B is the only exchange: devices[0] uploads it column chunk by column
-//     chunk and each chunk is broadcast over NVLink / NVSwitch with
-//     ncclBroadcast on a communication stream; every device's compute stream
+//   * B is the only exchange: column chunk j is uploaded by device j mod G
+//     (each device moves ~1/G of B over its own PCIe link) and broadcast from
+//     it over NVLink / NVSwitch with ncclBroadcast on a communication stream; every device's compute stream
 //     waits only for the chunk it needs, transforms it (K1) and multiplies it
 //     into the matching columns of its C slab (strided K2), so the broadcast of
 //     chunk j+1 overlaps the compute of chunk j;
@@ -169,16 +169,19 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     return (double*)((char*)st[g].buf + 4 * ab + 2 * cb + 2 * NJ * bchunk + plane * bchunk);
   };
 
-  // 2) B chunks: upload to devices[0] and broadcast (one NCCL group per chunk)
+  // 2) B chunks: chunk j is uploaded by device owner(j) = j mod ndev (so each
+  //    device moves ~1/ndev of B over its own PCIe link) and broadcast from it
+  //    (one NCCL group per chunk)
   std::vector<std::vector<cudaEvent_t>> arrived(ndev, std::vector<cudaEvent_t>(NJ, nullptr));
   for (uint64_t j = 0; j < NJ && !rc; ++j) {
     const uint64_t cols = chunk_cols(j);
-    cudaSetDevice(st[0].dev);
+    const int own = (int)(j % (uint64_t)ndev);
+    cudaSetDevice(st[own].dev);
     const size_t pitch = s * cx, width = cols * cx;
-    if (cudaMemcpy2DAsync(chunk_ptr(0, j, 0), width, b1 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
-                          st[0].comm) ||
-        cudaMemcpy2DAsync(chunk_ptr(0, j, 1), width, b2 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
-                          st[0].comm)) {
+    if (cudaMemcpy2DAsync(chunk_ptr(own, j, 0), width, b1 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[own].comm) ||
+        cudaMemcpy2DAsync(chunk_ptr(own, j, 1), width, b2 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[own].comm)) {
       rc = QT_ECUDA;
       break;
     }
@@ -187,9 +190,9 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     for (int g = 0; g < ndev; ++g) {
       cudaSetDevice(st[g].dev);
       // both planes of chunk j are contiguous: [plane0 (n*cols*p)][gap][plane1] — broadcast each plane
-      if (api.Broadcast(chunk_ptr(g, j, 0), chunk_ptr(g, j, 0), count / 2, ncclFloat64, 0, comms[g], st[g].comm) !=
+      if (api.Broadcast(chunk_ptr(g, j, 0), chunk_ptr(g, j, 0), count / 2, ncclFloat64, own, comms[g], st[g].comm) !=
               ncclSuccess ||
-          api.Broadcast(chunk_ptr(g, j, 1), chunk_ptr(g, j, 1), count / 2, ncclFloat64, 0, comms[g], st[g].comm) !=
+          api.Broadcast(chunk_ptr(g, j, 1), chunk_ptr(g, j, 1), count / 2, ncclFloat64, own, comms[g], st[g].comm) !=
               ncclSuccess)
         rc = QT_ENCCL;
     }

@@ -4,8 +4,9 @@ for the plumbing).
 
 Row i of C depends only on row i of A, and column j of C only on column j of
 B.  Rank r owns rows shard.row_slab(m, world, r) of A and C; B
-lives on rank 0 as NJ column chunks and is broadcast chunk by chunk
-(async NCCL collectives on the process group's stream).  The compute stream
+lives as NJ column chunks owned round-robin by the ranks (shard.column_chunks)
+and is broadcast chunk by chunk from each owner (async NCCL collectives on
+the process group's stream).  The compute stream
 transforms the A slab once, then for every chunk j waits only for chunk j's
 broadcast, transforms it (K1) and runs the paired-frequency GEMM (K2) straight
 into columns [c0_j, c1_j) of the C slab (qt_spectral_product_f64_device_ld);
@@ -34,9 +35,9 @@ class RowShardedTProduct:
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.lo, self.hi = shard.row_slab(m, world, rank)
         self.rows = self.hi - self.lo
-        q = -(-s // max(1, nchunks))
-        q = min(s, -(-q // 16) * 16)  # multiple of the GEMM column tile
-        self.chunks = [(c0, min(s, c0 + q)) for c0 in range(0, s, q)]
+        plan = shard.column_chunks(s, nchunks, world)  # multiples of the GEMM column tile
+        self.chunks = [(c0, c1) for c0, c1, _ in plan]
+        self.owner = [o for _, _, o in plan]
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.a = torch.empty((2, p, self.rows, 2 * n), **f64)
         self.ah = torch.empty_like(self.a)
@@ -56,22 +57,28 @@ class RowShardedTProduct:
             slab = np.ascontiguousarray(src[:, self.lo:self.hi]).view(np.float64)
             self.a[k].copy_(self.torch.from_numpy(slab))
 
-    def load_b(self, b1: np.ndarray, b2: np.ndarray) -> None:
-        """Rank 0: B (p, n, s) host planes into the chunk buffers."""
-        for t, (c0, c1) in zip(self.bc, self.chunks):
+    def owned(self, j: int) -> bool:
+        return self.owner[j] == self.rank
+
+    def load_b(self, b1: np.ndarray, b2: np.ndarray, owned_only: bool = True) -> None:
+        """The chunks of B (p, n, s host planes) this rank owns into their
+        buffers (all chunks with owned_only=False: one rank run without peers)."""
+        for j, (t, (c0, c1)) in enumerate(zip(self.bc, self.chunks)):
+            if owned_only and not self.owned(j):
+                continue
             for k, src in enumerate((b1, b2)):
                 t[k].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, :, c0:c1]).view(np.float64)))
 
     # ----------------------------------------------------------------- step
     def step(self, broadcast=None, stream=None) -> None:
-        """One T-product step.  `broadcast(tensor)` must enqueue an async
-        broadcast from rank 0 and return an object with .wait() (a
-        torch.distributed Work); None on a single rank."""
+        """One T-product step.  `broadcast(tensor, src)` must enqueue an async
+        broadcast from rank `src` (the chunk's owner) and return an object with
+        .wait() (a torch.distributed Work); None on a single rank."""
         torch = self.torch
         st = torch.cuda.current_stream() if stream is None else stream
         sh = st.cuda_stream
         L, n, s, p, rows = self.L, self.n, self.s, self.p, self.rows
-        works = [broadcast(t) for t in self.bc] if broadcast is not None else None
+        works = [broadcast(t, o) for t, o in zip(self.bc, self.owner)] if broadcast is not None else None
         if rows:
             _native.check(L.qt_qfft3_conj_f64_device(self.a[0].data_ptr(), self.a[1].data_ptr(),
                                                      self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh),

@@ -3,7 +3,8 @@
 Row i of C = A *_T B depends only on row i of A and all of B (every slice
 product and every tube transform is row-local), so the rows of A
 and C are split into contiguous slabs of ceil(m / world) rows and B is
-replicated by ONE broadcast from rank 0 — the only exchange on the path.  The
+replicated by broadcasts of its column chunks, each from the rank that owns
+(uploaded) it — the only exchange on the path.  The
 slab computation is the single-GPU pipeline unchanged, so the stitched result
 is bitwise identical to the one-GPU result for every world size.
 
@@ -23,6 +24,19 @@ def row_slab(m: int, world: int, rank: int) -> tuple[int, int]:
     lo = min(m, rank * slab)
     hi = min(m, lo + slab)
     return lo, hi
+
+
+def column_chunks(s: int, nchunks: int, world: int, tile: int = 16) -> list[tuple[int, int, int]]:
+    """B's column chunks as (c0, c1, owner): ~nchunks chunks of a multiple of
+    `tile` columns, owned round-robin.  The owner of chunk j holds (uploads)
+    those columns of B and is the root of their broadcast, so with G ranks each
+    rank moves ~1/G of B over its PCIe link and its NVLink egress instead of
+    rank 0 moving all of it."""
+    q = -(-s // max(1, nchunks))
+    q = min(s, -(-q // tile) * tile) if s else 0
+    if q == 0:
+        return []
+    return [(c0, min(s, c0 + q), j % max(1, world)) for j, c0 in enumerate(range(0, s, q))]
 
 
 def take_rows(t1: np.ndarray, t2: np.ndarray, lo: int, hi: int):

@@ -230,7 +230,7 @@ def test_int8_row_sharded_chunked_pipeline_bitwise(world, nchunks):
         sh = RowShardedTProduct(m, n, s, p, r, world, "cuda:0", nchunks=nchunks)
         assert sh.algo == INT8
         sh.load_a(a.t1, a.t2)
-        sh.load_b(b.t1, b.t2)
+        sh.load_b(b.t1, b.t2, owned_only=False)  # no peers here: this rank holds every chunk
         sh.step()
         torch.cuda.synchronize()
         c1, c2 = sh.result()

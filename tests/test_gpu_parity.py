@@ -258,7 +258,7 @@ def test_chunked_row_sharded_pipeline_bitwise(world, nchunks):
     for r in range(world):
         sh = RowShardedTProduct(m, n, s, p, r, world, "cuda:0", nchunks=nchunks)
         sh.load_a(a.t1, a.t2)
-        sh.load_b(b.t1, b.t2)
+        sh.load_b(b.t1, b.t2, owned_only=False)  # no peers here: this rank holds every chunk
         sh.step()
         torch.cuda.synchronize()
         c1, c2 = sh.result()

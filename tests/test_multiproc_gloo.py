@@ -77,3 +77,80 @@ def test_row_sharded_world2_equals_single(tmp_path, m, n, s, p):
     want = O.tprod_fast(a, b)
     assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
     assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
+
+
+def _worker_chunks(rank, world, port, m, n, s, p, nchunks, out_path):
+    """B in column chunks owned round-robin (shard.column_chunks): each rank
+    fills only the chunks it owns, every chunk is broadcast from its owner,
+    then each rank computes its C slab — the N > 1 bench pipeline's schedule."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2212_14318_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = O.gen_random_tensor(m, n, p, 21)
+    lo, hi = shard.row_slab(m, world, rank)
+    a_slab = shard.take_rows(a[0], a[1], lo, hi)
+    b_full = O.gen_random_tensor(n, s, p, 22)
+    plan = shard.column_chunks(s, nchunks, world, tile=1)
+    assert len(plan) >= 1 and plan[0][0] == 0 and plan[-1][1] == s
+    bufs = []
+    for (c0, c1, owner) in plan:
+        t1 = np.zeros((p, n, c1 - c0), np.complex128)
+        t2 = np.zeros((p, n, c1 - c0), np.complex128)
+        if owner == rank:  # only the owner holds (uploads) this chunk
+            t1[:] = b_full[0][:, :, c0:c1]
+            t2[:] = b_full[1][:, :, c0:c1]
+        bufs.append((t1, t2, owner))
+    works = []
+    for (t1, t2, owner) in bufs:
+        for t in (t1, t2):
+            works.append(dist.broadcast(torch.from_numpy(t.view(np.float64)), src=owner, async_op=True))
+    for w in works:
+        w.wait()
+    b1 = np.concatenate([t1 for t1, _, _ in bufs], axis=2)
+    b2 = np.concatenate([t2 for _, t2, _ in bufs], axis=2)
+    assert np.array_equal(b1.view(np.uint64), b_full[0].view(np.uint64))
+    assert np.array_equal(b2.view(np.uint64), b_full[1].view(np.uint64))
+    c = O.tprod_fast(a_slab, (b1, b2))
+    slab = -(-m // world)
+    buf = np.zeros((2, p, slab, s), np.complex128)
+    buf[0, :, :hi - lo] = c[0]
+    buf[1, :, :hi - lo] = c[1]
+    t = torch.from_numpy(buf.view(np.float64))
+    gathered = [torch.zeros_like(t) for _ in range(world)] if rank == 0 else None
+    dist.gather(t, gathered, dst=0)
+    if rank == 0:
+        c1 = np.zeros((p, m, s), np.complex128)
+        c2 = np.zeros((p, m, s), np.complex128)
+        for r, g in enumerate(gathered):
+            lo_r, hi_r = shard.row_slab(m, world, r)
+            gg = g.numpy().view(np.complex128)
+            c1[:, lo_r:hi_r] = gg[0, :, :hi_r - lo_r]
+            c2[:, lo_r:hi_r] = gg[1, :, :hi_r - lo_r]
+        np.savez(out_path, c1=c1, c2=c2)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,s,p,nchunks", [(9, 5, 7, 8, 3), (4, 3, 5, 6, 8)])
+def test_owner_rooted_chunk_broadcast_world2(tmp_path, m, n, s, p, nchunks):
+    import oracle as O
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_worker_chunks, args=(2, _free_port(), m, n, s, p, nchunks, out), nprocs=2, join=True)
+    got = np.load(out)
+    want = O.tprod_fast(O.gen_random_tensor(m, n, p, 21), O.gen_random_tensor(n, s, p, 22))
+    assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
+    assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
+
+
+def test_column_chunk_plan():
+    from paper_2212_14318_b200 import shard
+    plan = shard.column_chunks(2048, 8, 8)
+    assert [o for _, _, o in plan] == list(range(8)) and all(c1 - c0 == 256 for c0, c1, _ in plan)
+    plan = shard.column_chunks(70, 8, 3)
+    assert plan[0][0] == 0 and plan[-1][1] == 70 and all((c1 - c0) % 16 == 0 or c1 == 70 for c0, c1, _ in plan)
+    assert [o for _, _, o in plan] == [j % 3 for j in range(len(plan))]
+    assert shard.column_chunks(0, 8, 2) == []
