@@ -71,8 +71,11 @@ def reference_spectral(ah, bh):
 
 
 def rel(x, y):
-    return float(np.sqrt(sum(np.sum(np.abs(a - b) ** 2) for a, b in zip(x, y)) /
-                         sum(np.sum(np.abs(b) ** 2) for b in y)))
+    """Relative Frobenius error, computed on values normalised by max |y| (so
+    extreme magnitudes neither overflow nor underflow when squared)."""
+    sc = max(float(np.max(np.abs(b))) for b in y) or 1.0
+    return float(np.sqrt(sum(np.sum(np.abs(a / sc - b / sc) ** 2) for a, b in zip(x, y)) /
+                         sum(np.sum(np.abs(b / sc) ** 2) for b in y)))
 
 
 # ---------------------------------------------------------------- algorithm
@@ -273,3 +276,36 @@ def test_int8_plan_chunks_bitwise_and_nonfinite_chunk():
     assert bits_equal(got[..., :131], full[..., :131].cpu().numpy())
     dm = spectral(ah, bb, m, n, s, p, DMMA, cols=(131, 300)).cpu().numpy()
     assert bits_equal(got[..., 131:], dm[..., 131:])
+
+
+# ------------------------------------------------------------ magnitudes
+@pytest.mark.parametrize("sa,sb", [(2.0 ** 600, 2.0 ** -600), (2.0 ** -500, 2.0 ** -500), (2.0 ** 900, 2.0 ** -1000),
+                                   (2.0 ** -1030, 2.0 ** 40)])
+def test_int8_extreme_magnitudes_match_fp64(sa, sb):
+    """Row/column scaling covers the whole fp64 exponent range (exponents
+    outside +-1022 take the ldexp path; subnormal inputs and results)."""
+    m, n, s, p = 20, 64, 24, 3
+    ah, bh = random_spectral(m, n, s, p, 61)
+    ah = ah * sa
+    bh = bh * sb
+    c8 = spectral(ah, bh, m, n, s, p, INT8)
+    cd = spectral(ah, bh, m, n, s, p, DMMA)
+    x8 = (c8[0].cpu().numpy(), c8[1].cpu().numpy())
+    xd = (cd[0].cpu().numpy(), cd[1].cpu().numpy())
+    assert all(np.isfinite(v).all() for v in x8)
+    ref = reference_spectral(ah, bh)
+    assert rel(x8, xd) <= 1e-13 or rel(x8, ref) <= 1e-13
+
+
+def test_int8_zero_rows_and_columns():
+    m, n, s, p = 24, 64, 30, 4
+    ah, bh = random_spectral(m, n, s, p, 62)
+    ah[0, :, 3, :] = 0      # row 3 of every A1 slice
+    ah[1, :, 3, :] = 0
+    bh[:, :, :, 7] = 0      # column 7 of every B slice
+    c8 = spectral(ah, bh, m, n, s, p, INT8).cpu().numpy()
+    cd = spectral(ah, bh, m, n, s, p, DMMA).cpu().numpy()
+    assert np.all(c8[..., 7] == 0)
+    ref = reference_spectral(ah, bh)
+    assert rel((c8[0], c8[1]), ref) <= 1e-13
+    assert rel((c8[0], c8[1]), (cd[0], cd[1])) <= 1e-13

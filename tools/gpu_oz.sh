@@ -1,4 +1,3 @@
 cd /root/repo
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "multi or sharded or chunked or row_sharded" > gpurun_out/oz_t8.log 2>&1; echo "rc=$?" >> gpurun_out/oz_t8.log
-timeout 300 python bench.py --config 5 --no-cpu-baseline --steps 5 --warmup 3 --e2e-steps 1 --sharded > gpurun_out/oz_bench_c5s.json 2> gpurun_out/oz_bench_c5s.err; echo "c5s rc=$?" >> gpurun_out/oz_t8.log
+timeout 900 python -m pytest tests/test_gpu_int8.py -x -q > gpurun_out/oz_t8.log 2>&1; echo "rc=$?" >> gpurun_out/oz_t8.log
