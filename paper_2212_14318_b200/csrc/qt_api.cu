@@ -638,15 +638,27 @@ static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const doub
     return cleanup(cuda_fail(e, "K2 B residues"));
   tr.mark("B' residues ready", scomp);
 
-  // phase 2: A row slabs
-  cudaEvent_t sa_free[2] = {nullptr, nullptr}, cs_free[2] = {nullptr, nullptr};
+  // phase 2: A row slabs.  The last slab is split in two halves (when each
+  // keeps >= 128 rows) so the work left after the final upload — its compute
+  // and its copy-out — is halved.
+  std::vector<std::pair<uint64_t, uint64_t>> slabs;  // (first row, rows)
   for (uint64_t i = 0; i < NI; ++i) {
+    const uint64_t r0 = i * R, rows = std::min<uint64_t>(R, m - r0);
+    if (i == NI - 1 && NI > 1 && rows >= 256) {
+      slabs.emplace_back(r0, rows / 2);
+      slabs.emplace_back(r0 + rows / 2, rows - rows / 2);
+    } else {
+      slabs.emplace_back(r0, rows);
+    }
+  }
+  cudaEvent_t sa_free[2] = {nullptr, nullptr}, cs_free[2] = {nullptr, nullptr};
+  for (uint64_t i = 0; i < slabs.size(); ++i) {
     const int b = (int)(i & 1);
-    const uint64_t rows = std::min<uint64_t>(R, m - i * R);
+    const uint64_t row0 = slabs[i].first, rows = slabs[i].second;
     if (sa_free[b]) cudaStreamWaitEvent(sin, sa_free[b], 0);
     const size_t apitch = m * n * cx, awidth = rows * n * cx;
-    if ((e = cudaMemcpy2DAsync(SA[b][0], awidth, a1 + 2 * i * R * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)) ||
-        (e = cudaMemcpy2DAsync(SA[b][1], awidth, a2 + 2 * i * R * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)))
+    if ((e = cudaMemcpy2DAsync(SA[b][0], awidth, a1 + 2 * row0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)) ||
+        (e = cudaMemcpy2DAsync(SA[b][1], awidth, a2 + 2 * row0 * n, apitch, awidth, p, cudaMemcpyHostToDevice, sin)))
       return cleanup(cuda_fail(e, "H2D A slab"));
     cudaEvent_t in = mkev();
     cudaEventRecord(in, sin);
@@ -673,8 +685,8 @@ static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const doub
     cudaEventRecord(done, scomp);
     cudaStreamWaitEvent(sout, done, 0);
     const size_t cpitch = m * s * cx, cwidth = rows * s * cx;
-    if ((e = cudaMemcpy2DAsync(c1 + 2 * i * R * s, cpitch, CS[b][0], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)) ||
-        (e = cudaMemcpy2DAsync(c2 + 2 * i * R * s, cpitch, CS[b][1], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)))
+    if ((e = cudaMemcpy2DAsync(c1 + 2 * row0 * s, cpitch, CS[b][0], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)) ||
+        (e = cudaMemcpy2DAsync(c2 + 2 * row0 * s, cpitch, CS[b][1], cwidth, cwidth, p, cudaMemcpyDeviceToHost, sout)))
       return cleanup(cuda_fail(e, "D2H C slab"));
     cs_free[b] = mkev();
     cudaEventRecord(cs_free[b], sout);

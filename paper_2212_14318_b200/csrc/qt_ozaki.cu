@@ -920,7 +920,9 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   // buffered.  Without B.all (B' rebuilt per batch) the batches run in order.
   const bool pipe = B.all && env_int("QTB_OZAKI_PIPE", 1) != 0;
   const uint64_t nbuf = pipe ? 2 : 1;
-  const uint64_t F = B.all ? batch_slots(p, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  uint64_t F = B.all ? batch_slots(p, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  // at least 4 batches when pipelining, so residues/CRT have a GEMM to hide behind
+  if (pipe && p >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((p + 3) / 4 + 1) & ~uint64_t(1)));
   const uint64_t nbatch = (p + F - 1) / F;
   if (nbuf * F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
   const size_t bytesA = A ? 0 : (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;

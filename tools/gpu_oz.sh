@@ -1,3 +1,3 @@
 cd /root/repo
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_int8.py -x -q > gpurun_out/oz_t8.log 2>&1; echo "rc=$?" >> gpurun_out/oz_t8.log
+timeout 300 python tools/e2e_prof.py > gpurun_out/e2e_prof.log 2>&1; echo "rc=$?" >> gpurun_out/e2e_prof.log
