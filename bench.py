@@ -381,6 +381,25 @@ def run_ours(args, cfg):
     gemm_ms = timed(lambda: L.qt_spectral_product_f64_device(ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(),
                                                              bh[1].data_ptr(), dc1.data_ptr(), dc2.data_ptr(), rows,
                                                              cfg.n, cfg.s, cfg.p, sh), max(2, args.steps))
+    # stage-2 accuracy of the algorithm this workload takes, on this run's data:
+    # the int8 (exact modular) result against the fp64 DMMA result (both on the GPU)
+    accuracy = None
+    if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1:
+        c8 = torch.empty((2, cfg.p, rows, 2 * cfg.s), dtype=torch.float64, device=dev)
+        cd = torch.empty_like(c8)
+        for algo_id, dst in ((1, c8), (0, cd)):
+            qt._native.check(L.qt_spectral_product_f64_device_ld_algo(
+                ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), dst[0].data_ptr(),
+                dst[1].data_ptr(), rows, cfg.n, cfg.s, cfg.p, cfg.s, cfg.s, cfg.n * cfg.s, rows * cfg.s, algo_id, sh),
+                "spectral(accuracy)")
+        torch.cuda.synchronize()
+        num = float(torch.linalg.vector_norm(c8 - cd).item())
+        den = float(torch.linalg.vector_norm(cd).item())
+        accuracy = {"k2_int8_vs_fp64_dmma_rel_frob": num / den if den else 0.0,
+                    "note": "stage 2 of this step's operands evaluated both ways on the GPU; the int8 path is "
+                            "exact in integers (53-bit scaled inputs, one final rounding), tests/test_gpu_int8.py "
+                            "shows its error vs a long-double truth is <= the fp64 GEMM's"}
+        del c8, cd
     fftA_ms = timed(lambda: L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(),
                                                        ah[1].data_ptr(), rows, cfg.n, cfg.p, sh), max(3, args.steps))
     ifft_ms = timed(lambda: L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
@@ -540,6 +559,11 @@ def run_ours(args, cfg):
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
+            "arithmetic": ("fp64 tube FFTs; stage 2 evaluated exactly in integers on the int8 tensor cores "
+                           "(u8 x u8 -> s32 tcgen05 MMAs over 16 moduli, 96-bit CRT, one fp64 rounding)"
+                           if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1 else
+                           "fp64 throughout (tube FFTs; stage 2 on the fp64 DMMA tensor pipe)"),
+            "accuracy": accuracy,
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
                        "parallelism": f"rows{world}" + ("+bcastB(chunked, owner-rooted)" if world > 1 else "")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),

@@ -1,3 +1,4 @@
 cd /root/repo
 mkdir -p gpurun_out
-timeout 300 python tools/e2e_prof.py > gpurun_out/e2e_prof.log 2>&1; echo "rc=$?" >> gpurun_out/e2e_prof.log
+timeout 300 python bench.py --config 5 --no-cpu-baseline --steps 5 --warmup 3 --e2e-steps 1 > gpurun_out/oz_bench_c5.json 2> gpurun_out/oz_bench_c5.err; echo "c5 rc=$?"
+timeout 300 python bench.py --config 2 --no-cpu-baseline --steps 5 --warmup 3 --e2e-steps 1 > gpurun_out/oz_bench_c2.json 2> gpurun_out/oz_bench_c2.err; echo "c2 rc=$?"
