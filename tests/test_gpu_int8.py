@@ -309,3 +309,25 @@ def test_int8_zero_rows_and_columns():
     ref = reference_spectral(ah, bh)
     assert rel((c8[0], c8[1]), ref) <= 1e-13
     assert rel((c8[0], c8[1]), (cd[0], cd[1])) <= 1e-13
+
+
+def test_int8_random_shape_sweep():
+    """Seeded sweep of ragged shapes (n a multiple of 32; odd and even p;
+    m, s off every tile multiple; multi-batch budgets) against the fp64 path."""
+    import os
+    rng = np.random.default_rng(2024)
+    for it in range(14):
+        m = int(rng.integers(1, 300))
+        n = 32 * int(rng.integers(1, 12))
+        s = int(rng.integers(1, 300))
+        p = int(rng.integers(1, 14))
+        ah, bh = random_spectral(m, n, s, p, 100 + it)
+        if it % 3 == 0:
+            os.environ["QTB_OZAKI_WS_MB"] = "1"
+        try:
+            c8 = spectral(ah, bh, m, n, s, p, INT8)
+        finally:
+            os.environ.pop("QTB_OZAKI_WS_MB", None)
+        cd = spectral(ah, bh, m, n, s, p, DMMA)
+        e = rel((c8[0].cpu().numpy(), c8[1].cpu().numpy()), (cd[0].cpu().numpy(), cd[1].cpu().numpy()))
+        assert e <= 1e-13, (m, n, s, p, e)
