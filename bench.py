@@ -440,9 +440,9 @@ def run_ours(args, cfg):
     algo_txt = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
                 else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
     if algo == 1 and "k2_int8_gemm" in prof:
-        # exact int8 path: 16 modular GEMMs of the real-embedded (2m x 4n) . (4n x 2s) product per frequency
+        # exact int8 path: 15 modular GEMMs of the real-embedded (2m x 4n) . (4n x 2s) product per frequency
         k_ms = prof["k2_int8_gemm"]["ms_per_step"]
-        ops = 2.0 * 16 * (2 * rows) * (4 * cfg.n) * (2 * cfg.s) * cfg.p
+        ops = 2.0 * 15 * (2 * rows) * (4 * cfg.n) * (2 * cfg.s) * cfg.p
         ach = ops / (k_ms * 1e-3) / 1e12
         peak_i8 = 2.0 * peaks["bf16_tflops"]
         roof = {"kernel": "K2 int8 modular GEMM oz_gemm2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)",
@@ -450,9 +450,9 @@ def run_ours(args, cfg):
                 "op_type": "int8 x int8 -> int32 tensor ops (multiply-add = 2), i.e. TOPS",
                 "peak_source": f"2 x {peak_src} bf16_tflops (MEASURED_PEAKS.json); int8:bf16 dense = 4.5:2.25 "
                                "PFLOP/s nominal",
-                "algorithmic": "2 * 16 moduli * (2m)(4n)(2s) * p int8 ops per step (= 512 m n s p), "
+                "algorithmic": "2 * 15 moduli * (2m)(4n)(2s) * p int8 ops per step (= 480 m n s p), "
                                "launched in frequency batches",
-                "algorithm": "exact Ozaki-II: 53-bit scaled integers, 16 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
+                "algorithm": "exact Ozaki-II: 53-bit scaled integers (norm-bounded), 15 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
                 "kernel_ms": k_ms, "launches_per_step": prof["k2_int8_gemm"]["launches_per_step"],
                 "share_of_step": k_ms / ms,
                 "fp64_equivalent_tflops": 32.0 * rows * cfg.n * cfg.s * cfg.p / (k_ms * 1e-3) / 1e12,
@@ -560,7 +560,7 @@ def run_ours(args, cfg):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
             "arithmetic": ("fp64 tube FFTs; stage 2 evaluated exactly in integers on the int8 tensor cores "
-                           "(u8 x u8 -> s32 tcgen05 MMAs over 16 moduli, 96-bit CRT, one fp64 rounding)"
+                           "(u8 x u8 -> s32 tcgen05 MMAs over 15 moduli, 96-bit CRT, one fp64 rounding)"
                            if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1 else
                            "fp64 throughout (tube FFTs; stage 2 on the fp64 DMMA tensor pipe)"),
             "accuracy": accuracy,

@@ -125,7 +125,7 @@ int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
 
 /* Stage-2 algorithm for a product of this shape: QT_GEMM_DMMA (FP64 DMMA
  * tensor cores, mma.sync m8n8k4) or QT_GEMM_INT8_EXACT (exact integer
- * evaluation on the int8 tcgen05 tensor cores: 16 modular int8 GEMMs + CRT,
+ * evaluation on the int8 tcgen05 tensor cores: 15 modular int8 GEMMs + CRT,
  * fp64-accurate).  Depends on (n, s) only and on
  * $QTB_OZAKI (0 never, 1 auto, 2 whenever n allows).  A caller that splits one
  * product into row slabs or column chunks passes the full-shape choice to
@@ -143,7 +143,7 @@ int qt_spectral_product_f64_device_ld_algo(const double* ahat1, const double* ah
                                            int algo, void* stream);
 
 /* Exact-int8 stage 2 against a fixed Â, for callers that feed B̂ in column
- * chunks (the chunked multi-GPU pipeline): the 16 modular residues of Â are
+ * chunks (the chunked multi-GPU pipeline): the 15 modular residues of Â are
  * built once by qt_int8_plan_create and reused by every
  * qt_int8_plan_multiply (same strides as qt_spectral_product_f64_device_ld;
  * Â must stay valid until qt_int8_plan_destroy).  Bitwise identical to one

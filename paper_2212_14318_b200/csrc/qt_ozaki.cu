@@ -8,16 +8,19 @@
 // FP64 has no tcgen05 path on B200 (DMMA peaks at 37 TF/s), so the product is
 // evaluated EXACTLY in integers and rounded once:
 //   1. scale: every row of X_k and every column of Y_k gets a power of two so
-//      that its largest |re|, |im| lies in [2^(b-1), 2^b), b = 53, and is rounded
-//      to integers X', Y' (the only approximation: <= 2^-53 of the row/column
-//      maximum, i.e. fp64 input precision);
-//   2. residues: X' and Y' mod each of Q = 16 pairwise-coprime moduli <= 256, as
+//      that its largest |re|, |im| stays below 2^53 and its Euclidean norm below
+//      2^T (T = 58), and is rounded to integers X', Y' (the only approximation:
+//      <= 2^-53 of the row/column maximum, i.e. fp64 input precision, whenever
+//      the norm bound is not the tighter one — max/rms > sqrt(4n)/32 — and at
+//      most ~1 bit less otherwise);
+//   2. residues: X' and Y' mod each of Q = 15 pairwise-coprime moduli <= 256, as
 //      uint8 in [0, p) (K2r kernels, K-major, ready for TMA);
 //   3. int8 GEMMs: for each modulus, X'_q Y'_q on tcgen05.mma.kind::i8 (u8 x u8)
 //      with an int32 TMEM accumulator (exact: sum < 255^2 * 4n < 2^31 for
 //      n <= 8192), reduced mod p_q in the epilogue and stored as one byte per
 //      real output (K2g kernel);
-//   4. CRT: the 16 residues give X'Y' exactly (|X'Y'| < 2^121 < M/2 = 2^124.2),
+//   4. CRT: the 15 residues give X'Y' exactly (Cauchy-Schwarz: |x'.y'| <=
+//      ||x'|| ||y'|| < 2^116 < M/2 = 2^116.6),
 //      reconstructed as a 96-bit fixed-point fraction X'Y'/M, converted to
 //      double once and scaled back by 2^-(eX + eY) (K2c kernel).
 // The integer product is exact, so the result does not depend on tiling,
@@ -44,10 +47,10 @@
 namespace qtb {
 namespace oz {
 
-constexpr int kQ = 16;
+constexpr int kQ = 15;
 constexpr int kBits = 53;
-// pairwise coprime, <= 256; product M = 2^125.2
-constexpr int kModuli[kQ] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+// pairwise coprime, <= 256; product M = 2^117.6
+constexpr int kModuli[kQ] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197};
 
 struct ModTable {
   uint32_t p[kQ];
@@ -58,6 +61,7 @@ struct ModTable {
   uint32_t bias[kQ];   // multiple of p >= 2^25 (keeps the limb combination non-negative)
   uint32_t w[kQ][3];   // round(2^96 * y_q / p_q) mod 2^96, y_q = (M/p_q)^-1 mod p_q (CRT weights)
   double M;            // prod p_q (rounded)
+  int ebound;          // T = floor((log2 M - 1) / 2) - margin: ||x'||, ||y'|| < 2^T keeps |x'.y'| < M/2
 };
 __constant__ ModTable c_mod;
 
@@ -489,6 +493,18 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return v;
 }
 
+// deterministic block sum (fixed shuffle tree, then warps in order)
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+  return v;
+}
+
 // binary exponent E of a finite nonzero max (max < 2^E, max >= 2^(E-1))
 __device__ __forceinline__ int exp_of(double mx) {
   int E;
@@ -496,7 +512,18 @@ __device__ __forceinline__ int exp_of(double mx) {
   return E;
 }
 constexpr double kDblMax = 1.7976931348623157e308;
-constexpr int kNoExp = (int)0xC0C0C0C0;  // column of zeros (cudaMemset byte 0xC0); below every exponent
+constexpr int kNoExp = (int)0xC0C0C0C0;  // no nonzero value seen (cudaMemset byte 0xC0); below every exponent
+
+// Scale exponent of a row / column with max < 2^E and ||v|| / 2^E = ns (the
+// scaled Euclidean norm, >= 1/2): e = min(53 - E, T - E_ns - E) with
+// ns < 2^E_ns, so every scaled value has <= 53 bits AND ||v 2^e|| < 2^T.  By
+// Cauchy-Schwarz |x'.y'| <= ||x'|| ||y'|| < 2^2T < M/2, so the CRT recovers
+// the integer product; for data whose max/rms exceeds ~sqrt(K)/2^(T-53) the
+// first bound is the binding one (no precision below 53 bits is given up).
+__device__ __forceinline__ int scale_exponent(int E, double ns) {
+  const int Ens = exp_of(ns * (1.0 + 0x1p-30));  // margin for the rounded sum of squares
+  return min(kBits, c_mod.ebound - Ens) - E;
+}
 
 // A side: one CTA per (slot f, row i < m) handles the row pair
 // (A1_k[i], A2_sk[i]), which shares one exponent, and writes
@@ -527,7 +554,18 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
     if (threadIdx.x == 0) atomicExch(nonfinite, 1);
     return;
   }
-  const int e = mx == 0.0 ? 0 : kBits - exp_of(mx);
+  int e = 0;
+  if (mx != 0.0) {
+    const int E = exp_of(mx);
+    double ss = 0.0;  // sum of squares of the row scaled by 2^-E (each term <= 1)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double2 x = P[j], y = Qr[j];
+      const double a = scale2(x.x, -E), b = scale2(x.y, -E), c = scale2(y.x, -E), d = scale2(y.y, -E);
+      ss = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ss))));
+    }
+    ss = block_sum(ss, red);
+    e = scale_exponent(E, sqrt(ss));
+  }
   if (threadIdx.x == 0) {
     eA[f * Mp + i] = e;
     eA[fpart * Mp + m + i] = e;
@@ -577,32 +615,72 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   }
 }
 
-// B side, pass 1: per (slot f, column c) the binary exponent of the max over
-// Y_k[:, c] = [B1_k[:, c]; B2_k[:, c]], by atomicMax over row blocks of 256
-// (eB pre-filled with kNoExp; monotone, so the order of the atomics is moot)
+// B side, pass 1: per (slot f, column c, 256-row block z of Y_k[:, c] =
+// [B1_k[:, c]; B2_k[:, c]]) the local max exponent and the sum of squares
+// scaled by it, into part[z][f][c] (deterministic: no atomics on the sums)
+struct ColPart {
+  int E;      // kNoExp: the block is all zeros
+  double ss;  // sum of (|re|^2 + |im|^2) 2^-2E over the block
+};
 __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
-                                                          const double2* __restrict__ b2, int* __restrict__ eB,
-                                                          int* nonfinite, int n, int s, int p, int f0, int Sp,
+                                                          const double2* __restrict__ b2, ColPart* __restrict__ part,
+                                                          int* nonfinite, int n, int s, int p, int f0, int Sp, int F,
                                                           uint64_t ldb, uint64_t bslice) {
   __shared__ double red[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
   const int k = slot_freq(f0 + f, p);
-  const int jend = min(2 * n, (int)(blockIdx.z + 1) * 256);
+  const int j0 = blockIdx.z * 256, jend = min(2 * n, j0 + 256);
+  auto load = [&](int j) {
+    return (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
+  };
   double mx = 0.0;
   if (c < s)
-    for (int j = blockIdx.z * 256 + w; j < jend; j += 8) {
-      const double2 y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
+    for (int j = j0 + w; j < jend; j += 8) {
+      const double2 y = load(j);
       // a sum of magnitudes is inf/nan iff a component is (or the pair overflows)
       mx = fmax(mx, (fabs(y.x) + fabs(y.y) <= kDblMax) ? fmax(fabs(y.x), fabs(y.y))
                                                        : __longlong_as_double(0x7ff0000000000000ll));
     }
   red[w][threadIdx.x & 31] = mx;
   __syncthreads();
-  if (w == 0 && c < s) {
-    for (int t = 1; t < 8; ++t) mx = fmax(mx, red[t][threadIdx.x]);
-    if (!(mx <= kDblMax)) atomicExch(nonfinite, 1);
-    else if (mx != 0.0) atomicMax(&eB[f * Sp + c], exp_of(mx));
+  for (int t = 0; t < 8; ++t) mx = fmax(mx, red[t][threadIdx.x & 31]);
+  __syncthreads();
+  const bool finite = mx <= kDblMax;
+  const int E = (finite && mx != 0.0) ? exp_of(mx) : 0;
+  double ss = 0.0;
+  if (c < s && finite && mx != 0.0)
+    for (int j = j0 + w; j < jend; j += 8) {
+      const double2 y = load(j);
+      const double a = scale2(y.x, -E), b = scale2(y.y, -E);
+      ss = fma(a, a, fma(b, b, ss));
+    }
+  red[w][threadIdx.x & 31] = ss;
+  __syncthreads();
+  if (w == 0) {
+    for (int t = 1; t < 8; ++t) ss += red[t][threadIdx.x];
+    if (c < s && !finite) atomicExch(nonfinite, 1);
+    part[((size_t)blockIdx.z * F + f) * Sp + c] = ColPart{(c < s && finite && mx != 0.0) ? E : kNoExp, ss};
   }
+}
+
+// B side, pass 1b: combine the row-block partials of each column in order
+__global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* __restrict__ eB, int nz, int F,
+                                        int Sp, int fcur) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= fcur * Sp) return;
+  const int f = t / Sp, c = t - f * Sp;
+  int E = kNoExp;
+  for (int z = 0; z < nz; ++z) E = max(E, part[((size_t)z * F + f) * Sp + c].E);
+  int e = 0;
+  if (E != kNoExp) {
+    double ss = 0.0;
+    for (int z = 0; z < nz; ++z) {
+      const ColPart pz = part[((size_t)z * F + f) * Sp + c];
+      if (pz.E != kNoExp) ss += scale2(pz.ss, 2 * (pz.E - E));
+    }
+    e = scale_exponent(E, sqrt(ss));
+  }
+  eB[f * Sp + c] = e;
 }
 
 // B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
@@ -637,8 +715,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   if (jb >= 2 * n) return;
   for (int cc = ty; cc < 32; cc += 8) {
     const int c = c0 + cc;
-    const int E = eB[f * Sp + c];
-    const int e = E == kNoExp ? 0 : kBits - E;
+    const int e = eB[f * Sp + c];
     const int tcol = c / BNC, ic = c % BNC;
     uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp + jb;
     uint8_t* im_row = re_row + (size_t)BNC * Kp;
@@ -701,8 +778,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
   int eb[kCrtVec];
 #pragma unroll
   for (int t = 0; t < kCrtVec; ++t) {
-    const int Eb = eB[(bslot0 + f) * Sp + cb + t];  // padding columns hold kNoExp
-    eb[t] = Eb == kNoExp ? 0 : kBits - Eb;
+    eb[t] = eB[(bslot0 + f) * Sp + cb + t];
   }
   const int k = slot_freq(f0 + f, p);
   const size_t plane = (size_t)F * Mp * Sp * 2;  // bytes
@@ -794,6 +870,7 @@ ModTable make_table() {
     t.w[q][2] = (uint32_t)(w >> 64);
   }
   t.M = (double)M;
+  t.ebound = (int)std::floor((std::log2((double)M) - 1.0) / 2.0 - 0.05);
   return t;
 }
 
@@ -808,7 +885,7 @@ bool ozaki_supported(uint64_t n, uint64_t s) {
   // QTB_OZAKI: 0 = never, 1 = auto, 2 = whenever the shape allows.  Auto takes
   // the int8 path where it measured faster than DMMA on B200 (tools/oz_sweep.py:
   // 256^3 0.86x, n = 1920 s = 64 0.61x, s = 128 1.10x, 512^3 1.68x, 2048^3
-  // 3.3x): the 16 residue GEMMs need enough columns to amortise the residues
+  // 3.3x): the 15 residue GEMMs need enough columns to amortise the residues
   // of A.  Callers that split one product (row slabs, column chunks) decide
   // once on the full shape; m never enters (row shards agree by construction).
   static const int mode = oz::env_int("QTB_OZAKI", 1);
@@ -875,16 +952,21 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   const uint64_t Sp = pad_cols(B.s);
   uint8_t* res = B.res + (size_t)bslot0 * 2 * Sp * 4 * B.n;
   int* eB = B.eB + (size_t)bslot0 * Sp;
-  cudaError_t e = cudaMemsetAsync(eB, 0xC0, (size_t)fcur * Sp * sizeof(int), stream);  // kNoExp
+  const int nz = (int)((2 * B.n + 255) / 256);
+  ColPart* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, sizeof(ColPart) * nz * fcur * Sp, stream);
   if (e != cudaSuccess) return e;
   ProfScope ps("k2_int8_residues", stream);
-  oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + 255) / 256)), 256, 0, stream>>>(
-      bh1, bh2, eB, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, B.ldb, B.bslice);
+  oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)nz), 256, 0, stream>>>(
+      bh1, bh2, part, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice);
+  oz_colexp_finish_kernel<<<(unsigned)((fcur * Sp + 255) / 256), 256, 0, stream>>>(part, eB, nz, fcur, (int)Sp, fcur);
+  e = cudaFreeAsync(part, stream);
+  if (e != cudaSuccess) return e;
   oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
                         stream>>>(
       bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice);
   ps.stop();
-  count_launches(2);
+  count_launches(3);
   return cudaGetLastError();
 }
 
