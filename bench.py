@@ -416,12 +416,32 @@ def run_ours(args, cfg):
         step()
     torch.cuda.synchronize()
     L.qt_prof_enable(0)
-    prof = {}
-    for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_crt"):
-        t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
-        qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
-        if n_l.value:
-            prof[tag] = {"ms_per_step": t_ms.value / nprof, "launches_per_step": n_l.value / nprof}
+    def read_prof():
+        out = {}
+        for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_crt"):
+            t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
+            qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
+            if n_l.value:
+                out[tag] = {"ms_per_step": t_ms.value / nprof, "launches_per_step": n_l.value / nprof}
+        return out
+
+    prof = read_prof()
+    # the int8 GEMM alone on the SMs (frequency batches in order, no co-running
+    # residue/CRT kernels): the kernel's own rate, reported beside the live one
+    prof_iso = {}
+    if algo == 1:
+        old_pipe = os.environ.get("QTB_OZAKI_PIPE")
+        os.environ["QTB_OZAKI_PIPE"] = "0"
+        L.qt_prof_enable(1)
+        for _ in range(nprof):
+            step()
+        torch.cuda.synchronize()
+        L.qt_prof_enable(0)
+        prof_iso = read_prof()
+        if old_pipe is None:
+            del os.environ["QTB_OZAKI_PIPE"]
+        else:
+            os.environ["QTB_OZAKI_PIPE"] = old_pipe
     # keep the GPU under the same load for >= 1 s of clock samples
     # (iteration count from the max-over-ranks step time: identical on every rank)
     for _ in range(min(2000, int(math.ceil(1000.0 / max(ms, 1e-3))))):
@@ -460,6 +480,11 @@ def run_ours(args, cfg):
                                "kernels of neighbouring batches run beside this kernel (kernel_ms is its own "
                                "event-timed duration, which includes that sharing)",
                 "traffic": None}
+        if "k2_int8_gemm" in prof_iso:
+            iso_ms = prof_iso["k2_int8_gemm"]["ms_per_step"]
+            roof["isolated"] = {"kernel_ms": iso_ms, "achieved": ops / (iso_ms * 1e-3) / 1e12,
+                                "frac": ops / (iso_ms * 1e-3) / 1e12 / peak_i8,
+                                "note": "same kernel, batches in order (QTB_OZAKI_PIPE=0), nothing co-running"}
         traffic, traffic_src = ncu_traffic(cfg, "K2_int8_gemm", rows)
         roof["algorithmic_bytes"] = None
     elif gemm_ai >= ridge:
