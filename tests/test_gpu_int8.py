@@ -331,3 +331,16 @@ def test_int8_random_shape_sweep():
         cd = spectral(ah, bh, m, n, s, p, DMMA)
         e = rel((c8[0].cpu().numpy(), c8[1].cpu().numpy()), (cd[0].cpu().numpy(), cd[1].cpu().numpy()))
         assert e <= 1e-13, (m, n, s, p, e)
+
+
+def test_int8_maximum_contraction_length():
+    """n = 8192 (K' = 4n = 32768: the largest int8 contraction, 255^2 K' < 2^31)
+    with near-maximal residues, against the fp64 path."""
+    m, n, s, p = 6, 8192, 10, 2
+    ah, bh = random_spectral(m, n, s, p, 71)
+    c8 = spectral(ah, bh, m, n, s, p, INT8)
+    cd = spectral(ah, bh, m, n, s, p, DMMA)
+    e = rel((c8[0].cpu().numpy(), c8[1].cpu().numpy()), (cd[0].cpu().numpy(), cd[1].cpu().numpy()))
+    assert e <= 1e-13, e
+    with pytest.raises(ValueError):  # n = 8224 exceeds the exact-accumulation bound
+        spectral(*random_spectral(2, 8224, 2, 1, 1), 2, 8224, 2, 1, INT8)
