@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -824,8 +825,12 @@ static int tprod_host_impl(const double* a1, const double* a2, const double* b1,
   // rows and ~8 chunks of >= 64 columns (a multiple of the GEMM tile).
   // Products on the int8 K2 stream row slabs against resident B' residues.
   if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20) && choose_gemm_algo(n, s) == kAlgoOzaki) {
-    uint64_t R = std::max<uint64_t>(64, (m + 7) / 8);
-    R = (R + 63) / 64 * 64;
+    // ~16 slabs of >= 128 rows (measured on config 5: 4 slabs 196 ms, 8 slabs
+    // 182 ms, 16 slabs 175 ms end to end — finer slabs start computing sooner
+    // and leave less after the last upload)
+    const uint64_t nsl = (uint64_t)std::max(1, atoi(getenv("QTB_E2E_SLABS") ? getenv("QTB_E2E_SLABS") : "16"));
+    uint64_t R = std::max<uint64_t>(128, (m + nsl - 1) / nsl);
+    R = (R + 127) / 128 * 128;
     return tprod_host_slabs_ozaki(a1, a2, b1, b2, c1, c2, m, n, s, p, R, hc);
   }
   if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20)) {
