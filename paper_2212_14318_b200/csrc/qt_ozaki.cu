@@ -884,8 +884,8 @@ int env_int(const char* name, int dflt) {
 bool ozaki_supported(uint64_t n, uint64_t s) {
   // QTB_OZAKI: 0 = never, 1 = auto, 2 = whenever the shape allows.  Auto takes
   // the int8 path where it measured faster than DMMA on B200 (tools/oz_sweep.py:
-  // 256^3 0.86x, n = 1920 s = 64 0.61x, s = 128 1.10x, 512^3 1.68x, 2048^3
-  // 3.3x): the 15 residue GEMMs need enough columns to amortise the residues
+  // 256^3 0.96x, n = 1920 s = 64 0.69x, s = 128 1.28x, 512^3 1.88x, 2048^3
+  // 3.7x): the 15 residue GEMMs need enough columns to amortise the residues
   // of A.  Callers that split one product (row slabs, column chunks) decide
   // once on the full shape; m never enters (row shards agree by construction).
   static const int mode = oz::env_int("QTB_OZAKI", 1);
