@@ -340,7 +340,7 @@ def test_concurrent_host_calls_are_reentrant_and_bitwise():
     pinned arena and twiddle cache); each result equals its sequential twin."""
     import threading
     shapes = [(40, 24, 30, 16), (300, 64, 200, 32), (16, 16, 16, 4096), (5, 4, 3, 7), (260, 70, 130, 64),
-              (33, 17, 40, 12)]
+              (33, 17, 40, 12), (64, 256, 512, 8), (150, 288, 520, 5)]  # the last two take the int8 stage 2
     ins = [(qt.gen_random_tensor(m, n, p, 10 + i), qt.gen_random_tensor(n, s, p, 20 + i))
            for i, (m, n, s, p) in enumerate(shapes)]
     want = [qt.tprod_fast(a, b) for a, b in ins]
