@@ -270,11 +270,11 @@ def run_ours(args, cfg):
     sh = stream.cuda_stream
 
     lo, hi = shard.row_slab(cfg.m, world, rank)
-    rows = hi - lo
+    rows, cols = hi - lo, cfg.s  # this rank's block of C (whole C at N = 1)
     # N = 1: pinned host inputs (the e2e leg copies from them); N > 1: every
-    # rank regenerates A (sequential generator) and keeps its slab, rank 0 owns B
+    # rank regenerates A and B (sequential generator) and keeps the pieces it owns
     sharded_mode = world > 1 or args.sharded
-    a, b, _ = host_inputs(cfg, pinned=not sharded_mode, need_b=(world == 1 or rank == 0))
+    a, b, _ = host_inputs(cfg, pinned=not sharded_mode, need_b=True)
     l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     big = (cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s)) > 2 * 126e6
     if not sharded_mode:
@@ -291,33 +291,46 @@ def run_ours(args, cfg):
                                        dc1.data_ptr(), dc2.data_ptr(), rows, cfg.n, cfg.s, cfg.p, sh)
             qt._native.check(rc, "tprod_fast")
     else:
-        # rows of A/C sharded; B broadcast in column chunks (each from the rank that owns it) that
-        # overlap K1/K2 (paper_2212_14318_b200/distributed.py)
-        from paper_2212_14318_b200.distributed import RowShardedTProduct
-        sharded = RowShardedTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+        # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
+        # block arrive as pieces broadcast (NCCL) from their owners inside the
+        # step, overlapping K1 / stage 2 (paper_2212_14318_b200/distributed.py)
+        from paper_2212_14318_b200.distributed import Grid2DTProduct
+        sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+        gr, gc = sharded.gr, sharded.gc
         sharded.load_a(a.t1, a.t2)
-        # pinned host copies for the e2e leg: this rank's A slab (+ B chunks on rank 0)
-        pin_a = torch.empty(sharded.a.shape, dtype=torch.float64, pin_memory=True)
-        pin_a.copy_(sharded.a)
-        pin_b = []  # pinned copies of the B chunks this rank owns (and uploads)
         sharded.load_b(b.t1, b.t2)
-        for j, t in enumerate(sharded.bc):
-            if sharded.owned(j):
+        # pinned host copies of the pieces this rank owns (and uploads) for the e2e leg
+        pin_own = []
+        for k, t in enumerate(sharded.a):
+            if sharded.owns_a(k):
+                pa = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+                pa.copy_(t)
+                pin_own.append((t, pa))
+        for k, t in enumerate(sharded.b):
+            if sharded.owns_b(k):
                 pb = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
                 pb.copy_(t)
-                pin_b.append((t, pb))
+                pin_own.append((t, pb))
         del a, b
-        da1, da2 = sharded.a[0], sharded.a[1]
+        rows, cols = sharded.rows, sharded.cols
+        bcast_row = bcast_col = None
+        if world > 1:
+            # every rank creates every group, in the same order
+            row_groups = [dist.new_group([i * gc + k for k in range(gc)]) for i in range(gr)]
+            col_groups = [dist.new_group([k * gc + j for k in range(gr)]) for j in range(gc)]
+            if gc > 1:
+                bcast_row = lambda t, src: dist.broadcast(t, src, group=row_groups[sharded.i], async_op=True)
+            if gr > 1:
+                bcast_col = lambda t, src: dist.broadcast(t, src, group=col_groups[sharded.j], async_op=True)
+        # stage-timing operands of this rank's block shape
+        da1 = torch.randn((cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
+        da2 = torch.randn_like(da1)
+        db1 = torch.randn((cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
+        db2 = torch.randn_like(db1)
         dc1, dc2 = sharded.c[0], sharded.c[1]
 
-        def bcast(t, src):
-            return dist.broadcast(t, src, async_op=True)
-
-        if world == 1:
-            bcast = None
-
         def step():
-            sharded.step(broadcast=bcast)
+            sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
 
     # clocks are sampled from the first warm-up step through the per-kernel
     # timing loops, so short steps still yield samples under load
@@ -354,18 +367,12 @@ def run_ours(args, cfg):
 
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
     # (full-B stage kernels; with N > 1 ranks the rank-0-shaped K2 on its slab)
-    if sharded_mode:  # full B for the stage kernels: every rank holds every chunk after a step
-        db1 = torch.zeros((cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
-        db2 = torch.zeros_like(db1)
-        for (c0, c1_), t in zip(sharded.chunks, sharded.bc):
-            db1[:, :, 2 * c0:2 * c1_].copy_(t[0])
-            db2[:, :, 2 * c0:2 * c1_].copy_(t[1])
     ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
-    bh = torch.empty((2, cfg.p, cfg.n, 2 * cfg.s), dtype=torch.float64, device=dev)
+    bh = torch.empty((2, cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
     qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
                                                 rows, cfg.n, cfg.p, sh), "qfft3")
     qt._native.check(L.qt_qfft3_conj_f64_device(db1.data_ptr(), db2.data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(),
-                                                cfg.n, cfg.s, cfg.p, sh), "qfft3")
+                                                cfg.n, cols, cfg.p, sh), "qfft3")
 
     def timed(fn, reps):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
@@ -378,19 +385,20 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         return sum(s0.elapsed_time(e0) for s0, e0 in evs) / reps
 
-    gemm_ms = timed(lambda: L.qt_spectral_product_f64_device(ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(),
-                                                             bh[1].data_ptr(), dc1.data_ptr(), dc2.data_ptr(), rows,
-                                                             cfg.n, cfg.s, cfg.p, sh), max(2, args.steps))
+    algo = L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p)   # 0 = fp64 DMMA, 1 = exact int8 (tcgen05)
+    gemm_ms = timed(lambda: L.qt_spectral_product_f64_device_ld_algo(
+        ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), dc1.data_ptr(), dc2.data_ptr(), rows,
+        cfg.n, cols, cfg.p, cols, cols, cfg.n * cols, rows * cols, algo, sh), max(2, args.steps))
     # stage-2 accuracy of the algorithm this workload takes, on this run's data:
     # the int8 (exact modular) result against the fp64 DMMA result (both on the GPU)
     accuracy = None
-    if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1:
-        c8 = torch.empty((2, cfg.p, rows, 2 * cfg.s), dtype=torch.float64, device=dev)
+    if algo == 1:
+        c8 = torch.empty((2, cfg.p, rows, 2 * cols), dtype=torch.float64, device=dev)
         cd = torch.empty_like(c8)
         for algo_id, dst in ((1, c8), (0, cd)):
             qt._native.check(L.qt_spectral_product_f64_device_ld_algo(
                 ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), dst[0].data_ptr(),
-                dst[1].data_ptr(), rows, cfg.n, cfg.s, cfg.p, cfg.s, cfg.s, cfg.n * cfg.s, rows * cfg.s, algo_id, sh),
+                dst[1].data_ptr(), rows, cfg.n, cols, cfg.p, cols, cols, cfg.n * cols, rows * cols, algo_id, sh),
                 "spectral(accuracy)")
         torch.cuda.synchronize()
         num = float(torch.linalg.vector_norm(c8 - cd).item())
@@ -403,11 +411,10 @@ def run_ours(args, cfg):
     fftA_ms = timed(lambda: L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(),
                                                        ah[1].data_ptr(), rows, cfg.n, cfg.p, sh), max(3, args.steps))
     ifft_ms = timed(lambda: L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
-                                                        dc2.data_ptr(), rows, cfg.s, cfg.p, sh), max(3, args.steps))
+                                                        dc2.data_ptr(), rows, cols, cfg.p, sh), max(3, args.steps))
     del ah, bh
     # ---- per-kernel device time of the stage-2 GEMM kernel itself (library
     # CUDA events on the launching stream, qt_prof_*), over a few extra steps
-    algo = L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p)   # 0 = fp64 DMMA, 1 = exact int8 (tcgen05)
     nprof = max(2, args.steps)
     L.qt_prof_enable(1)
     for _ in range(nprof):
@@ -450,19 +457,19 @@ def run_ours(args, cfg):
     clk.__exit__(None, None, None)
     peaks, peak_src = load_peaks()
     gauss = os.environ.get("QTB_GEMM", "3m")[:1] != "4"
-    gemm_tf = 32.0 * rows * cfg.n * cfg.s * cfg.p / (gemm_ms * 1e-3) / 1e12   # algorithmic (reference) flops
+    gemm_tf = 32.0 * rows * cfg.n * cols * cfg.p / (gemm_ms * 1e-3) / 1e12   # algorithmic (reference) flops
     exec_tf = gemm_tf * (0.75 if gauss else 1.0)                              # DMMA flops actually executed
     fftA_gbs = 2 * cfg.bytes_tensor(rows, cfg.n) / (fftA_ms * 1e-3) / 1e9
-    ifft_gbs = 2 * cfg.bytes_tensor(rows, cfg.s) / (ifft_ms * 1e-3) / 1e9
-    gemm_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s) + cfg.bytes_tensor(rows, cfg.s)
-    gemm_ai = 32.0 * rows * cfg.n * cfg.s * cfg.p / gemm_bytes
+    ifft_gbs = 2 * cfg.bytes_tensor(rows, cols) / (ifft_ms * 1e-3) / 1e9
+    gemm_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cols) + cfg.bytes_tensor(rows, cols)
+    gemm_ai = 32.0 * rows * cfg.n * cols * cfg.p / gemm_bytes
     ridge = PEAK_FP64_DMMA_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
     algo_txt = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
                 else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
     if algo == 1 and "k2_int8_gemm" in prof:
         # exact int8 path: 15 modular GEMMs of the real-embedded (2m x 4n) . (4n x 2s) product per frequency
         k_ms = prof["k2_int8_gemm"]["ms_per_step"]
-        ops = 2.0 * 15 * (2 * rows) * (4 * cfg.n) * (2 * cfg.s) * cfg.p
+        ops = 2.0 * 15 * (2 * rows) * (4 * cfg.n) * (2 * cols) * cfg.p
         ach = ops / (k_ms * 1e-3) / 1e12
         peak_i8 = 2.0 * peaks["bf16_tflops"]
         roof = {"kernel": "K2 int8 modular GEMM oz_gemm2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)",
@@ -475,7 +482,7 @@ def run_ours(args, cfg):
                 "algorithm": "exact Ozaki-II: 53-bit scaled integers (norm-bounded), 15 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
                 "kernel_ms": k_ms, "launches_per_step": prof["k2_int8_gemm"]["launches_per_step"],
                 "share_of_step": k_ms / ms,
-                "fp64_equivalent_tflops": 32.0 * rows * cfg.n * cfg.s * cfg.p / (k_ms * 1e-3) / 1e12,
+                "fp64_equivalent_tflops": 32.0 * rows * cfg.n * cols * cfg.p / (k_ms * 1e-3) / 1e12,
                 "concurrency": "frequency batches software-pipelined over two streams: the residue and CRT "
                                "kernels of neighbouring batches run beside this kernel (kernel_ms is its own "
                                "event-timed duration, which includes that sharing)",
@@ -489,7 +496,7 @@ def run_ours(args, cfg):
         roof["algorithmic_bytes"] = None
     elif gemm_ai >= ridge:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
-        ktf = 32.0 * rows * cfg.n * cfg.s * cfg.p / (k_ms * 1e-3) / 1e12
+        ktf = 32.0 * rows * cfg.n * cols * cfg.p / (k_ms * 1e-3) / 1e12
         roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": ktf,
                 "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ktf / PEAK_FP64_DMMA_TFLOPS,
                 "peak_source": "measured fp64 DMMA burst (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no fp64",
@@ -545,11 +552,10 @@ def run_ours(args, cfg):
     elif sharded_mode and args.e2e_steps > 0:
         pin_c = torch.empty(sharded.c.shape, dtype=torch.float64, pin_memory=True)
 
-        def e2e_step():  # per rank: A slab (+ B on rank 0) H2D, broadcast + pipeline, C slab D2H
-            sharded.a.copy_(pin_a, non_blocking=True)
-            for t, pb in pin_b:
-                t.copy_(pb, non_blocking=True)
-            sharded.step(broadcast=bcast)
+        def e2e_step():  # per rank: its owned A/B pieces H2D, broadcasts + pipeline, its C block D2H
+            for t, pt in pin_own:
+                t.copy_(pt, non_blocking=True)
+            step()
             pin_c.copy_(sharded.c, non_blocking=True)
             torch.cuda.synchronize()
 
@@ -566,7 +572,7 @@ def run_ours(args, cfg):
         e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
-               "api": "per rank: pinned A slab + the B chunks it owns H2D, chunked NCCL broadcasts from the owners, "
+               "api": "per rank: the pinned A/B pieces it owns H2D, NCCL broadcasts of the pieces over row/column groups, "
                       "qt_* device pipeline, pinned C slab D2H; max over ranks"}
 
     cpu = None
@@ -590,7 +596,8 @@ def run_ours(args, cfg):
                            "fp64 throughout (tube FFTs; stage 2 on the fp64 DMMA tensor pipe)"),
             "accuracy": accuracy,
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                       "parallelism": f"rows{world}" + ("+bcastB(chunked, owner-rooted)" if world > 1 else "")
+                       "parallelism": (f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts"
+                                       if sharded_mode else f"rows{world}")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
                        "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
                        "flops_eff_per_step": cfg.flops_eff},

@@ -121,3 +121,135 @@ class RowShardedTProduct:
         """(c1, c2) of this rank's rows as host complex128 (p, rows, s)."""
         out = self.c.cpu().numpy().view(np.complex128)
         return out[0], out[1]
+
+
+class Grid2DTProduct:
+    """One rank's share of the 2-D block-decomposed T-product (gr x gc ranks).
+
+    Rank (i, j) = divmod(rank, gc) computes block (rows of row block i, columns
+    of column block j) of C.  Row i of C needs only row i of A and column j
+    only column j of B, so a block needs A's row block i and
+    B's column block j.  Those arrive inside the step: A's row block is split
+    into gc pieces, piece k owned (resident, uploaded) by rank (i, k) and
+    broadcast over its row group; B's column block into gr pieces, piece k
+    owned by rank (k, j) and broadcast over its column group.  Per rank: K1 of
+    each arriving A piece into the Â block, then the stage-2 residues of Â
+    (int8 path: one plan), then per arriving B piece K1 + stage 2 into its
+    columns of the C block, then K3.  Against row sharding (gc = 1) the
+    replicated work per rank — the transform and residues of ALL of B — drops
+    to those of one column block: config 5 at 8 ranks, (gr, gc) = (4, 2).
+    Every element goes through the same kernels and arithmetic as the
+    single-GPU product (the stage-2 algorithm is the full shape's), so the
+    stitched C is bitwise identical for every grid.
+    """
+
+    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None, grid=None):
+        import torch
+        self.torch = torch
+        self.m, self.n, self.s, self.p = m, n, s, p
+        self.rank, self.world = rank, world
+        self.gr, self.gc = grid if grid is not None else shard.grid_shape(world, m, s)
+        assert self.gr * self.gc == world
+        self.i, self.j = divmod(rank, self.gc)
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.r0, self.r1 = shard.row_slab(m, self.gr, self.i)
+        self.c0, self.c1 = shard.split_range(0, s, self.gc, tile=16)[self.j]
+        self.rows, self.cols = self.r1 - self.r0, self.c1 - self.c0
+        # pieces: (lo, hi, owner rank)
+        self.apieces = [(lo, hi, self.i * self.gc + k)
+                        for k, (lo, hi) in enumerate(shard.split_range(self.r0, self.r1, self.gc))]
+        self.bpieces = [(lo, hi, k * self.gc + self.j)
+                        for k, (lo, hi) in enumerate(shard.split_range(self.c0, self.c1, self.gr, tile=16))]
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.a = [torch.empty((2, p, hi - lo, 2 * n), **f64) for lo, hi, _ in self.apieces]
+        self.ah_p = [torch.empty_like(t) for t in self.a]
+        self.ah = torch.empty((2, p, self.rows, 2 * n), **f64)
+        self.b = [torch.empty((2, p, n, 2 * (hi - lo)), **f64) for lo, hi, _ in self.bpieces]
+        self.bh = [torch.empty_like(t) for t in self.b]
+        self.c = torch.empty((2, p, self.rows, 2 * self.cols), **f64)
+        self.L = _native.lib()
+        self.algo = self.L.qt_gemm_algo(m, n, s, p)
+
+    # ---------------------------------------------------------------- inputs
+    def owns_a(self, k: int) -> bool:
+        return self.apieces[k][2] == self.rank
+
+    def owns_b(self, k: int) -> bool:
+        return self.bpieces[k][2] == self.rank
+
+    def load_a(self, a1: np.ndarray, a2: np.ndarray, owned_only: bool = True) -> None:
+        for k, (lo, hi, _) in enumerate(self.apieces):
+            if (owned_only and not self.owns_a(k)) or hi == lo:
+                continue
+            for t, src in enumerate((a1, a2)):
+                self.a[k][t].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, lo:hi]).view(np.float64)))
+
+    def load_b(self, b1: np.ndarray, b2: np.ndarray, owned_only: bool = True) -> None:
+        for k, (lo, hi, _) in enumerate(self.bpieces):
+            if (owned_only and not self.owns_b(k)) or hi == lo:
+                continue
+            for t, src in enumerate((b1, b2)):
+                self.b[k][t].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, :, lo:hi]).view(np.float64)))
+
+    # ----------------------------------------------------------------- step
+    def step(self, bcast_row=None, bcast_col=None, stream=None) -> None:
+        """One step.  bcast_row(tensor, src) / bcast_col(tensor, src) enqueue
+        an async broadcast from global rank `src` over this rank's row /
+        column group and return a Work (None: no peers in that group)."""
+        torch = self.torch
+        st = torch.cuda.current_stream() if stream is None else stream
+        sh = st.cuda_stream
+        L, n, p = self.L, self.n, self.p
+        wa = [bcast_row(t, o) if hi > lo else None for t, (lo, hi, o) in zip(self.a, self.apieces)] \
+            if bcast_row is not None else None
+        wb = [bcast_col(t, o) if hi > lo else None for t, (lo, hi, o) in zip(self.b, self.bpieces)] \
+            if bcast_col is not None else None
+        for k, (lo, hi, _) in enumerate(self.apieces):
+            if wa is not None and wa[k] is not None:
+                wa[k].wait()
+            if hi == lo:
+                continue
+            one = len(self.apieces) == 1
+            dst = self.ah if one else self.ah_p[k]
+            _native.check(L.qt_qfft3_conj_f64_device(self.a[k][0].data_ptr(), self.a[k][1].data_ptr(),
+                                                     dst[0].data_ptr(), dst[1].data_ptr(), hi - lo, n, p, sh),
+                          "qfft3_conj(A piece)")
+            if not one:
+                self.ah[:, :, lo - self.r0:hi - self.r0].copy_(self.ah_p[k])
+        plan = None
+        if self.rows and self.algo == 1:
+            h = ctypes.c_void_p()
+            _native.check(L.qt_int8_plan_create(self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.rows, n, p, sh,
+                                                ctypes.byref(h)), "int8 plan")
+            plan = h
+        for k, (lo, hi, _) in enumerate(self.bpieces):
+            if wb is not None and wb[k] is not None:
+                wb[k].wait()
+            if hi == lo or not self.rows:
+                continue
+            cols = hi - lo
+            _native.check(L.qt_qfft3_conj_f64_device(self.b[k][0].data_ptr(), self.b[k][1].data_ptr(),
+                                                     self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), n, cols, p,
+                                                     sh), "qfft3_conj(B piece)")
+            off = 16 * (lo - self.c0)
+            if plan is not None:
+                _native.check(L.qt_int8_plan_multiply(
+                    plan, self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), self.c[0].data_ptr() + off,
+                    self.c[1].data_ptr() + off, cols, cols, self.cols, n * cols, self.rows * self.cols, sh),
+                    "int8 plan multiply")
+            else:
+                _native.check(L.qt_spectral_product_f64_device_ld_algo(
+                    self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(),
+                    self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, self.rows, n, cols, p,
+                    cols, self.cols, n * cols, self.rows * self.cols, self.algo, sh), "spectral_product(piece)")
+        if plan is not None:
+            _native.check(L.qt_int8_plan_destroy(plan, sh), "int8 plan destroy")
+        if self.rows and self.cols:
+            _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
+                                                      self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
+                                                      self.cols, p, sh), "qifft3_conj(C block)")
+
+    def result(self):
+        """(c1, c2) of this rank's block as host complex128 (p, rows, cols)."""
+        out = self.c.cpu().numpy().view(np.complex128)
+        return out[0], out[1]

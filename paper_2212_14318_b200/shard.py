@@ -39,6 +39,32 @@ def column_chunks(s: int, nchunks: int, world: int, tile: int = 16) -> list[tupl
     return [(c0, min(s, c0 + q), j % max(1, world)) for j, c0 in enumerate(range(0, s, q))]
 
 
+def split_range(lo: int, hi: int, parts: int, tile: int = 1) -> list[tuple[int, int]]:
+    """[lo, hi) in `parts` contiguous pieces of ceil(len/parts) rounded up to a
+    multiple of `tile` (trailing pieces may be empty)."""
+    n = hi - lo
+    q = -(-n // max(1, parts))
+    q = -(-q // tile) * tile if q else 0
+    return [(min(hi, lo + k * q), min(hi, lo + (k + 1) * q)) for k in range(parts)]
+
+
+def grid_shape(world: int, m: int, s: int) -> tuple[int, int]:
+    """(gr, gc) with gr * gc = world for the 2-D block decomposition of C.
+    Every rank of row group i needs the residues/transform of A's row block i
+    and every rank of column group j those of B's column block j, so the
+    per-rank replicated work is ~ m/gr + s/gc: minimise it (ties: more row
+    groups).  world = 2 gives (2, 1), i.e. plain row sharding."""
+    best = None
+    for gr in range(1, world + 1):
+        if world % gr:
+            continue
+        gc = world // gr
+        cost = m / gr + s / gc
+        if best is None or cost < best[0] - 1e-12 or (abs(cost - best[0]) <= 1e-12 and gr > best[1]):
+            best = (cost, gr, gc)
+    return best[1], best[2]
+
+
 def take_rows(t1: np.ndarray, t2: np.ndarray, lo: int, hi: int):
     """Rows [lo, hi) of a slice-major (p, m, n) tensor, as a contiguous slab."""
     return np.ascontiguousarray(t1[:, lo:hi, :]), np.ascontiguousarray(t2[:, lo:hi, :])

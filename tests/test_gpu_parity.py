@@ -362,3 +362,31 @@ def test_concurrent_host_calls_are_reentrant_and_bitwise():
     assert not errors, errors
     for w, g in zip(want, got):
         assert bits_equal(w.t1, g.t1) and bits_equal(w.t2, g.t2)
+
+
+@pytest.mark.parametrize("m,n,s,p,grid", [(150, 40, 70, 12, (2, 2)), (150, 40, 70, 12, (1, 3)), (97, 33, 50, 5, (3, 2)),
+                                          (150, 256, 520, 6, (4, 2)), (150, 256, 520, 6, (2, 2)),
+                                          (64, 288, 512, 4, (1, 1))])
+def test_grid2d_pipeline_bitwise(m, n, s, p, grid):
+    """The N > 1 bench pipeline (2-D blocks of C over a gr x gc grid: K1 of the A
+    row-block pieces, Â residues / stage 2 per B column-block piece, K3), run
+    rank by rank on one GPU with every piece loaded locally, stitches to
+    tprod_fast bitwise — DMMA and int8 stage 2."""
+    import torch
+    from paper_2212_14318_b200.distributed import Grid2DTProduct
+    a = qt.gen_random_tensor(m, n, p, 61)
+    b = qt.gen_random_tensor(n, s, p, 62)
+    want = qt.tprod_fast(a, b)
+    world = grid[0] * grid[1]
+    covered = np.zeros((m, s), bool)
+    for r in range(world):
+        g = Grid2DTProduct(m, n, s, p, r, world, "cuda:0", grid=grid)
+        g.load_a(a.t1, a.t2, owned_only=False)  # no peers: this rank holds every piece
+        g.load_b(b.t1, b.t2, owned_only=False)
+        g.step()
+        torch.cuda.synchronize()
+        c1, c2 = g.result()
+        assert bits_equal(c1, want.t1[:, g.r0:g.r1, g.c0:g.c1]), (grid, r)
+        assert bits_equal(c2, want.t2[:, g.r0:g.r1, g.c0:g.c1]), (grid, r)
+        covered[g.r0:g.r1, g.c0:g.c1] = True
+    assert covered.all()

@@ -154,3 +154,97 @@ def test_column_chunk_plan():
     assert plan[0][0] == 0 and plan[-1][1] == 70 and all((c1 - c0) % 16 == 0 or c1 == 70 for c0, c1, _ in plan)
     assert [o for _, _, o in plan] == [j % 3 for j in range(len(plan))]
     assert shard.column_chunks(0, 8, 2) == []
+
+
+def _worker_grid(rank, world, port, m, n, s, p, grid, out_path):
+    """2-D block decomposition (distributed.Grid2DTProduct's schedule) over gloo:
+    A row-block pieces broadcast over row groups, B column-block pieces over
+    column groups, each from its owner; each rank computes its C block."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2212_14318_b200 import shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    gr, gc = grid
+    i, j = divmod(rank, gc)
+    row_groups = [dist.new_group([ii * gc + k for k in range(gc)]) for ii in range(gr)]
+    col_groups = [dist.new_group([k * gc + jj for k in range(gr)]) for jj in range(gc)]
+    A = O.gen_random_tensor(m, n, p, 31)
+    B = O.gen_random_tensor(n, s, p, 32)
+    r0, r1 = shard.row_slab(m, gr, i)
+    c0, c1 = shard.split_range(0, s, gc, tile=16)[j]
+    apieces = [(lo, hi, i * gc + k) for k, (lo, hi) in enumerate(shard.split_range(r0, r1, gc))]
+    bpieces = [(lo, hi, k * gc + j) for k, (lo, hi) in enumerate(shard.split_range(c0, c1, gr, tile=16))]
+    abuf, bbuf = [], []
+    for lo, hi, own in apieces:
+        t = [np.zeros((p, hi - lo, n), np.complex128) for _ in range(2)]
+        if own == rank:
+            t[0][:] = A[0][:, lo:hi]
+            t[1][:] = A[1][:, lo:hi]
+        abuf.append(t)
+    for lo, hi, own in bpieces:
+        t = [np.zeros((p, n, hi - lo), np.complex128) for _ in range(2)]
+        if own == rank:
+            t[0][:] = B[0][:, :, lo:hi]
+            t[1][:] = B[1][:, :, lo:hi]
+        bbuf.append(t)
+    works = []
+    for (lo, hi, own), t in zip(apieces, abuf):
+        if gc > 1 and hi > lo:
+            works += [dist.broadcast(torch.from_numpy(x.view(np.float64)), own, group=row_groups[i], async_op=True)
+                      for x in t]
+    for (lo, hi, own), t in zip(bpieces, bbuf):
+        if gr > 1 and hi > lo:
+            works += [dist.broadcast(torch.from_numpy(x.view(np.float64)), own, group=col_groups[j], async_op=True)
+                      for x in t]
+    for w in works:
+        w.wait()
+    a_blk = (np.concatenate([t[0] for t in abuf], axis=1), np.concatenate([t[1] for t in abuf], axis=1))
+    b_blk = (np.concatenate([t[0] for t in bbuf], axis=2), np.concatenate([t[1] for t in bbuf], axis=2))
+    assert np.array_equal(a_blk[0], A[0][:, r0:r1]) and np.array_equal(b_blk[1], B[1][:, :, c0:c1])
+    c = O.tprod_fast(a_blk, b_blk)
+    mb = -(-m // gr)
+    sb = shard.split_range(0, s, gc, tile=16)[0][1]
+    buf = np.zeros((2, p, mb, sb), np.complex128)
+    buf[0, :, :r1 - r0, :c1 - c0] = c[0]
+    buf[1, :, :r1 - r0, :c1 - c0] = c[1]
+    tt = torch.from_numpy(buf.view(np.float64))
+    gathered = [torch.zeros_like(tt) for _ in range(world)] if rank == 0 else None
+    dist.gather(tt, gathered, dst=0)
+    if rank == 0:
+        c1o = np.zeros((p, m, s), np.complex128)
+        c2o = np.zeros((p, m, s), np.complex128)
+        for r, g in enumerate(gathered):
+            ii, jj = divmod(r, gc)
+            rr0, rr1 = shard.row_slab(m, gr, ii)
+            cc0, cc1 = shard.split_range(0, s, gc, tile=16)[jj]
+            gg = g.numpy().view(np.complex128)
+            c1o[:, rr0:rr1, cc0:cc1] = gg[0, :, :rr1 - rr0, :cc1 - cc0]
+            c2o[:, rr0:rr1, cc0:cc1] = gg[1, :, :rr1 - rr0, :cc1 - cc0]
+        np.savez(out_path, c1=c1o, c2=c2o)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (1, 2)])
+def test_grid2d_piece_broadcasts(tmp_path, grid):
+    import oracle as O
+    m, n, s, p = 9, 5, 40, 6
+    world = grid[0] * grid[1]
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_worker_grid, args=(world, _free_port(), m, n, s, p, grid, out), nprocs=world, join=True)
+    got = np.load(out)
+    want = O.tprod_fast(O.gen_random_tensor(m, n, p, 31), O.gen_random_tensor(n, s, p, 32))
+    assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
+    assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
+
+
+def test_grid_shape():
+    from paper_2212_14318_b200 import shard
+    assert shard.grid_shape(1, 2048, 2048) == (1, 1)
+    assert shard.grid_shape(2, 2048, 2048) == (2, 1)
+    assert shard.grid_shape(4, 2048, 2048) == (2, 2)
+    assert shard.grid_shape(8, 2048, 2048) == (4, 2)
+    assert shard.grid_shape(8, 1080, 64) == (8, 1)   # narrow B: plain row sharding
