@@ -492,7 +492,7 @@ static int tprod_host_tiled(const double* a1, const double* a2, const double* b1
     return QT_OK;
   };
   uint64_t unit = 0;
-  const int algo = choose_gemm_algo(n, s);  // one algorithm for every tile of the product
+  const int algo = choose_gemm_algo(n, s, p);  // one algorithm for every tile of the product
   auto compute_tile = [&](uint64_t i, uint64_t j) -> int {
     const int t = (int)(unit % 3);
     ++unit;
@@ -714,8 +714,8 @@ int qt_spectral_product_f64_device_ld_algo(const double* ah1, const double* ah2,
     return fail(QT_EINVAL, "spectral_product: leading dimensions smaller than the matrices");
   if (algo != QT_GEMM_AUTO && algo != QT_GEMM_DMMA && algo != QT_GEMM_INT8_EXACT)
     return fail(QT_EINVAL, "spectral_product: unknown algorithm");
-  if (algo == QT_GEMM_INT8_EXACT && (n % 32 != 0 || n > 8192))
-    return fail(QT_EINVAL, "spectral_product: the int8 path needs n % 32 == 0 and n <= 8192");
+  if (algo == QT_GEMM_INT8_EXACT && (n % 32 != 0 || n > 8192 || p > 65534))
+    return fail(QT_EINVAL, "spectral_product: the int8 path needs n %% 32 == 0, n <= 8192 and p <= 65534");
   int dev = 0;
   if ((rc = current_device(&dev))) return rc;
   cudaError_t e = launch_spectral_gemm_ld((const double2*)ah1, (const double2*)ah2, (const double2*)bh1,
@@ -748,8 +748,8 @@ int qt_int8_plan_create(const double* ah1, const double* ah2, uint64_t m, uint64
   *plan = nullptr;
   int rc = check_dims(m, n, 1, p, "int8 plan");
   if (rc) return rc;
-  if (m == 0 || n == 0 || n % 32 != 0 || n > 8192)
-    return fail(QT_EINVAL, "int8 plan: needs m > 0 and n %% 32 == 0, 0 < n <= 8192");
+  if (m == 0 || n == 0 || n % 32 != 0 || n > 8192 || p > 65534)
+    return fail(QT_EINVAL, "int8 plan: needs m > 0, n %% 32 == 0, 0 < n <= 8192 and p <= 65534");
   int dev = 0;
   if ((rc = current_device(&dev))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -814,7 +814,7 @@ int qt_int8_plan_destroy(void* plan, void* stream) {
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
   (void)m;
   (void)p;
-  return choose_gemm_algo(n, s);
+  return choose_gemm_algo(n, s, p);
 }
 
 static int tprod_host_impl(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
@@ -824,7 +824,7 @@ static int tprod_host_impl(const double* a1, const double* a2, const double* b1,
   // Large problems stream (row slab x column chunk) tiles: ~8 slabs of >= 64
   // rows and ~8 chunks of >= 64 columns (a multiple of the GEMM tile).
   // Products on the int8 K2 stream row slabs against resident B' residues.
-  if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20) && choose_gemm_algo(n, s) == kAlgoOzaki) {
+  if (n > 0 && s > 0 && m >= 128 && ab + bb + cb >= (128ull << 20) && choose_gemm_algo(n, s, p) == kAlgoOzaki) {
     // ~16 slabs of >= 128 rows (measured on config 5: 4 slabs 196 ms, 8 slabs
     // 182 ms, 16 slabs 175 ms end to end — finer slabs start computing sooner
     // and leave less after the last upload)

@@ -459,8 +459,8 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
                                     int algo) {
   if (m == 0 || s == 0 || p == 0) return cudaSuccess;
-  if (algo == kAlgoAuto) algo = choose_gemm_algo(n, s);
-  if (algo == kAlgoOzaki && (n % 32 != 0 || n > 8192)) return cudaErrorInvalidValue;
+  if (algo == kAlgoAuto) algo = choose_gemm_algo(n, s, p);
+  if (algo == kAlgoOzaki && (n % 32 != 0 || n > 8192 || p > 65534)) return cudaErrorInvalidValue;
   if (algo != kAlgoOzaki)
     return dmma_spectral_gemm(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, nullptr);
   // exact int8 tensor-core path (qt_ozaki.cu); the DMMA kernels run only if

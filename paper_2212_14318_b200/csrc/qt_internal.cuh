@@ -79,10 +79,12 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
 // (qt_ozaki.cu).  *flag (device int, zeroed by the caller) is set to 1 if the
 // inputs hold a non-finite value, in which case C is left untouched.
 enum GemmAlgo { kAlgoAuto = -1, kAlgoDmma = 0, kAlgoOzaki = 1 };
-bool ozaki_supported(uint64_t n, uint64_t s);
+bool ozaki_supported(uint64_t n, uint64_t s, uint64_t p);
 // the algorithm a product of this shape uses (callers that split one product
 // into row slabs or column chunks decide once, on the full shape)
-inline int choose_gemm_algo(uint64_t n, uint64_t s) { return ozaki_supported(n, s) ? kAlgoOzaki : kAlgoDmma; }
+inline int choose_gemm_algo(uint64_t n, uint64_t s, uint64_t p) {
+  return ozaki_supported(n, s, p) ? kAlgoOzaki : kAlgoDmma;
+}
 cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, const double2* bh1,
                                        const double2* bh2, double2* ch1, double2* ch2, uint64_t m, uint64_t n,
                                        uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc, uint64_t bslice,

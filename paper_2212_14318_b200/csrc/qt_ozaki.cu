@@ -881,7 +881,7 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace oz
 
-bool ozaki_supported(uint64_t n, uint64_t s) {
+bool ozaki_supported(uint64_t n, uint64_t s, uint64_t p) {
   // QTB_OZAKI: 0 = never, 1 = auto, 2 = whenever the shape allows.  Auto takes
   // the int8 path where it measured faster than DMMA on B200 (tools/oz_sweep.py:
   // 256^3 0.96x, n = 1920 s = 64 0.69x, s = 128 1.28x, 512^3 1.88x, 2048^3
@@ -889,7 +889,7 @@ bool ozaki_supported(uint64_t n, uint64_t s) {
   // of A.  Callers that split one product (row slabs, column chunks) decide
   // once on the full shape; m never enters (row shards agree by construction).
   static const int mode = oz::env_int("QTB_OZAKI", 1);
-  if (mode == 0 || n == 0 || n % 32 != 0 || n > 8192) return false;
+  if (mode == 0 || n == 0 || n % 32 != 0 || n > 8192 || p == 0 || p > 65534) return false;
   if (mode == 2) return true;
   return n >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_N", 256) && s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_S", 128) &&
          n * s >= (uint64_t)oz::env_int("QTB_OZAKI_MIN_NS", 1 << 17);
@@ -940,7 +940,9 @@ uint64_t env_mb(const char* name, uint64_t dflt_mb) { return (uint64_t)oz::env_i
 
 // slots per batch: even (pairs stay together), balanced over the batches
 uint64_t batch_slots(uint64_t p, uint64_t per_slot, uint64_t budget) {
-  uint64_t F = std::max<uint64_t>(2, std::min<uint64_t>(p, budget / std::max<uint64_t>(1, per_slot)) & ~uint64_t(1));
+  // (slots are a grid dimension of the residue / CRT kernels: <= 65534)
+  uint64_t F = std::max<uint64_t>(
+      2, std::min<uint64_t>({p, budget / std::max<uint64_t>(1, per_slot), uint64_t(65534)}) & ~uint64_t(1));
   const uint64_t nb = (p + F - 1) / F;
   return std::min<uint64_t>(p, ((p + nb - 1) / nb + 1) & ~uint64_t(1));
 }
