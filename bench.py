@@ -423,13 +423,14 @@ def run_ours(args, cfg):
         step()
     torch.cuda.synchronize()
     L.qt_prof_enable(0)
-    def read_prof():
+    def read_prof(steps_done=None):
+        steps_done = steps_done or nprof
         out = {}
         for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_crt"):
             t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
             qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
             if n_l.value:
-                out[tag] = {"ms_per_step": t_ms.value / nprof, "launches_per_step": n_l.value / nprof}
+                out[tag] = {"ms_per_step": t_ms.value / steps_done, "launches_per_step": n_l.value / steps_done}
         return out
 
     prof = read_prof()
@@ -528,6 +529,42 @@ def run_ours(args, cfg):
         "K3_ifft_C": {"ms": ifft_ms, "GB_s": ifft_gbs, "frac_hbm": ifft_gbs / peaks["hbm_gbs"]},
     }
 
+    # ---- the fp64 DMMA stage 2 on the same step (the north_star's design), when
+    # this workload's default is the int8 path: K1 -> paired DMMA GEMM -> K3
+    dmma_path = None
+    if algo == 1 and not sharded_mode:
+        ahd = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
+        bhd = torch.empty((2, cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
+
+        def dmma_step():
+            qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ahd[0].data_ptr(),
+                                                        ahd[1].data_ptr(), rows, cfg.n, cfg.p, sh), "qfft3")
+            qt._native.check(L.qt_qfft3_conj_f64_device(db1.data_ptr(), db2.data_ptr(), bhd[0].data_ptr(),
+                                                        bhd[1].data_ptr(), cfg.n, cols, cfg.p, sh), "qfft3")
+            qt._native.check(L.qt_spectral_product_f64_device_ld_algo(
+                ahd[0].data_ptr(), ahd[1].data_ptr(), bhd[0].data_ptr(), bhd[1].data_ptr(), dc1.data_ptr(),
+                dc2.data_ptr(), rows, cfg.n, cols, cfg.p, cols, cols, cfg.n * cols, rows * cols, 0, sh), "dmma")
+            qt._native.check(L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
+                                                         dc2.data_ptr(), rows, cols, cfg.p, sh), "qifft3")
+
+        dmma_step()
+        nd = max(2, min(args.steps, 3))
+        L.qt_prof_enable(1)
+        t_d = timed(dmma_step, nd)
+        L.qt_prof_enable(0)
+        pd = read_prof(nd)
+        k_d = pd.get("k2_dmma", {}).get("ms_per_step", 0.0)
+        ktf_d = 32.0 * rows * cfg.n * cols * cfg.p / (k_d * 1e-3) / 1e12 if k_d else None
+        dmma_path = {"ms_per_step": t_d, "value": cfg.flops_eff / (t_d * 1e-3) / 1e9, "unit": "GFLOP/s",
+                     "k2_kernel_ms": k_d, "k2_algorithmic_tflops": ktf_d,
+                     "k2_frac_of_fp64_peak": ktf_d / PEAK_FP64_DMMA_TFLOPS if ktf_d else None,
+                     "k2_executed_frac_of_dmma_pipe": (ktf_d * (0.75 if gauss else 1.0) / PEAK_FP64_DMMA_TFLOPS
+                                                       if ktf_d else None),
+                     "note": "same step with stage 2 on the fp64 DMMA tensor pipe (mma.sync.m8n8k4.f64, Gauss 3M): "
+                             "the north_star's FP64-tensor-core design, kept as the path for configs 1-4 and as the "
+                             "non-finite fallback"}
+        del ahd, bhd
+
     # ---- end to end: host buffers in, host buffers out, copies inside the timed region ----
     e2e = None
     if not sharded_mode and args.e2e_steps > 0:
@@ -595,6 +632,7 @@ def run_ours(args, cfg):
                            if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1 else
                            "fp64 throughout (tube FFTs; stage 2 on the fp64 DMMA tensor pipe)"),
             "accuracy": accuracy,
+            "fp64_dmma_path": dmma_path,
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
                        "parallelism": (f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts"
                                        if sharded_mode else f"rows{world}")
