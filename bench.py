@@ -528,6 +528,12 @@ def run_ours(args, cfg):
                     **({} if algo == 1 else {"executed_TFLOP_s": exec_tf})},
         "K3_ifft_C": {"ms": ifft_ms, "GB_s": ifft_gbs, "frac_hbm": ifft_gbs / peaks["hbm_gbs"]},
     }
+    if "fft" in prof:  # the step's own tube-FFT launches (K1 of A and B in one launch, K3), event-timed
+        fb = 2 * (cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cols) + cfg.bytes_tensor(rows, cols))
+        f_ms = prof["fft"]["ms_per_step"]
+        stages["K1_K3_in_step"] = {"ms": f_ms, "GB_s": fb / (f_ms * 1e-3) / 1e9,
+                                   "frac_hbm": fb / (f_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                   "algorithmic": "64 (mn + ns + ms) p bytes (read + write of both planes)"}
 
     # ---- the fp64 DMMA stage 2 on the same step (the north_star's design), when
     # this workload's default is the int8 path: K1 -> paired DMMA GEMM -> K3
