@@ -422,7 +422,9 @@ __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom
         const int kk = idxD + k * R0;
         double2 y = v[k];
         if (G.post_tw && g != 0) y = cmul(y, __ldg(&tw[g * kk]));
-        out[(uint64_t)kk * ostr + t] = make_double2(y.x * sc, y.y * sci);
+        const double2 o = make_double2(y.x * sc, y.y * sci);
+        if (job.stream_out) __stcs(&out[(uint64_t)kk * ostr + t], o);
+        else out[(uint64_t)kk * ostr + t] = o;
       }
     }
   }
@@ -611,10 +613,11 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
         A.job[i].out = scratch + off;
         A.job[i].conj_out = 0;
         A.job[i].scale = 1.0;
-        // pass B: from scratch, output ops of the job
+        // pass B: from scratch, output ops of the job; its output streams past L2
         B.job[i].in = scratch + off;
         B.job[i].conj_in = 0;
         B.job[i].out = J.out;
+        B.job[i].stream_out = 1;
         off += J.ntubes * (uint64_t)p;
       }
       const FftGeom GA{p1, 1, p2, 1, p2, 1, p2};  // rows g + p2*i -> g + p2*k, twiddle W_p^(g*k)

@@ -32,6 +32,7 @@ struct TubeJob {
   int conj_in;
   int conj_out;
   double scale;
+  int stream_out = 0;  // 1: evict-first stores (final pass of the split FFT: keep its L2 scratch resident)
 };
 
 constexpr int kMaxJobs = 4;
