@@ -155,6 +155,27 @@ int qt_int8_plan_multiply(void* plan, const double* bhat1, const double* bhat2, 
                           uint64_t s, uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream);
 int qt_int8_plan_destroy(void* plan, void* stream);
 
+/* Frequency slots (multi-GPU plumbing; no reference counterpart — the
+ * reference's tprod_fast is single-process, tproduct.cpp:75-111).  Stage 2
+ * visits frequencies in slots: slot 2j, 2j+1 hold the pair (j+1, p-j-1), the
+ * self-paired 0 (and p/2 for even p) come last.  qt_slot_frequency maps a
+ * slot to its frequency (-1 if slot >= p). */
+int qt_slot_frequency(uint64_t p, uint64_t slot);
+
+/* Exact int8 stage 2 on a compact slot range [slot0, slot0 + nslots) (the
+ * frequency-parallel multi-GPU driver: one range per rank).  B̂ (nslots, n, s),
+ * and the Â (nslots, m, n) / Ĉ (nslots, m, s) of every multiply, hold slice t
+ * = slot slot0 + t (two complex128 planes each, dense).  Neither end of the
+ * range may split a pair (an odd boundary below 2 * ((p - 1) / 2)).  `nonfinite` is a device
+ * int the caller zeroes: it becomes non-zero if Â or B̂ held an inf/NaN, and
+ * then Ĉ is NOT written (the caller must use the DMMA path for that product).
+ * Bitwise identical to the same slots of a full-range int8 product. */
+int qt_int8_slots_create(const double* bhat1, const double* bhat2, uint64_t n, uint64_t s, uint64_t p, int slot0,
+                         int nslots, int* nonfinite, void* stream, void** handle);
+int qt_int8_slots_multiply(void* handle, const double* ahat1, const double* ahat2, uint64_t m, double* chat1,
+                           double* chat2, void* stream);
+int qt_int8_slots_destroy(void* handle, void* stream);
+
 /* Definitional product tprod_naive = fold(bcirc(A) . unfold(B))
  * (tproduct.hpp:23-25, tproduct.cpp:49-53) without materialising bcirc:
  * C_k = sum_r A_{(k-r) mod p} (.) B_r on FP64 DMMA.  16 m n s p^2 real

@@ -38,6 +38,11 @@ SIGNATURES = {
     "qt_int8_plan_create": (ctypes.c_int, [_dp, _dp] + [_u64] * 3 + [_vp, ctypes.POINTER(ctypes.c_void_p)]),
     "qt_int8_plan_multiply": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp] + [_u64] * 5 + [_vp]),
     "qt_int8_plan_destroy": (ctypes.c_int, [ctypes.c_void_p, _vp]),
+    "qt_slot_frequency": (ctypes.c_int, [_u64, _u64]),
+    "qt_int8_slots_create": (ctypes.c_int, [_dp, _dp] + [_u64] * 3 + [ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                                                      ctypes.POINTER(ctypes.c_void_p)]),
+    "qt_int8_slots_multiply": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _u64, _dp, _dp, _vp]),
+    "qt_int8_slots_destroy": (ctypes.c_int, [ctypes.c_void_p, _vp]),
     "qt_tprod_naive_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_tprod_naive_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),
     "qt_tprod_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),

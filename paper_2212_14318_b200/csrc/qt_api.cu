@@ -811,6 +811,74 @@ int qt_int8_plan_destroy(void* plan, void* stream) {
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 plan destroy");
 }
 
+namespace {
+struct Int8Slots {
+  OzakiB B;
+  int* nonfinite = nullptr;
+  int device = 0;
+};
+}  // namespace
+
+int qt_slot_frequency(uint64_t p, uint64_t slot) {
+  if (p == 0 || slot >= p) return -1;
+  const uint64_t npairs = (p - 1) / 2;
+  if (slot < 2 * npairs) return (int)((slot & 1) ? p - (slot / 2 + 1) : slot / 2 + 1);
+  return slot == 2 * npairs ? 0 : (int)(p / 2);
+}
+
+int qt_int8_slots_create(const double* bh1, const double* bh2, uint64_t n, uint64_t s, uint64_t p, int slot0,
+                         int nslots, int* nonfinite, void* stream, void** handle) {
+  t_err.clear();
+  if (!handle) return fail(QT_EINVAL, "int8 slots: null handle pointer");
+  *handle = nullptr;
+  int rc = check_dims(1, n, s, p, "int8 slots");
+  if (rc) return rc;
+  if (!nonfinite) return fail(QT_EINVAL, "int8 slots: null non-finite flag");
+  if (n == 0 || s == 0 || n % 32 != 0 || n > 8192 || p > 65534)
+    return fail(QT_EINVAL, "int8 slots: needs s > 0, n %% 32 == 0, 0 < n <= 8192 and p <= 65534");
+  const uint64_t pair_end = 2 * ((p - 1) / 2);  // slots [0, pair_end) hold pairs (2j, 2j+1)
+  auto splits = [&](uint64_t b) { return (b & 1) && b < pair_end; };
+  if (slot0 < 0 || nslots <= 0 || (uint64_t)slot0 + nslots > p || splits((uint64_t)slot0) ||
+      splits((uint64_t)slot0 + nslots))
+    return fail(QT_EINVAL, "int8 slots: the slot range must lie inside [0, p) and keep pairs whole");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  Int8Slots* H = new Int8Slots;
+  H->nonfinite = nonfinite;
+  H->device = dev;
+  cudaError_t e = ozaki_prepare_b_slots((const double2*)bh1, (const double2*)bh2, n, s, p, slot0, nslots, nonfinite,
+                                        &H->B, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    delete H;
+    return cuda_fail(e, "int8 slots: residues of B");
+  }
+  *handle = H;
+  return QT_OK;
+}
+
+int qt_int8_slots_multiply(void* handle, const double* ah1, const double* ah2, uint64_t m, double* ch1, double* ch2,
+                           void* stream) {
+  t_err.clear();
+  Int8Slots* H = (Int8Slots*)handle;
+  if (!H) return fail(QT_EINVAL, "int8 slots: null handle");
+  int rc = check_dims(m, H->B.n, H->B.s, H->B.p, "int8 slots multiply");
+  if (rc) return rc;
+  if (m == 0) return QT_OK;
+  const uint64_t s = H->B.s;
+  cudaError_t e = ozaki_multiply(H->B, (const double2*)ah1, (const double2*)ah2, nullptr, nullptr, m, (double2*)ch1,
+                                 (double2*)ch2, s, m * s, H->nonfinite, (cudaStream_t)stream);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 slots multiply");
+}
+
+int qt_int8_slots_destroy(void* handle, void* stream) {
+  t_err.clear();
+  Int8Slots* H = (Int8Slots*)handle;
+  if (!H) return QT_OK;
+  const cudaError_t e = ozaki_release(H->B, (cudaStream_t)stream);
+  delete H;
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 slots destroy");
+}
+
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
   (void)m;
   (void)p;

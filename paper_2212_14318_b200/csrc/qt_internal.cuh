@@ -98,6 +98,7 @@ struct OzakiB {
   uint64_t n = 0, s = 0, p = 0, ldb = 0, bslice = 0;
   int nslots = 0;
   bool all = false;
+  int s0 = 0, ns = 0, cbase = -1;  // slot range; cbase >= 0: compact operand tensors (slot - cbase)
 };
 cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                             uint64_t ldb, uint64_t bslice, int* flag, bool require_all, OzakiB* out,
@@ -106,6 +107,8 @@ cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, co
                            uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
                            cudaStream_t stream);
 cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream);
+cudaError_t ozaki_prepare_b_slots(const double2* bh1, const double2* bh2, uint64_t n, uint64_t s, uint64_t p, int s0,
+                                  int ns, int* flag, OzakiB* out, cudaStream_t stream);
 // X' residues of every frequency, prepared once and reused against many B'
 // (column chunks of B: the chunked multi-GPU pipeline, the e2e wavefront)
 struct OzakiA {

@@ -452,6 +452,12 @@ __device__ __forceinline__ int slot_freq(int slot, int p) {
   return slot == 2 * npairs ? 0 : p / 2;
 }
 
+// Slice of a frequency slot in the operand tensors: the frequency itself, or
+// (compact tensors holding slots [cbase, ...) in slot order) slot - cbase.
+__device__ __forceinline__ int slot_slice(int slot, int p, int cbase) {
+  return cbase < 0 ? slot_freq(slot, p) : slot - cbase;
+}
+
 // x * 2^e, exact for the finite values scaled here (one multiply in range)
 __device__ __forceinline__ double scale2(double x, int e) {
   if (e >= -1022 && e <= 1023) return x * __longlong_as_double((long long)(e + 1023) << 52);
@@ -534,13 +540,15 @@ constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32
 __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __restrict__ a1,
                                                            const double2* __restrict__ a2, uint8_t* __restrict__ out,
                                                            int* __restrict__ eA, int* nonfinite, int m, int n, int p,
-                                                           int f0, int Mp, int F) {
+                                                           int f0, int Mp, int F, int cbase) {
   __shared__ double red[8];
   const int i = blockIdx.x, f = blockIdx.y;
-  const int k = slot_freq(f0 + f, p), sk = (p - k) % p;
+  const int slot = f0 + f;
+  const int k = slot_freq(slot, p), sk = (p - k) % p;
   const int fpart = (k == sk) ? f : (f ^ 1);
-  const double2* P = a1 + ((size_t)k * m + i) * n;
-  const double2* Qr = a2 + ((size_t)sk * m + i) * n;
+  const int kq = slot_slice(slot, p, cbase), skq = slot_slice((k == sk) ? slot : (slot ^ 1), p, cbase);
+  const double2* P = a1 + ((size_t)kq * m + i) * n;
+  const double2* Qr = a2 + ((size_t)skq * m + i) * n;
   double mx = 0.0;
   bool bad = false;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -625,10 +633,10 @@ struct ColPart {
 __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
                                                           const double2* __restrict__ b2, ColPart* __restrict__ part,
                                                           int* nonfinite, int n, int s, int p, int f0, int Sp, int F,
-                                                          uint64_t ldb, uint64_t bslice) {
+                                                          uint64_t ldb, uint64_t bslice, int cbase) {
   __shared__ double red[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
-  const int k = slot_freq(f0 + f, p);
+  const int k = slot_slice(f0 + f, p, cbase);
   const int j0 = blockIdx.z * 256, jend = min(2 * n, j0 + 256);
   auto load = [&](int j) {
     return (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
@@ -697,10 +705,10 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
                                                            const double2* __restrict__ b2,
                                                            const int* __restrict__ eB, uint8_t* __restrict__ out,
                                                            int n, int s, int p, int f0, int Sp, int F, uint64_t ldb,
-                                                           uint64_t bslice) {
+                                                           uint64_t bslice, int cbase) {
   extern __shared__ double2 tile[];  // [32][kBStride]
   const int c0 = blockIdx.x * 32, j0 = blockIdx.z * kBRows, f = blockIdx.y;
-  const int k = slot_freq(f0 + f, p);
+  const int k = slot_slice(f0 + f, p, cbase);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int jj = ty; jj < kBRows; jj += 8) {
     const int j = j0 + jj, c = c0 + tx;
@@ -770,7 +778,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
                                                      const int* __restrict__ eB, const int* nonfinite,
                                                      double2* __restrict__ c1, double2* __restrict__ c2, int m,
                                                      int s, int p, int f0, int bslot0, int Mp, int Sp, int F,
-                                                     uint64_t ldc, uint64_t cslice) {
+                                                     uint64_t ldc, uint64_t cslice, int cbase) {
   if (*nonfinite) return;
   const int cb = (blockIdx.x * blockDim.x + threadIdx.x) * kCrtVec;
   const int f = blockIdx.z;
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
   for (int t = 0; t < kCrtVec; ++t) {
     eb[t] = eB[(bslot0 + f) * Sp + cb + t];
   }
-  const int k = slot_freq(f0 + f, p);
+  const int k = slot_slice(f0 + f, p, cbase);
   const size_t plane = (size_t)F * Mp * Sp * 2;  // bytes
   for (int r = blockIdx.y; r < 2 * m; r += gridDim.y) {
     const uint8_t* ptr = R + ((size_t)(f * Mp + r) * Sp + cb) * 2;
@@ -960,13 +968,13 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   if (e != cudaSuccess) return e;
   ProfScope ps("k2_int8_residues", stream);
   oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)nz), 256, 0, stream>>>(
-      bh1, bh2, part, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice);
+      bh1, bh2, part, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice, B.cbase);
   oz_colexp_finish_kernel<<<(unsigned)((fcur * Sp + 255) / 256), 256, 0, stream>>>(part, eB, nz, fcur, (int)Sp, fcur);
   e = cudaFreeAsync(part, stream);
   if (e != cudaSuccess) return e;
   oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
                         stream>>>(
-      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice);
+      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase);
   ps.stop();
   count_launches(3);
   return cudaGetLastError();
@@ -982,7 +990,7 @@ cudaError_t prep_a(const OzakiA& A, const double2* ah1, const double2* ah2, int*
   if (e != cudaSuccess) return e;
   ProfScope pr("k2_int8_residues", stream);
   oz_residue_a_kernel<<<dim3((unsigned)A.m, (unsigned)A.p), 256, 0, stream>>>(
-      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p);
+      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p, -1);
   pr.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -1004,10 +1012,11 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   // buffered.  Without B.all (B' rebuilt per batch) the batches run in order.
   const bool pipe = B.all && env_int("QTB_OZAKI_PIPE", 1) != 0;
   const uint64_t nbuf = pipe ? 2 : 1;
-  uint64_t F = B.all ? batch_slots(p, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  const uint64_t ps = B.ns ? (uint64_t)B.ns : p;  // slots [B.s0, B.s0 + ps) of the p
+  uint64_t F = B.all ? batch_slots(ps, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
   // at least 4 batches when pipelining, so residues/CRT have a GEMM to hide behind
-  if (pipe && p >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((p + 3) / 4 + 1) & ~uint64_t(1)));
-  const uint64_t nbatch = (p + F - 1) / F;
+  if (pipe && ps >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((ps + 3) / 4 + 1) & ~uint64_t(1)));
+  const uint64_t nbatch = (ps + F - 1) / F;
   if (nbuf * F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
   const size_t bytesA = A ? 0 : (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
   const size_t offR = bytesA, offE = offR + nbuf * bytesR, wsbytes = offE + (A ? 0 : nbuf * F * Mp * sizeof(int));
@@ -1042,8 +1051,8 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     }
   }
   auto batch = [&](uint64_t i, uint64_t& f0, int& fcur) {
-    f0 = i * F;
-    fcur = (int)std::min<uint64_t>(F, p - f0);
+    f0 = B.s0 + i * F;
+    fcur = (int)std::min<uint64_t>(F, B.s0 + ps - f0);
   };
   auto residues = [&](uint64_t i, cudaStream_t st) {
     uint64_t f0;
@@ -1053,7 +1062,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     ProfScope pr("k2_int8_residues", st);
     oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp, eA + b * F * Mp,
                                                                  flag, (int)m, (int)n, (int)p, (int)f0, (int)Mp,
-                                                                 (int)aslots);
+                                                                 (int)aslots, B.cbase);
     pr.stop();
     count_launches(1);
   };
@@ -1062,13 +1071,14 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     int fcur;
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
-    const int bslot0 = B.all ? (int)f0 : 0;
+    const int bslot0 = B.all ? (int)(f0 - B.s0) : 0;
     const uint64_t aslot0 = A ? f0 : b * F;
     const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 65535),
                      (unsigned)fcur);
     ProfScope pc("k2_int8_crt", st);
     oz_crt_kernel<<<cgrid, 256, 0, st>>>(ws + offR + b * bytesR, eA + aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m,
-                                         (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice);
+                                         (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice,
+                                         B.cbase);
     pc.stop();
     count_launches(1);
   };
@@ -1079,7 +1089,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     int fcur;
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
-    int bslot0 = (int)f0;
+    int bslot0 = (int)(f0 - B.s0);
     if (!B.all) {  // B' for this batch only (sequential schedule)
       bslot0 = 0;
       if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
@@ -1149,6 +1159,9 @@ cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, 
   const uint64_t per_b = b_slot_bytes(n, s);
   // keep B' for every frequency when it fits (one residue pass over B̂, reused
   // by every A batch / row slab); otherwise B' is rebuilt per A batch
+  B.s0 = 0;
+  B.ns = (int)p;
+  B.cbase = -1;
   B.all = require_all || per_b * p <= env_mb("QTB_OZAKI_B_MB", 24576);
   B.nslots = B.all ? (int)p : (int)batch_slots(p, a_slot_bytes(m, n, s) + per_b, env_mb("QTB_OZAKI_WS_MB", 6144));
   if ((uint64_t)B.nslots * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
@@ -1158,6 +1171,45 @@ cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, 
   B.eB = reinterpret_cast<int*>(B.res + bytes);
   if (B.all) e = prep_b(B, bh1, bh2, 0, (int)p, 0, flag, stream);
   if (e != cudaSuccess) {
+    cudaFreeAsync(B.res, stream);
+    return e;
+  }
+  *out = B;
+  return cudaSuccess;
+}
+
+// Compact slot range: B̂ (ns, n, s) holds the frequency slots [s0, s0 + ns)
+// in slot order (slice t = slot s0 + t), and so do the Â (ns, m, n) and Ĉ
+// (ns, m, s) of every ozaki_multiply against the returned B'.  A pair occupies
+// two adjacent slots (2j, 2j+1): neither end of the range may split one.  The
+// frequency-parallel multi-GPU driver gives each rank such a range.
+cudaError_t ozaki_prepare_b_slots(const double2* bh1, const double2* bh2, uint64_t n, uint64_t s, uint64_t p, int s0,
+                                  int ns, int* flag, OzakiB* out, cudaStream_t stream) {
+  *out = OzakiB{};
+  // a boundary may not split a pair (an odd slot below 2 * npairs)
+  const uint64_t pair_end = 2 * ((p - 1) / 2);
+  auto splits = [&](uint64_t b) { return (b & 1) && b < pair_end; };
+  if (n % 32 != 0 || n > 8192 || n == 0 || s == 0 || p == 0 || p > 65534 || s0 < 0 || ns <= 0 ||
+      (uint64_t)s0 + ns > p || splits((uint64_t)s0) || splits((uint64_t)s0 + ns))
+    return cudaErrorInvalidValue;
+  cudaError_t e = oz_init();
+  if (e != cudaSuccess) return e;
+  OzakiB B{};
+  B.n = n;
+  B.s = s;
+  B.p = p;
+  B.ldb = s;
+  B.bslice = n * s;
+  B.s0 = s0;
+  B.ns = ns;
+  B.cbase = s0;
+  B.all = true;
+  B.nslots = ns;
+  if ((uint64_t)ns * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
+  const size_t bytes = (size_t)oz::kQ * ns * 2 * pad_cols(s) * 4 * n;
+  if ((e = cudaMallocAsync(&B.res, bytes + (size_t)ns * pad_cols(s) * sizeof(int), stream)) != cudaSuccess) return e;
+  B.eB = reinterpret_cast<int*>(B.res + bytes);
+  if ((e = prep_b(B, bh1, bh2, (uint64_t)s0, ns, 0, flag, stream)) != cudaSuccess) {
     cudaFreeAsync(B.res, stream);
     return e;
   }

@@ -253,3 +253,240 @@ class Grid2DTProduct:
         """(c1, c2) of this rank's block as host complex128 (p, rows, cols)."""
         out = self.c.cpu().numpy().view(np.complex128)
         return out[0], out[1]
+
+
+class FreqParallelTProduct:
+    """One rank's share of the frequency-parallel T-product (int8 stage 2).
+
+    The three stages partition along different axes, with one exchange
+    between neighbours and no replicated work:
+      K1  tube FFTs are independent per (row, column) tube: rank r transforms
+          its rows [a0, a1) of A (shard.row_slab(m)) and rows [b0, b1) of B
+          (shard.row_slab(n));
+      K2  stage 2 is independent per frequency pair (k, p - k): rank r owns
+          the slot range shard.slot_ranges(p)[r] and runs the exact int8 GEMM
+          on compact operands holding just those slots, for all of m, n, s
+          (qt_int8_slots_*: B' residues once, then Â);
+      K3  the inverse tube FFTs of rank r's rows [a0, a1) of C.
+    Between them, each (slot, rows) piece goes point to point from the rank
+    that transformed it to the rank that needs it: Â[k] rows [a0, a1) and
+    B̂[k] rows [b0, b1) to the owner of k's slot, Ĉ[k] rows of rank i back to
+    rank i — every piece a contiguous block of both the sender's and the
+    receiver's buffer, so the exchange is a group of NCCL send/recv pairs
+    straight from and into the stage buffers.  Per rank that is 1/G of every
+    kernel's work plus (G-1)/G of its own Â, B̂ and Ĉ rows over NVLink, where
+    the 2-D block decomposition replicates the transforms and residues of a
+    whole row block of A and column block of B.
+
+    Every slot is evaluated with the same kernels and arithmetic as the
+    single-GPU int8 product (row and column scalings depend on the slot's
+    own data only), so the stitched C is bitwise identical to it.  Inputs
+    holding inf/NaN are detected (nonfinite()) and rejected by result(): the
+    fp64 DMMA decomposition (Grid2DTProduct) handles those.
+    """
+
+    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None):
+        import torch
+        self.torch = torch
+        self.m, self.n, self.s, self.p = m, n, s, p
+        self.rank, self.world = rank, world
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.arows = [shard.row_slab(m, world, r) for r in range(world)]
+        self.brows = [shard.row_slab(n, world, r) for r in range(world)]
+        self.ranges = shard.slot_ranges(p, world)
+        self.a0, self.a1 = self.arows[rank]
+        self.b0, self.b1 = self.brows[rank]
+        self.s0, self.s1 = self.ranges[rank]
+        self.rows, self.ns = self.a1 - self.a0, self.s1 - self.s0
+        self.freq = [shard.slot_freq(p, t) for t in range(p)]
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        br = self.b1 - self.b0
+        self.a = torch.empty((2, p, self.rows, 2 * n), **f64)
+        self.ah = torch.empty_like(self.a)
+        self.b = torch.empty((2, p, br, 2 * s), **f64)
+        self.bh = torch.empty_like(self.b)
+        self.ac = torch.empty((2, self.ns, m, 2 * n), **f64)
+        self.bc = torch.empty((2, self.ns, n, 2 * s), **f64)
+        self.cc = torch.empty((2, self.ns, m, 2 * s), **f64)
+        self.c = torch.empty((2, p, self.rows, 2 * s), **f64)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.L = _native.lib() if self.dev.type == "cuda" else None
+
+    @staticmethod
+    def eligible(m: int, n: int, s: int, p: int) -> bool:
+        """The full product would run stage 2 on the int8 path (so the
+        decomposition keeps the single-GPU arithmetic), and the exchange stays
+        a modest number of messages (2p per stage buffer and rank)."""
+        return _native.lib().qt_gemm_algo(m, n, s, p) == 1 and p <= 1024
+
+    # ---------------------------------------------------------------- inputs
+    def load_a(self, a1: np.ndarray, a2: np.ndarray) -> None:
+        for k, src in enumerate((a1, a2)):
+            self.a[k].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, self.a0:self.a1]).view(np.float64)))
+
+    def load_b(self, b1: np.ndarray, b2: np.ndarray) -> None:
+        for k, src in enumerate((b1, b2)):
+            self.b[k].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, self.b0:self.b1]).view(np.float64)))
+
+    # ----------------------------------------------------- exchange schedule
+    # Each list is [(view, peer)] in one fixed order (peer, slot, plane) that
+    # the sending and the receiving side enumerate identically, so NCCL's
+    # in-order matching of a send/recv pair lines every piece up.
+    def sends_a(self):
+        if not self.rows:
+            return []
+        return [(self.ah[pl, self.freq[t]], j) for j, (t0, t1) in enumerate(self.ranges)
+                for t in range(t0, t1) for pl in (0, 1)]
+
+    def recvs_a(self):
+        return [(self.ac[pl, t - self.s0, r0:r1], i) for i, (r0, r1) in enumerate(self.arows) if r1 > r0
+                for t in range(self.s0, self.s1) for pl in (0, 1)]
+
+    def sends_b(self):
+        if self.b1 == self.b0:
+            return []
+        return [(self.bh[pl, self.freq[t]], j) for j, (t0, t1) in enumerate(self.ranges)
+                for t in range(t0, t1) for pl in (0, 1)]
+
+    def recvs_b(self):
+        return [(self.bc[pl, t - self.s0, r0:r1], i) for i, (r0, r1) in enumerate(self.brows) if r1 > r0
+                for t in range(self.s0, self.s1) for pl in (0, 1)]
+
+    def sends_c(self):
+        return [(self.cc[pl, t - self.s0, r0:r1], i) for i, (r0, r1) in enumerate(self.arows) if r1 > r0
+                for t in range(self.s0, self.s1) for pl in (0, 1)]
+
+    def recvs_c(self):
+        if not self.rows:
+            return []
+        return [(self.c[pl, self.freq[t]], j) for j, (t0, t1) in enumerate(self.ranges)
+                for t in range(t0, t1) for pl in (0, 1)]
+
+    # ---------------------------------------------------------------- stages
+    def _stream(self, stream):
+        return (self.torch.cuda.current_stream() if stream is None else stream).cuda_stream
+
+    def k1(self, stream=None) -> None:
+        """Forward tube FFTs of this rank's rows of A and of B."""
+        sh, L = self._stream(stream), self.L
+        if self.b1 > self.b0:
+            _native.check(L.qt_qfft3_conj_f64_device(self.b[0].data_ptr(), self.b[1].data_ptr(), self.bh[0].data_ptr(),
+                                                     self.bh[1].data_ptr(), self.b1 - self.b0, self.s, self.p, sh),
+                          "qfft3_conj(B rows)")
+        if self.rows:
+            _native.check(L.qt_qfft3_conj_f64_device(self.a[0].data_ptr(), self.a[1].data_ptr(), self.ah[0].data_ptr(),
+                                                     self.ah[1].data_ptr(), self.rows, self.n, self.p, sh),
+                          "qfft3_conj(A rows)")
+
+    def k2_prepare(self, stream=None):
+        """B' residues of this rank's slots (needs the B̂ exchange only)."""
+        if not self.ns:
+            return None
+        h = ctypes.c_void_p()
+        _native.check(self.L.qt_int8_slots_create(self.bc[0].data_ptr(), self.bc[1].data_ptr(), self.n, self.s, self.p,
+                                                  self.s0, self.ns, self.flag.data_ptr(), self._stream(stream),
+                                                  ctypes.byref(h)), "int8 slots (B')")
+        return h
+
+    def k2_multiply(self, h, stream=None) -> None:
+        """Ĉ of this rank's slots for all m rows (needs the Â exchange)."""
+        if h is None:
+            return
+        sh = self._stream(stream)
+        _native.check(self.L.qt_int8_slots_multiply(h, self.ac[0].data_ptr(), self.ac[1].data_ptr(), self.m,
+                                                    self.cc[0].data_ptr(), self.cc[1].data_ptr(), sh),
+                      "int8 slots multiply")
+        _native.check(self.L.qt_int8_slots_destroy(h, sh), "int8 slots destroy")
+
+    def k3(self, stream=None) -> None:
+        if self.rows:
+            _native.check(self.L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
+                                                           self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
+                                                           self.s, self.p, self._stream(stream)), "qifft3_conj(C rows)")
+
+    def step(self, exchange=None, stream=None) -> None:
+        """One step.  `exchange(sends, recvs)` starts the point-to-point
+        transfers and returns a list of Works to wait on (make_exchange);
+        None runs a single rank (its own pieces are copied locally)."""
+        ex = exchange if exchange is not None else make_exchange(self.rank, None)
+        self.flag.zero_()
+        self.k1(stream)
+        wb = ex(self.sends_b(), self.recvs_b())
+        # (the Â transfers are started before waiting for B̂, so they overlap
+        # the B' residues)
+        wa = ex(self.sends_a(), self.recvs_a())
+        for w in wb:
+            w.wait()
+        h = self.k2_prepare(stream)
+        for w in wa:
+            w.wait()
+        self.k2_multiply(h, stream)
+        for w in ex(self.sends_c(), self.recvs_c()):
+            w.wait()
+        self.k3(stream)
+
+    def nonfinite(self) -> bool:
+        """True if this rank's slots met an inf/NaN (its Ĉ was not written)."""
+        return bool(self.flag.item())
+
+    def result(self):
+        """(c1, c2) of this rank's rows as host complex128 (p, rows, s)."""
+        if self.nonfinite():
+            raise FloatingPointError("frequency-parallel int8 product: non-finite input values; "
+                                     "use Grid2DTProduct (fp64 DMMA stage 2) for this product")
+        out = self.c.cpu().numpy().view(np.complex128)
+        return out[0], out[1]
+
+
+def make_exchange(rank: int, dist_mod, group=None):
+    """exchange(sends, recvs) over torch.distributed point-to-point ops (NCCL:
+    one group of send/recv pairs on the process group's stream; gloo on CPU),
+    with the rank's own pieces copied locally; returns the Works to wait on.
+    dist_mod None: a single rank, local copies only."""
+
+    def ex(sends, recvs):
+        own_src = [v for v, peer in sends if peer == rank]
+        own_dst = [v for v, peer in recvs if peer == rank]
+        assert len(own_src) == len(own_dst)
+        for src, dst in zip(own_src, own_dst):
+            dst.copy_(src)
+        if dist_mod is None:
+            assert len(own_src) == len(sends) and len(own_dst) == len(recvs)
+            return []
+        ops = [dist_mod.P2POp(dist_mod.isend, v, peer, group) for v, peer in sends if peer != rank]
+        ops += [dist_mod.P2POp(dist_mod.irecv, v, peer, group) for v, peer in recvs if peer != rank]
+        return dist_mod.batch_isend_irecv(ops) if ops else []
+
+    return ex
+
+
+def emulate_freq_parallel(ranks) -> None:
+    """Run one step of G FreqParallelTProduct instances (rank r = ranks[r]) on
+    one device in lockstep, moving every exchanged piece by a device copy:
+    the single-GPU check of the decomposition (the kernels' results do not
+    depend on who runs them)."""
+
+    def route(sends_of, recvs_of):
+        inbox = {}
+        for r, x in enumerate(ranks):
+            for v, peer in sends_of(x):
+                inbox.setdefault((r, peer), []).append(v)
+        for r, x in enumerate(ranks):
+            got = {}
+            for v, peer in recvs_of(x):
+                i = got.get(peer, 0)
+                v.copy_(inbox[(peer, r)][i])
+                got[peer] = i + 1
+            for peer, cnt in got.items():
+                assert cnt == len(inbox[(peer, r)])
+
+    for x in ranks:
+        x.flag.zero_()
+        x.k1()
+    route(lambda x: x.sends_b(), lambda x: x.recvs_b())
+    route(lambda x: x.sends_a(), lambda x: x.recvs_a())
+    for x in ranks:
+        x.k2_multiply(x.k2_prepare())
+    route(lambda x: x.sends_c(), lambda x: x.recvs_c())
+    for x in ranks:
+        x.k3()

@@ -65,6 +65,34 @@ def grid_shape(world: int, m: int, s: int) -> tuple[int, int]:
     return best[1], best[2]
 
 
+def slot_freq(p: int, slot: int) -> int:
+    """Frequency of stage-2 slot `slot` (qt_slot_frequency): slots 2j, 2j+1
+    hold the pair (j+1, p-j-1); the self-paired 0 (and p/2 for even p) come
+    last (csrc/qt_ozaki.cu slot_freq)."""
+    npairs = (p - 1) // 2
+    if slot < 2 * npairs:
+        return p - (slot // 2 + 1) if slot & 1 else slot // 2 + 1
+    return 0 if slot == 2 * npairs else p // 2
+
+
+def slot_ranges(p: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous slot ranges [s0, s1), one per rank, for the frequency-
+    parallel decomposition: the work units (a pair = 2 slots, a self-paired
+    frequency = 1 slot; each unit costs the same GEMM) are dealt out as evenly
+    as possible in order, so every range starts even and keeps pairs whole."""
+    npairs = (p - 1) // 2
+    units = [2] * npairs + [1] * (p - 2 * npairs)
+    q, r = divmod(len(units), max(1, world))
+    out, slot, u = [], 0, 0
+    for k in range(world):
+        take = q + (1 if k < r else 0)
+        s0 = slot
+        slot += sum(units[u:u + take])
+        u += take
+        out.append((s0, slot))
+    return out
+
+
 def take_rows(t1: np.ndarray, t2: np.ndarray, lo: int, hi: int):
     """Rows [lo, hi) of a slice-major (p, m, n) tensor, as a contiguous slab."""
     return np.ascontiguousarray(t1[:, lo:hi, :]), np.ascontiguousarray(t2[:, lo:hi, :])

@@ -344,3 +344,118 @@ def test_int8_maximum_contraction_length():
     assert e <= 1e-13, e
     with pytest.raises(ValueError):  # n = 8224 exceeds the exact-accumulation bound
         spectral(*random_spectral(2, 8224, 2, 1, 1), 2, 8224, 2, 1, INT8)
+
+
+# ------------------------------------------------ compact slot ranges (N > 1)
+def slots_product(ah, bh, m, n, s, p, t0, t1, flag=None):
+    """qt_int8_slots_* on the compact slot range [t0, t1) of frequency-ordered
+    Â/B̂; returns the compact Ĉ (slot order) and the non-finite flag."""
+    import ctypes
+    from paper_2212_14318_b200 import shard
+    torch = torch_cuda()
+    L = _native.lib()
+    idx = torch.tensor([shard.slot_freq(p, t) for t in range(t0, t1)], device="cuda")
+    a = ah[:, idx].contiguous()
+    b = bh[:, idx].contiguous()
+    c = torch.zeros((2, t1 - t0, m, s), dtype=torch.complex128, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda") if flag is None else flag
+    h = ctypes.c_void_p()
+    _native.check(L.qt_int8_slots_create(b[0].data_ptr(), b[1].data_ptr(), n, s, p, t0, t1 - t0, flag.data_ptr(), None,
+                                         ctypes.byref(h)), "slots create")
+    _native.check(L.qt_int8_slots_multiply(h, a[0].data_ptr(), a[1].data_ptr(), m, c[0].data_ptr(), c[1].data_ptr(),
+                                           None), "slots multiply")
+    _native.check(L.qt_int8_slots_destroy(h, None), "slots destroy")
+    torch.cuda.synchronize()
+    return c, int(flag.item())
+
+
+@pytest.mark.parametrize("m,n,s,p", [(70, 64, 300, 5), (40, 96, 130, 8), (33, 32, 17, 2), (20, 64, 40, 1),
+                                     (300, 128, 256, 7)])
+def test_int8_slot_ranges_bitwise(m, n, s, p):
+    """Every slot of a compact range equals the same frequency of the full
+    int8 product bitwise, for every range of every decomposition."""
+    from paper_2212_14318_b200 import shard
+    L = _native.lib()
+    assert [L.qt_slot_frequency(p, t) for t in range(p + 1)] == [shard.slot_freq(p, t) for t in range(p)] + [-1]
+    ah, bh = random_spectral(m, n, s, p, 70 + p)
+    full = spectral(ah, bh, m, n, s, p, INT8).cpu().numpy()
+    ranges = {r for G in (1, 2, 3, 5) for r in shard.slot_ranges(p, G) if r[1] > r[0]}
+    for t0, t1 in sorted(ranges):
+        c, flag = slots_product(ah, bh, m, n, s, p, t0, t1)
+        assert flag == 0
+        got = c.cpu().numpy()
+        for t in range(t0, t1):
+            k = shard.slot_freq(p, t)
+            assert bits_equal(got[:, t - t0], full[:, k]), (t0, t1, t)
+
+
+def test_int8_slot_ranges_nonfinite_and_rejection():
+    import ctypes
+    torch = torch_cuda()
+    L = _native.lib()
+    m, n, s, p = 30, 64, 50, 6
+    ah, bh = random_spectral(m, n, s, p, 81)
+    bh[0, 2, 3, 4] = float("nan")  # frequency 2 = slot 2
+    _, flag = slots_product(ah, bh, m, n, s, p, 2, 4)
+    assert flag != 0
+    _, flag = slots_product(ah, bh, m, n, s, p, 0, 2)
+    assert flag == 0
+    ah2, bh2 = random_spectral(m, n, s, p, 82)
+    ah2[1, 5, 0, 0] = float("inf")  # frequency 5 = slot 1 (partner of slot 0)
+    _, flag = slots_product(ah2, bh2, m, n, s, p, 0, 2)
+    assert flag != 0
+    f = torch.zeros(1, dtype=torch.int32, device="cuda")
+    h = ctypes.c_void_p()
+    for t0, ns in [(1, 2), (0, 3), (2, 5), (-2, 2), (0, 0)]:  # splits a pair / leaves [0, p)
+        assert L.qt_int8_slots_create(bh[0].data_ptr(), bh[1].data_ptr(), n, s, p, t0, ns, f.data_ptr(), None,
+                                      ctypes.byref(h)) == _native.QT_EINVAL, (t0, ns)
+    # p = 6: slots 4 (frequency 0) and 5 (frequency 3) are self-paired, so [5, 6) is a valid range
+    ah3, bh3 = random_spectral(m, n, s, p, 83)
+    c, flag = slots_product(ah3, bh3, m, n, s, p, 5, 6)
+    full = spectral(ah3, bh3, m, n, s, p, INT8).cpu().numpy()
+    assert flag == 0 and bits_equal(c.cpu().numpy()[:, 0], full[:, 3])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_freq_parallel_emulated_bitwise(world):
+    """distributed.FreqParallelTProduct, `world` ranks emulated on one GPU in
+    lockstep (every exchanged piece moved by a device copy): each rank's rows
+    of C equal tprod_fast bitwise."""
+    import torch
+    from paper_2212_14318_b200.distributed import FreqParallelTProduct, emulate_freq_parallel
+    m, n, s, p = 150, 256, 520, 6
+    assert FreqParallelTProduct.eligible(m, n, s, p)
+    a = qt.gen_random_tensor(m, n, p, 91)
+    b = qt.gen_random_tensor(n, s, p, 92)
+    want = qt.tprod_fast(a, b)
+    ranks = [FreqParallelTProduct(m, n, s, p, r, world, "cuda:0") for r in range(world)]
+    for x in ranks:
+        x.load_a(a.t1, a.t2)
+        x.load_b(b.t1, b.t2)
+    emulate_freq_parallel(ranks)
+    torch.cuda.synchronize()
+    for x in ranks:
+        c1, c2 = x.result()
+        assert bits_equal(c1, want.t1[:, x.a0:x.a1]) and bits_equal(c2, want.t2[:, x.a0:x.a1]), (world, x.rank)
+
+
+def test_freq_parallel_single_rank_step_and_nonfinite():
+    import torch
+    from paper_2212_14318_b200.distributed import FreqParallelTProduct
+    m, n, s, p = 140, 256, 512, 5
+    a = qt.gen_random_tensor(m, n, p, 93)
+    b = qt.gen_random_tensor(n, s, p, 94)
+    want = qt.tprod_fast(a, b)
+    x = FreqParallelTProduct(m, n, s, p, 0, 1, "cuda:0")
+    x.load_a(a.t1, a.t2)
+    x.load_b(b.t1, b.t2)
+    x.step()
+    torch.cuda.synchronize()
+    c1, c2 = x.result()
+    assert bits_equal(c1, want.t1) and bits_equal(c2, want.t2)
+    b1 = b.t1.copy()
+    b1[2, 3, 4] = float("inf")
+    x.load_b(b1, b.t2)
+    x.step()
+    with pytest.raises(FloatingPointError):
+        x.result()

@@ -248,3 +248,110 @@ def test_grid_shape():
     assert shard.grid_shape(4, 2048, 2048) == (2, 2)
     assert shard.grid_shape(8, 2048, 2048) == (4, 2)
     assert shard.grid_shape(8, 1080, 64) == (8, 1)   # narrow B: plain row sharding
+
+
+def _cpu_freq_class():
+    """FreqParallelTProduct with its three stages restated in numpy (the
+    oracle's tube transforms; the paired per-frequency product of
+    csrc/qt_ozaki.cu in complex arithmetic) and its exchange schedule as is."""
+    import oracle as O
+    from paper_2212_14318_b200 import distributed
+
+    def cview(t):
+        return t.numpy().view(np.complex128)
+
+    class CpuFreq(distributed.FreqParallelTProduct):
+        def k1(self, stream=None):
+            if self.b1 > self.b0:
+                y = O.qfft3_conj((cview(self.b[0]), cview(self.b[1])))
+                cview(self.bh[0])[:], cview(self.bh[1])[:] = y
+            if self.rows:
+                y = O.qfft3_conj((cview(self.a[0]), cview(self.a[1])))
+                cview(self.ah[0])[:], cview(self.ah[1])[:] = y
+
+        def k2_prepare(self, stream=None):
+            return True if self.ns else None
+
+        def k2_multiply(self, h, stream=None):
+            if h is None:
+                return
+            A1, A2, B1, B2 = cview(self.ac[0]), cview(self.ac[1]), cview(self.bc[0]), cview(self.bc[1])
+            C1, C2 = cview(self.cc[0]), cview(self.cc[1])
+            for t in range(self.s0, self.s1):
+                k = self.freq[t]
+                part = t if (self.p - k) % self.p == k else t ^ 1
+                i, j = t - self.s0, part - self.s0
+                C1[i] = A1[i] @ B1[i] - np.conj(A2[j]) @ B2[i]
+                C2[i] = A2[i] @ B1[i] + np.conj(A1[j]) @ B2[i]
+
+        def k3(self, stream=None):
+            if self.rows:
+                y = O.qifft3_conj((cview(self.c[0]), cview(self.c[1])))
+                cview(self.c[0])[:], cview(self.c[1])[:] = y
+
+    return CpuFreq
+
+
+def _worker_freq(rank, world, port, m, n, s, p, out_path):
+    """distributed.FreqParallelTProduct's exchange over gloo point-to-point
+    ops (make_exchange), stages on the CPU: Â/B̂ row pieces to the slot
+    owners, Ĉ pieces back to the row owners."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2212_14318_b200 import distributed, shard
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    A = O.gen_random_tensor(m, n, p, 41)
+    B = O.gen_random_tensor(n, s, p, 42)
+    x = _cpu_freq_class()(m, n, s, p, rank, world, device="cpu")
+    x.load_a(*A)
+    x.load_b(*B)
+    x.step(distributed.make_exchange(rank, dist))
+    c = x.c.numpy().view(np.complex128)
+    mb = -(-m // world)
+    buf = np.zeros((2, p, mb, s), np.complex128)
+    buf[:, :, :x.rows] = c
+    tt = torch.from_numpy(buf.view(np.float64))
+    gathered = [torch.zeros_like(tt) for _ in range(world)] if rank == 0 else None
+    dist.gather(tt, gathered, dst=0)
+    if rank == 0:
+        out = np.zeros((2, p, m, s), np.complex128)
+        for r, g in enumerate(gathered):
+            r0, r1 = shard.row_slab(m, world, r)
+            out[:, :, r0:r1] = g.numpy().view(np.complex128)[:, :, :r1 - r0]
+        np.save(out_path, out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,s,p,world", [(9, 5, 6, 8, 2), (7, 3, 4, 7, 2), (5, 6, 3, 4, 3), (3, 2, 2, 2, 2)])
+def test_freq_parallel_exchange(tmp_path, m, n, s, p, world):
+    import oracle as O
+    out = str(tmp_path / "c.npy")
+    mp.spawn(_worker_freq, args=(world, _free_port(), m, n, s, p, out), nprocs=world, join=True)
+    got = np.load(out)
+    A = O.gen_random_tensor(m, n, p, 41)
+    B = O.gen_random_tensor(n, s, p, 42)
+    # the same stages on one rank: bitwise (every slot is computed identically)
+    one = _cpu_freq_class()(m, n, s, p, 0, 1, device="cpu")
+    one.load_a(*A)
+    one.load_b(*B)
+    one.step()
+    assert np.array_equal(got.view(np.uint64), one.c.numpy().view(np.uint64))
+    want = O.tprod_fast(A, B)
+    assert O.rel_frob_error((got[0], got[1]), want) < 1e-13
+
+
+def test_slot_ranges_keep_pairs_whole():
+    from paper_2212_14318_b200 import shard
+    for p in range(1, 70):
+        assert sorted(shard.slot_freq(p, t) for t in range(p)) == list(range(p))
+        for world in (1, 2, 3, 8):
+            rs = shard.slot_ranges(p, world)
+            assert rs[0][0] == 0 and rs[-1][1] == p and all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            pair_end = 2 * ((p - 1) // 2)
+            assert all(not (b & 1 and b < pair_end) for r in rs for b in r)
+            sizes = [(min(t1, pair_end) - min(t0, pair_end)) // 2 + max(0, t1 - max(t0, pair_end)) for t0, t1 in rs]
+            assert max(sizes) - min(sizes) <= 1
