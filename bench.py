@@ -77,6 +77,9 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
+    ap.add_argument("--multi", choices=["auto", "freq", "grid"], default="auto",
+                    help="N > 1 decomposition: freq = frequency-parallel (int8 stage 2), grid = 2-D blocks of C; "
+                         "auto = freq when the product takes the int8 stage 2")
     ap.add_argument("--sharded", action="store_true",
                     help="use the N>1 row-sharded chunked-broadcast pipeline even on one GPU (no broadcast)")
     return ap.parse_args()
@@ -271,6 +274,8 @@ def run_ours(args, cfg):
 
     lo, hi = shard.row_slab(cfg.m, world, rank)
     rows, cols = hi - lo, cfg.s  # this rank's block of C (whole C at N = 1)
+    mode = None
+    k2_shape = None  # (rows, cols, frequencies) of this rank's stage 2, if not (rows, cols, p)
     # N = 1: pinned host inputs (the e2e leg copies from them); N > 1: every
     # rank regenerates A and B (sequential generator) and keeps the pieces it owns
     sharded_mode = world > 1 or args.sharded
@@ -291,46 +296,69 @@ def run_ours(args, cfg):
                                        dc1.data_ptr(), dc2.data_ptr(), rows, cfg.n, cfg.s, cfg.p, sh)
             qt._native.check(rc, "tprod_fast")
     else:
-        # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
-        # block arrive as pieces broadcast (NCCL) from their owners inside the
-        # step, overlapping K1 / stage 2 (paper_2212_14318_b200/distributed.py)
-        from paper_2212_14318_b200.distributed import Grid2DTProduct
-        sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
-        gr, gc = sharded.gr, sharded.gc
-        sharded.load_a(a.t1, a.t2)
-        sharded.load_b(b.t1, b.t2)
-        # pinned host copies of the pieces this rank owns (and uploads) for the e2e leg
-        pin_own = []
-        for k, t in enumerate(sharded.a):
-            if sharded.owns_a(k):
-                pa = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
-                pa.copy_(t)
-                pin_own.append((t, pa))
-        for k, t in enumerate(sharded.b):
-            if sharded.owns_b(k):
-                pb = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
-                pb.copy_(t)
-                pin_own.append((t, pb))
+        from paper_2212_14318_b200.distributed import FreqParallelTProduct, Grid2DTProduct, make_exchange
+        mode = args.multi
+        if mode == "auto":
+            mode = "freq" if FreqParallelTProduct.eligible(cfg.m, cfg.n, cfg.s, cfg.p) else "grid"
+        pin_own = []  # (device buffer, pinned host copy) this rank uploads on the e2e leg
+
+        def pin(t):
+            pt = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+            pt.copy_(t)
+            pin_own.append((t, pt))
+
+        if mode == "freq":
+            # frequency-parallel: K1 of this rank's rows of A and B, Â/B̂ pieces
+            # point to point to the owners of their frequency slots, int8 stage 2
+            # of this rank's slots, Ĉ pieces back, K3 of this rank's rows of C
+            sharded = FreqParallelTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+            sharded.load_a(a.t1, a.t2)
+            sharded.load_b(b.t1, b.t2)
+            pin(sharded.a)
+            pin(sharded.b)
+            exchange = make_exchange(rank, dist if world > 1 else None)
+            rows, cols = sharded.rows, cfg.s
+            if world > 1:
+                dist.barrier()  # communicator up on every rank before the first point-to-point group
+
+            def step():
+                sharded.step(exchange)
+        else:
+            # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
+            # block arrive as pieces broadcast (NCCL) from their owners inside the
+            # step, overlapping K1 / stage 2 (paper_2212_14318_b200/distributed.py)
+            sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+            gr, gc = sharded.gr, sharded.gc
+            sharded.load_a(a.t1, a.t2)
+            sharded.load_b(b.t1, b.t2)
+            for k, t in enumerate(sharded.a):
+                if sharded.owns_a(k):
+                    pin(t)
+            for k, t in enumerate(sharded.b):
+                if sharded.owns_b(k):
+                    pin(t)
+            rows, cols = sharded.rows, sharded.cols
+            bcast_row = bcast_col = None
+            if world > 1:
+                # every rank creates every group, in the same order
+                row_groups = [dist.new_group([i * gc + k for k in range(gc)]) for i in range(gr)]
+                col_groups = [dist.new_group([k * gc + j for k in range(gr)]) for j in range(gc)]
+                if gc > 1:
+                    bcast_row = lambda t, src: dist.broadcast(t, src, group=row_groups[sharded.i], async_op=True)
+                if gr > 1:
+                    bcast_col = lambda t, src: dist.broadcast(t, src, group=col_groups[sharded.j], async_op=True)
+
+            def step():
+                sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
         del a, b
-        rows, cols = sharded.rows, sharded.cols
-        bcast_row = bcast_col = None
-        if world > 1:
-            # every rank creates every group, in the same order
-            row_groups = [dist.new_group([i * gc + k for k in range(gc)]) for i in range(gr)]
-            col_groups = [dist.new_group([k * gc + j for k in range(gr)]) for j in range(gc)]
-            if gc > 1:
-                bcast_row = lambda t, src: dist.broadcast(t, src, group=row_groups[sharded.i], async_op=True)
-            if gr > 1:
-                bcast_col = lambda t, src: dist.broadcast(t, src, group=col_groups[sharded.j], async_op=True)
         # stage-timing operands of this rank's block shape
         da1 = torch.randn((cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
         da2 = torch.randn_like(da1)
         db1 = torch.randn((cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
         db2 = torch.randn_like(db1)
         dc1, dc2 = sharded.c[0], sharded.c[1]
-
-        def step():
-            sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
+        if mode == "freq":  # this rank's stage 2: all m x s of its ns frequency slots
+            k2_shape = (cfg.m, cfg.s, max(1, sharded.ns))
 
     # clocks are sampled from the first warm-up step through the per-kernel
     # timing loops, so short steps still yield samples under load
@@ -366,13 +394,21 @@ def run_ours(args, cfg):
     value = cfg.flops_eff / (ms * 1e-3) / 1e9  # whole-job GFLOP/s (all ranks' rows)
 
     # ---- per-kernel timing for the roofline (same stream, CUDA events) ----
-    # (full-B stage kernels; with N > 1 ranks the rank-0-shaped K2 on its slab)
-    ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
-    bh = torch.empty((2, cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
-    qt._native.check(L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
-                                                rows, cfg.n, cfg.p, sh), "qfft3")
-    qt._native.check(L.qt_qfft3_conj_f64_device(db1.data_ptr(), db2.data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(),
-                                                cfg.n, cols, cfg.p, sh), "qfft3")
+    # (full-B stage kernels; with N > 1 ranks this rank's block / slot shape)
+    krows, kcols, kp = k2_shape or (rows, cols, cfg.p)
+    ah = torch.empty((2, kp, krows, 2 * cfg.n), dtype=torch.float64, device=dev)
+    bh = torch.empty((2, kp, cfg.n, 2 * kcols), dtype=torch.float64, device=dev)
+    kc = torch.empty((2, kp, krows, 2 * kcols), dtype=torch.float64, device=dev) if k2_shape else None
+    kc1, kc2 = (kc[0], kc[1]) if k2_shape else (dc1, dc2)
+    ka1 = torch.randn((kp, krows, 2 * cfg.n), dtype=torch.float64, device=dev) if k2_shape else da1
+    ka2 = torch.randn_like(ka1) if k2_shape else da2
+    kb1 = torch.randn((kp, cfg.n, 2 * kcols), dtype=torch.float64, device=dev) if k2_shape else db1
+    kb2 = torch.randn_like(kb1) if k2_shape else db2
+    qt._native.check(L.qt_qfft3_conj_f64_device(ka1.data_ptr(), ka2.data_ptr(), ah[0].data_ptr(), ah[1].data_ptr(),
+                                                krows, cfg.n, kp, sh), "qfft3")
+    qt._native.check(L.qt_qfft3_conj_f64_device(kb1.data_ptr(), kb2.data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(),
+                                                cfg.n, kcols, kp, sh), "qfft3")
+    del ka1, ka2, kb1, kb2
 
     def timed(fn, reps):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
@@ -387,18 +423,18 @@ def run_ours(args, cfg):
 
     algo = L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p)   # 0 = fp64 DMMA, 1 = exact int8 (tcgen05)
     gemm_ms = timed(lambda: L.qt_spectral_product_f64_device_ld_algo(
-        ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), dc1.data_ptr(), dc2.data_ptr(), rows,
-        cfg.n, cols, cfg.p, cols, cols, cfg.n * cols, rows * cols, algo, sh), max(2, args.steps))
+        ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), kc1.data_ptr(), kc2.data_ptr(), krows,
+        cfg.n, kcols, kp, kcols, kcols, cfg.n * kcols, krows * kcols, algo, sh), max(2, args.steps))
     # stage-2 accuracy of the algorithm this workload takes, on this run's data:
     # the int8 (exact modular) result against the fp64 DMMA result (both on the GPU)
     accuracy = None
     if algo == 1:
-        c8 = torch.empty((2, cfg.p, rows, 2 * cols), dtype=torch.float64, device=dev)
+        c8 = torch.empty((2, kp, krows, 2 * kcols), dtype=torch.float64, device=dev)
         cd = torch.empty_like(c8)
         for algo_id, dst in ((1, c8), (0, cd)):
             qt._native.check(L.qt_spectral_product_f64_device_ld_algo(
                 ah[0].data_ptr(), ah[1].data_ptr(), bh[0].data_ptr(), bh[1].data_ptr(), dst[0].data_ptr(),
-                dst[1].data_ptr(), rows, cfg.n, cols, cfg.p, cols, cols, cfg.n * cols, rows * cols, algo_id, sh),
+                dst[1].data_ptr(), krows, cfg.n, kcols, kp, kcols, kcols, cfg.n * kcols, krows * kcols, algo_id, sh),
                 "spectral(accuracy)")
         torch.cuda.synchronize()
         num = float(torch.linalg.vector_norm(c8 - cd).item())
@@ -408,11 +444,13 @@ def run_ours(args, cfg):
                             "exact in integers (53-bit scaled inputs, one final rounding), tests/test_gpu_int8.py "
                             "shows its error vs a long-double truth is <= the fp64 GEMM's"}
         del c8, cd
+    del ah, bh, kc
+    ah = torch.empty((2, cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
     fftA_ms = timed(lambda: L.qt_qfft3_conj_f64_device(da1.data_ptr(), da2.data_ptr(), ah[0].data_ptr(),
                                                        ah[1].data_ptr(), rows, cfg.n, cfg.p, sh), max(3, args.steps))
     ifft_ms = timed(lambda: L.qt_qifft3_conj_f64_device(dc1.data_ptr(), dc2.data_ptr(), dc1.data_ptr(),
                                                         dc2.data_ptr(), rows, cols, cfg.p, sh), max(3, args.steps))
-    del ah, bh
+    del ah
     # ---- per-kernel device time of the stage-2 GEMM kernel itself (library
     # CUDA events on the launching stream, qt_prof_*), over a few extra steps
     nprof = max(2, args.steps)
@@ -458,19 +496,20 @@ def run_ours(args, cfg):
     clk.__exit__(None, None, None)
     peaks, peak_src = load_peaks()
     gauss = os.environ.get("QTB_GEMM", "3m")[:1] != "4"
-    gemm_tf = 32.0 * rows * cfg.n * cols * cfg.p / (gemm_ms * 1e-3) / 1e12   # algorithmic (reference) flops
+    gemm_tf = 32.0 * krows * cfg.n * kcols * kp / (gemm_ms * 1e-3) / 1e12   # algorithmic (reference) flops
     exec_tf = gemm_tf * (0.75 if gauss else 1.0)                              # DMMA flops actually executed
     fftA_gbs = 2 * cfg.bytes_tensor(rows, cfg.n) / (fftA_ms * 1e-3) / 1e9
     ifft_gbs = 2 * cfg.bytes_tensor(rows, cols) / (ifft_ms * 1e-3) / 1e9
-    gemm_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cols) + cfg.bytes_tensor(rows, cols)
-    gemm_ai = 32.0 * rows * cfg.n * cols * cfg.p / gemm_bytes
+    gemm_bytes = (cfg.bytes_tensor(krows, cfg.n) + cfg.bytes_tensor(cfg.n, kcols) + cfg.bytes_tensor(krows, kcols)) \
+        * kp / cfg.p
+    gemm_ai = 32.0 * krows * cfg.n * kcols * kp / gemm_bytes
     ridge = PEAK_FP64_DMMA_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
     algo_txt = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
                 else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
     if algo == 1 and "k2_int8_gemm" in prof:
         # exact int8 path: 15 modular GEMMs of the real-embedded (2m x 4n) . (4n x 2s) product per frequency
         k_ms = prof["k2_int8_gemm"]["ms_per_step"]
-        ops = 2.0 * 15 * (2 * rows) * (4 * cfg.n) * (2 * cols) * cfg.p
+        ops = 2.0 * 15 * (2 * krows) * (4 * cfg.n) * (2 * kcols) * kp
         ach = ops / (k_ms * 1e-3) / 1e12
         peak_i8 = 2.0 * peaks["bf16_tflops"]
         roof = {"kernel": "K2 int8 modular GEMM oz_gemm2_kernel (tcgen05.mma.cta_group::2.kind::i8, TMA, TMEM)",
@@ -483,7 +522,7 @@ def run_ours(args, cfg):
                 "algorithm": "exact Ozaki-II: 53-bit scaled integers (norm-bounded), 15 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
                 "kernel_ms": k_ms, "launches_per_step": prof["k2_int8_gemm"]["launches_per_step"],
                 "share_of_step": k_ms / ms,
-                "fp64_equivalent_tflops": 32.0 * rows * cfg.n * cols * cfg.p / (k_ms * 1e-3) / 1e12,
+                "fp64_equivalent_tflops": 32.0 * krows * cfg.n * kcols * kp / (k_ms * 1e-3) / 1e12,
                 "concurrency": "frequency batches software-pipelined over two streams: the residue and CRT "
                                "kernels of neighbouring batches run beside this kernel (kernel_ms is its own "
                                "event-timed duration, which includes that sharing)",
@@ -493,11 +532,11 @@ def run_ours(args, cfg):
             roof["isolated"] = {"kernel_ms": iso_ms, "achieved": ops / (iso_ms * 1e-3) / 1e12,
                                 "frac": ops / (iso_ms * 1e-3) / 1e12 / peak_i8,
                                 "note": "same kernel, batches in order (QTB_OZAKI_PIPE=0), nothing co-running"}
-        traffic, traffic_src = ncu_traffic(cfg, "K2_int8_gemm", rows)
+        traffic, traffic_src = ncu_traffic(cfg, "K2_int8_gemm", rows if k2_shape is None else -1)
         roof["algorithmic_bytes"] = None
     elif gemm_ai >= ridge:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
-        ktf = 32.0 * rows * cfg.n * cols * cfg.p / (k_ms * 1e-3) / 1e12
+        ktf = 32.0 * krows * cfg.n * kcols * kp / (k_ms * 1e-3) / 1e12
         roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": ktf,
                 "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ktf / PEAK_FP64_DMMA_TFLOPS,
                 "peak_source": "measured fp64 DMMA burst (profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no fp64",
@@ -506,7 +545,7 @@ def run_ours(args, cfg):
                 "algorithm": algo_txt, "executed_tflops": ktf * (0.75 if gauss else 1.0),
                 "executed_frac": ktf * (0.75 if gauss else 1.0) / PEAK_FP64_DMMA_TFLOPS,
                 "kernel_ms": k_ms, "share_of_step": k_ms / ms, "traffic": None}
-        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows if k2_shape is None else -1)
         roof["algorithmic_bytes"] = gemm_bytes
     else:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
@@ -516,7 +555,7 @@ def run_ours(args, cfg):
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
                 "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "algorithm": algo_txt,
                 "kernel_ms": k_ms, "share_of_step": k_ms / ms, "traffic": None}
-        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows)
+        traffic, traffic_src = ncu_traffic(cfg, "K2_gemm", rows if k2_shape is None else -1)
         roof["algorithmic_bytes"] = gemm_bytes
     roof["traffic"] = traffic
     roof["traffic_source"] = traffic_src
@@ -640,7 +679,9 @@ def run_ours(args, cfg):
             "accuracy": accuracy,
             "fp64_dmma_path": dmma_path,
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                       "parallelism": (f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts"
+                       "parallelism": ((f"freq{world}(frequency slots; rows of A, B, C for the tube FFTs)"
+                                        "+point-to-point exchange" if mode == "freq" else
+                                        f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts")
                                        if sharded_mode else f"rows{world}")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
                        "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",

@@ -77,20 +77,20 @@ def slot_freq(p: int, slot: int) -> int:
 
 def slot_ranges(p: int, world: int) -> list[tuple[int, int]]:
     """Contiguous slot ranges [s0, s1), one per rank, for the frequency-
-    parallel decomposition: the work units (a pair = 2 slots, a self-paired
-    frequency = 1 slot; each unit costs the same GEMM) are dealt out as evenly
-    as possible in order, so every range starts even and keeps pairs whole."""
-    npairs = (p - 1) // 2
-    units = [2] * npairs + [1] * (p - 2 * npairs)
-    q, r = divmod(len(units), max(1, world))
-    out, slot, u = [], 0, 0
-    for k in range(world):
-        take = q + (1 if k < r else 0)
-        s0 = slot
-        slot += sum(units[u:u + take])
-        u += take
-        out.append((s0, slot))
-    return out
+    parallel decomposition.  Every slot costs the same stage-2 GEMM (a pair is
+    two slots, a self-paired frequency one), so the boundaries sit at the
+    nearest slot to k p / world that does not split a pair (an odd slot below
+    2 ((p - 1) / 2)): range sizes differ by at most 2 slots."""
+    pair_end = 2 * ((p - 1) // 2)
+    bounds = [0]
+    for k in range(1, world):
+        ideal = k * p / world
+        b = int(round(ideal))
+        if b & 1 and b < pair_end:
+            b = b - 1 if ideal < b else b + 1
+        bounds.append(min(p, max(bounds[-1], b)))
+    bounds.append(p)
+    return list(zip(bounds[:-1], bounds[1:]))
 
 
 def take_rows(t1: np.ndarray, t2: np.ndarray, lo: int, hi: int):

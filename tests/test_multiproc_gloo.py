@@ -353,5 +353,5 @@ def test_slot_ranges_keep_pairs_whole():
             assert rs[0][0] == 0 and rs[-1][1] == p and all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             pair_end = 2 * ((p - 1) // 2)
             assert all(not (b & 1 and b < pair_end) for r in rs for b in r)
-            sizes = [(min(t1, pair_end) - min(t0, pair_end)) // 2 + max(0, t1 - max(t0, pair_end)) for t0, t1 in rs]
-            assert max(sizes) - min(sizes) <= 1
+            sizes = [t1 - t0 for t0, t1 in rs]
+            assert max(sizes) - min(sizes) <= 2, (p, world, rs)
