@@ -74,6 +74,11 @@ uint64_t qt_kernel_launches(void);
  * (tcgen05 int8 modular GEMM), "k2_int8_residues", "k2_int8_crt". */
 void qt_prof_enable(int on);
 int qt_prof_read(const char* tag, double* ms, uint64_t* launches);
+/* Timeline mode (qt_prof_enable(2)): every tagged launch is also kept in
+ * order; qt_prof_timeline writes "tag stream start_ms end_ms" lines (times
+ * from the enable call) into buf (NUL-terminated, truncated to cap), clears
+ * them and returns the full text length (negative status on error). */
+int qt_prof_timeline(char* buf, uint64_t cap);
 
 /* ---- device-resident entry points (all pointers are device pointers) ---
  * stream is a cudaStream_t (NULL = legacy default stream).  Work is enqueued

@@ -27,6 +27,7 @@ SIGNATURES = {
     "qt_last_error": (ctypes.c_char_p, []),
     "qt_kernel_launches": (_u64, []),
     "qt_prof_enable": (None, [ctypes.c_int]),
+    "qt_prof_timeline": (ctypes.c_int, [ctypes.c_char_p, _u64]),
     "qt_prof_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "qt_tprod_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_qfft3_conj_f64_device": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),

@@ -222,12 +222,24 @@ namespace {
 std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;
 std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
+// timeline mode (qt_prof_enable(2)): every scope also kept in launch order
+struct TlRec {
+  const char* tag;
+  cudaStream_t st;
+  cudaEvent_t e0, e1;
+};
+std::atomic<bool> g_tl{false};
+std::vector<TlRec> g_tl_rec;
+cudaEvent_t g_tl_base = nullptr;
 }  // namespace
 
 bool prof_on() { return g_prof.load(std::memory_order_relaxed); }
 
 ProfScope::ProfScope(const char* t, cudaStream_t s) : tag(t), st(s) {
-  if (prof_on() && cudaEventCreate(&e0) == cudaSuccess) cudaEventRecord(e0, st);
+  if (prof_on() && cudaEventCreate(&e0) == cudaSuccess) {
+    cudaEventRecord(e0, st);
+    if (g_tl.load(std::memory_order_relaxed) && cudaEventCreate(&t0) == cudaSuccess) cudaEventRecord(t0, st);
+  }
 }
 
 void ProfScope::stop() {
@@ -237,6 +249,16 @@ void ProfScope::stop() {
   cudaEventRecord(e1, st);
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_ev[tag].emplace_back(e0, e1);
+  if (t0) {
+    cudaEvent_t t1 = nullptr;
+    if (cudaEventCreate(&t1) == cudaSuccess) {
+      cudaEventRecord(t1, st);
+      g_tl_rec.push_back(TlRec{tag, st, t0, t1});
+    } else {
+      cudaEventDestroy(t0);
+    }
+    t0 = nullptr;
+  }
   e0 = nullptr;
 }
 
@@ -252,7 +274,47 @@ const char* qt_last_error(void) { return t_err.c_str(); }
 
 uint64_t qt_kernel_launches(void) { return g_launches.load(); }
 
-void qt_prof_enable(int on) { g_prof.store(on != 0); }
+void qt_prof_enable(int on) {
+  if (on == 2) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaDeviceSynchronize();
+    if (!g_tl_base) cudaEventCreate(&g_tl_base);
+    cudaEventRecord(g_tl_base, 0);
+    g_tl.store(true);
+  } else if (!on) {
+    g_tl.store(false);
+  }
+  g_prof.store(on != 0);
+}
+
+int qt_prof_timeline(char* buf, uint64_t cap) {
+  t_err.clear();
+  std::vector<TlRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    recs.swap(g_tl_rec);
+  }
+  std::string out;
+  int rc = QT_OK;
+  for (auto& r : recs) {
+    float a = 0.f, b = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e == cudaSuccess && g_tl_base) e = cudaEventElapsedTime(&a, g_tl_base, r.e0);
+    if (e == cudaSuccess && g_tl_base) e = cudaEventElapsedTime(&b, g_tl_base, r.e1);
+    if (e != cudaSuccess && rc == QT_OK) rc = cuda_fail(e, "qt_prof_timeline");
+    char line[160];
+    snprintf(line, sizeof line, "%s %p %.4f %.4f\n", r.tag, (void*)r.st, a, b);
+    out += line;
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  if (buf && cap) {
+    const size_t k = std::min<size_t>(out.size(), cap - 1);
+    memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return rc != QT_OK ? -rc : (int)out.size();
+}
 
 int qt_prof_read(const char* tag, double* ms, uint64_t* launches) {
   t_err.clear();
@@ -785,7 +847,7 @@ int qt_int8_plan_multiply(void* plan, const double* bh1, const double* bh2, doub
   cudaError_t e = cudaMemcpyAsync(flag, P->flags, sizeof(int), cudaMemcpyDeviceToDevice, st);
   OzakiB B;
   if (e == cudaSuccess)
-    e = ozaki_prepare_b((const double2*)bh1, (const double2*)bh2, m, n, s, p, ldb, bslice, flag, true, &B, st);
+    e = ozaki_prepare_b((const double2*)bh1, (const double2*)bh2, m, n, s, p, ldb, bslice, flag, true, &B, st, true);
   if (e == cudaSuccess)
     e = ozaki_multiply_prepared(P->A, B, (double2*)ch1, (double2*)ch2, ldc, cslice, flag, st);
   if (B.res) {

@@ -99,10 +99,17 @@ struct OzakiB {
   int nslots = 0;
   bool all = false;
   int s0 = 0, ns = 0, cbase = -1;  // slot range; cbase >= 0: compact operand tensors (slot - cbase)
+  // all && !ready: B' is built batch by batch inside the first multiply (its
+  // residues pipelined beside the GEMMs of earlier batches) from bh1/bh2
+  bool ready = false;
+  const double2* bh1 = nullptr;
+  const double2* bh2 = nullptr;
 };
+// lazy: with B' kept for every slot, defer its residues into the first
+// multiply's batch pipeline (B̂ must stay valid until then)
 cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                             uint64_t ldb, uint64_t bslice, int* flag, bool require_all, OzakiB* out,
-                            cudaStream_t stream);
+                            cudaStream_t stream, bool lazy = false);
 cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                            uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
                            cudaStream_t stream);
@@ -164,6 +171,7 @@ struct ProfScope {
   const char* tag;
   cudaStream_t st;
   cudaEvent_t e0 = nullptr;
+  cudaEvent_t t0 = nullptr;  // timeline twin of e0 (qt_prof_enable(2))
   ProfScope(const char* t, cudaStream_t s);
   void stop();
 };

@@ -691,15 +691,17 @@ __global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* _
   eB[f * Sp + c] = e;
 }
 
-// B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
+// B side, pass 2: one CTA per (slot f, 32 columns, 32-row block of Y); writes
 // the Re-row [Re Y | -Im Y] and the Im-row [Im Y | Re Y] of each column.  Row
 // order inside a slot: tile t = c / 128 holds its 128 Re-rows, then its 128
-// Im-rows.  Columns c >= s (padding) get zero rows.  The 128 x 32 block is
+// Im-rows.  Columns c >= s (padding) get zero rows.  The 32 x 32 block is
 // transposed through shared memory (column-major, row j at j + j/8 so both the
 // column-wise fill and the 4-consecutive-rows-per-lane reads are conflict
-// free); each warp then writes 128 contiguous bytes of a B' row per store.
-constexpr int kBRows = 128;
-constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 145 double2 per column
+// free); 8 lanes then write one 32-byte sector of a B' row per store.  19 KB
+// of shared memory, so a CTA fits beside the GEMM's 193 KB on every SM and
+// the B' residues of the next frequency batch run under the current GEMM.
+constexpr int kBRows = 32;
+constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 37 double2 per column
 constexpr size_t kResBSmem = sizeof(double2) * 32 * kBStride;
 __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2,
@@ -719,9 +721,10 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   }
   __syncthreads();
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
-  const int jl = 4 * tx, jb = j0 + jl;  // this lane's 4 consecutive rows
+  const int jl = 4 * (tx & 7), jb = j0 + jl;  // this lane's 4 consecutive rows
   if (jb >= 2 * n) return;
-  for (int cc = ty; cc < 32; cc += 8) {
+  {
+    const int cc = ty * 4 + (tx >> 3);
     const int c = c0 + cc;
     const int e = eB[f * Sp + c];
     const int tcol = c / BNC, ic = c % BNC;
@@ -1054,11 +1057,17 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     f0 = B.s0 + i * F;
     fcur = (int)std::min<uint64_t>(F, B.s0 + ps - f0);
   };
+  const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
   auto residues = [&](uint64_t i, cudaStream_t st) {
     uint64_t f0;
     int fcur;
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
+    if (lazyB) {
+      const cudaError_t eb = prep_b(B, B.bh1, B.bh2, f0, fcur, (int)(f0 - B.s0), flag, st);
+      if (eb != cudaSuccess && e == cudaSuccess) e = eb;
+    }
+    if (A) return;
     ProfScope pr("k2_int8_residues", st);
     oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp, eA + b * F * Mp,
                                                                  flag, (int)m, (int)n, (int)p, (int)f0, (int)Mp,
@@ -1082,7 +1091,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     pc.stop();
     count_launches(1);
   };
-  if (e == cudaSuccess && !A) residues(0, stream);
+  if (e == cudaSuccess && (!A || lazyB)) residues(0, stream);
   cudaEvent_t res_ready = nullptr, prev_gemm_done = nullptr;
   for (uint64_t i = 0; i < nbatch && e == cudaSuccess; ++i) {
     uint64_t f0;
@@ -1115,7 +1124,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
       cudaEventRecord(gemm_done, stream);
       // aux: X' residues of batch i+1 into the other buffer (free once GEMM i-1,
       // which precedes GEMM i on the main stream, is done), then the CRT of batch i
-      if (!A && i + 1 < nbatch) {
+      if ((!A || lazyB) && i + 1 < nbatch) {
         if (prev_gemm_done) cudaStreamWaitEvent(aux, prev_gemm_done, 0);  // GEMM i-1 read this X' buffer
         residues(i + 1, aux);
       }
@@ -1126,7 +1135,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
       prev_gemm_done = gemm_done;
     } else {
       crt(i, stream);
-      if (!A && B.all && i + 1 < nbatch) residues(i + 1, stream);
+      if ((!A || lazyB) && B.all && i + 1 < nbatch) residues(i + 1, stream);
     }
     e = cudaGetLastError();
   }
@@ -1135,6 +1144,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     cudaEventRecord(join, aux);
     cudaStreamWaitEvent(stream, join, 0);
   }
+  if (e == cudaSuccess && lazyB) B.ready = true;
   const cudaError_t fe = cudaFreeAsync(ws, stream);
   if (aux != stream) cudaStreamDestroy(aux);
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
@@ -1145,7 +1155,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
 
 cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                             uint64_t ldb, uint64_t bslice, int* flag, bool require_all, OzakiB* out,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, bool lazy) {
   *out = OzakiB{};
   if (n % 32 != 0 || n > 8192 || p == 0) return cudaErrorInvalidValue;
   cudaError_t e = oz_init();
@@ -1169,7 +1179,10 @@ cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, 
   if ((e = cudaMallocAsync(&B.res, bytes + (size_t)B.nslots * pad_cols(s) * sizeof(int), stream)) != cudaSuccess)
     return e;
   B.eB = reinterpret_cast<int*>(B.res + bytes);
-  if (B.all) e = prep_b(B, bh1, bh2, 0, (int)p, 0, flag, stream);
+  B.bh1 = bh1;
+  B.bh2 = bh2;
+  if (B.all && !lazy) e = prep_b(B, bh1, bh2, 0, (int)p, 0, flag, stream);
+  B.ready = B.all && !lazy;
   if (e != cudaSuccess) {
     cudaFreeAsync(B.res, stream);
     return e;
@@ -1213,6 +1226,7 @@ cudaError_t ozaki_prepare_b_slots(const double2* bh1, const double2* bh2, uint64
     cudaFreeAsync(B.res, stream);
     return e;
   }
+  B.ready = true;
   *out = B;
   return cudaSuccess;
 }
@@ -1274,7 +1288,8 @@ cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, c
   cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   OzakiB B;
-  if ((e = ozaki_prepare_b(bh1, bh2, m, n, s, p, ldb, bslice, flag, false, &B, stream)) != cudaSuccess) return e;
+  if ((e = ozaki_prepare_b(bh1, bh2, m, n, s, p, ldb, bslice, flag, false, &B, stream, true)) != cudaSuccess)
+    return e;
   e = ozaki_multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
   const cudaError_t fe = ozaki_release(B, stream);
   return e != cudaSuccess ? e : fe;
