@@ -464,7 +464,8 @@ def run_ours(args, cfg):
     def read_prof(steps_done=None):
         steps_done = steps_done or nprof
         out = {}
-        for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_crt"):
+        for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_residues_b", "k2_int8_colnorms",
+                    "k2_int8_crt"):
             t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
             qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
             if n_l.value:

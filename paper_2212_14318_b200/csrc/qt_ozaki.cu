@@ -281,9 +281,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // CTAs land on the even CTA's full[s]; MMA commits multicast to both CTAs'
 // empty[s] / tfull[b]; both epilogues arrive on the even CTA's tempty[b].
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the even CTA's copy
-constexpr int STAGES2 = 6;
 constexpr int B2_STAGE = (BN / 2) * BK;  // 16 KB: this CTA's half of the B' tile
-constexpr size_t GEMM2_SMEM = (size_t)STAGES2 * (A_STAGE + B2_STAGE) + 1024;
+constexpr size_t gemm2_smem(int stages) { return (size_t)stages * (A_STAGE + B2_STAGE) + 1024; }
 constexpr uint32_t kIdesc2 = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
 
@@ -315,6 +314,7 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+template <int STAGES2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     oz_gemm2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                     GemmParams P) {
@@ -918,8 +918,11 @@ cudaError_t oz_init() {
     if (r != cudaSuccess) return r;
     r = cudaFuncSetAttribute(oz_residue_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResBSmem);
     if (r != cudaSuccess) return r;
-    r = cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
-    if (r != cudaSuccess) return r;
+    for (auto [k, st] : {std::pair{oz_gemm2_kernel<4>, 4}, std::pair{oz_gemm2_kernel<5>, 5},
+                         std::pair{oz_gemm2_kernel<6>, 6}})
+      if ((r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2_smem(st))) !=
+          cudaSuccess)
+        return r;
     return cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
   });
   if (e != cudaSuccess) return e;
@@ -959,27 +962,38 @@ uint64_t batch_slots(uint64_t p, uint64_t per_slot, uint64_t budget) {
 }
 
 // B' residues (and column exponents) of slots [f0, f0 + fcur) into buffer slots [bslot0, ...)
+// (parts: kPrepExp = column exponents only, kPrepRes = residues only, from
+// exponents already in B.eB; both by default)
+constexpr int kPrepExp = 1, kPrepRes = 2;
 cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint64_t f0, int fcur, int bslot0,
-                   int* flag, cudaStream_t stream) {
+                   int* flag, cudaStream_t stream, int parts = kPrepExp | kPrepRes) {
   using namespace oz;
   const uint64_t Sp = pad_cols(B.s);
   uint8_t* res = B.res + (size_t)bslot0 * 2 * Sp * 4 * B.n;
   int* eB = B.eB + (size_t)bslot0 * Sp;
   const int nz = (int)((2 * B.n + 255) / 256);
+  if (parts & kPrepRes && !(parts & kPrepExp)) goto residues;
+  {
   ColPart* part = nullptr;
   cudaError_t e = cudaMallocAsync(&part, sizeof(ColPart) * nz * fcur * Sp, stream);
   if (e != cudaSuccess) return e;
-  ProfScope ps("k2_int8_residues", stream);
+  ProfScope ps("k2_int8_colnorms", stream);
   oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)nz), 256, 0, stream>>>(
       bh1, bh2, part, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice, B.cbase);
   oz_colexp_finish_kernel<<<(unsigned)((fcur * Sp + 255) / 256), 256, 0, stream>>>(part, eB, nz, fcur, (int)Sp, fcur);
+  ps.stop();
+  count_launches(2);
   e = cudaFreeAsync(part, stream);
   if (e != cudaSuccess) return e;
+  if (!(parts & kPrepRes)) return cudaGetLastError();
+  }
+residues:
+  ProfScope pb("k2_int8_residues_b", stream);
   oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
                         stream>>>(
       bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase);
-  ps.stop();
-  count_launches(3);
+  pb.stop();
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -1057,6 +1071,9 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     f0 = B.s0 + i * F;
     fcur = (int)std::min<uint64_t>(F, B.s0 + ps - f0);
   };
+  if (B.all && !B.ready && env_int("QTB_OZAKI_LAZYB", 1) == 0) {  // (experiment switch) B' first, all slots
+    if ((e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream)) == cudaSuccess) B.ready = true;
+  }
   const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
   auto residues = [&](uint64_t i, cudaStream_t st) {
     uint64_t f0;
@@ -1064,7 +1081,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
     if (lazyB) {
-      const cudaError_t eb = prep_b(B, B.bh1, B.bh2, f0, fcur, (int)(f0 - B.s0), flag, st);
+      const cudaError_t eb = prep_b(B, B.bh1, B.bh2, f0, fcur, (int)(f0 - B.s0), flag, st, kPrepRes);
       if (eb != cudaSuccess && e == cudaSuccess) e = eb;
     }
     if (A) return;
@@ -1091,6 +1108,9 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     pc.stop();
     count_launches(1);
   };
+  // the column exponents of every slot first (a streaming read of B̂ that
+  // would crawl beside the GEMM), the B' residues then batch by batch
+  if (e == cudaSuccess && lazyB) e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream, kPrepExp);
   if (e == cudaSuccess && (!A || lazyB)) residues(0, stream);
   cudaEvent_t res_ready = nullptr, prev_gemm_done = nullptr;
   for (uint64_t i = 0; i < nbatch && e == cudaSuccess; ++i) {
@@ -1112,7 +1132,15 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     if (use_pair()) {
       const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
       const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
-      oz_gemm2_kernel<<<2 * clusters, GEMM_THREADS, GEMM2_SMEM, stream>>>(mapA, mapB, gp);
+      // pipeline depth: fewer stages leave shared memory for the residue / CRT
+      // CTAs of neighbouring batches that run beside the GEMM
+      static const int stages = std::min(6, std::max(4, env_int("QTB_OZAKI_STAGES", 6)));
+      if (stages == 4)
+        oz_gemm2_kernel<4><<<2 * clusters, GEMM_THREADS, gemm2_smem(4), stream>>>(mapA, mapB, gp);
+      else if (stages == 5)
+        oz_gemm2_kernel<5><<<2 * clusters, GEMM_THREADS, gemm2_smem(5), stream>>>(mapA, mapB, gp);
+      else
+        oz_gemm2_kernel<6><<<2 * clusters, GEMM_THREADS, gemm2_smem(6), stream>>>(mapA, mapB, gp);
     } else {
       oz_gemm_kernel<<<dim3((unsigned)((Mp / BM) * (Sp / BNC)), fcur), GEMM_THREADS, GEMM_SMEM, stream>>>(mapA,
                                                                                                          mapB, gp);

@@ -41,6 +41,10 @@ for tag, st, t0, t1 in lines:
     rows.append((float(t0), float(t1), tag, streams[st]))
 rows.sort()
 base = rows[0][0] if rows else 0.0
-print(f"step {e0.elapsed_time(e1):.2f} ms (events around the call); {len(rows)} tagged launches")
+tot = {}
 for t0, t1, tag, si in rows:
+    tot[tag] = tot.get(tag, 0.0) + t1 - t0
+print(f"step {e0.elapsed_time(e1):.2f} ms (events around the call); {len(rows)} tagged launches; "
+      + ", ".join(f"{k} {v:.2f}" for k, v in sorted(tot.items())), flush=True)
+for t0, t1, tag, si in ([] if os.environ.get("QUIET") else rows):
     print(f"  s{si} {t0 - base:8.3f} {t1 - base:8.3f} {t1 - t0:7.3f}  {tag}")
