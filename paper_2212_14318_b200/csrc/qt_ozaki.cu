@@ -625,49 +625,75 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
 
 // B side, pass 1: per (slot f, column c, 256-row block z of Y_k[:, c] =
 // [B1_k[:, c]; B2_k[:, c]]) the local max exponent and the sum of squares
-// scaled by it, into part[z][f][c] (deterministic: no atomics on the sums)
+// scaled by it, into part[z][f][c] (deterministic: no atomics on the sums).
+// One streaming pass: each thread keeps a running exponent E_t and its sum
+// scaled by 2^-2E_t, rescaled (exactly, by a power of two) when a larger
+// exponent appears; the warps' partials are then combined in order.
 struct ColPart {
   int E;      // kNoExp: the block is all zeros
   double ss;  // sum of (|re|^2 + |im|^2) 2^-2E over the block
 };
+// binary exponent E of |v| > 0 finite (|v| < 2^E, |v| >= 2^(E-1)), from the bits
+__device__ __forceinline__ int exp_bits(double v) {
+  const int f = (int)((__double_as_longlong(v) >> 52) & 0x7ff);
+  return f ? f - 1022 : exp_of(v);  // subnormal: frexp
+}
 __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
                                                           const double2* __restrict__ b2, ColPart* __restrict__ part,
                                                           int* nonfinite, int n, int s, int p, int f0, int Sp, int F,
                                                           uint64_t ldb, uint64_t bslice, int cbase) {
-  __shared__ double red[8][33];
+  __shared__ int se[8][33];
+  __shared__ double sss[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
   const int k = slot_slice(f0 + f, p, cbase);
   const int j0 = blockIdx.z * 256, jend = min(2 * n, j0 + 256);
-  auto load = [&](int j) {
-    return (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
-  };
-  double mx = 0.0;
-  if (c < s)
-    for (int j = j0 + w; j < jend; j += 8) {
-      const double2 y = load(j);
-      // a sum of magnitudes is inf/nan iff a component is (or the pair overflows)
-      mx = fmax(mx, (fabs(y.x) + fabs(y.y) <= kDblMax) ? fmax(fabs(y.x), fabs(y.y))
-                                                       : __longlong_as_double(0x7ff0000000000000ll));
-    }
-  red[w][threadIdx.x & 31] = mx;
-  __syncthreads();
-  for (int t = 0; t < 8; ++t) mx = fmax(mx, red[t][threadIdx.x & 31]);
-  __syncthreads();
-  const bool finite = mx <= kDblMax;
-  const int E = (finite && mx != 0.0) ? exp_of(mx) : 0;
+  int E = kNoExp;
   double ss = 0.0;
-  if (c < s && finite && mx != 0.0)
-    for (int j = j0 + w; j < jend; j += 8) {
-      const double2 y = load(j);
-      const double a = scale2(y.x, -E), b = scale2(y.y, -E);
-      ss = fma(a, a, fma(b, b, ss));
+  bool bad = false;
+  if (c < s) {
+    const double2* base1 = b1 + k * bslice + c;
+    const double2* base2 = b2 + k * bslice + c;
+    constexpr int kU = 8;  // loads in flight per thread
+    for (int jb = j0 + w; jb < jend; jb += 8 * kU) {
+      double2 y[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = jb + 8 * u;
+        y[u] = j < jend ? __ldcs(j < n ? base1 + (size_t)j * ldb : base2 + (size_t)(j - n) * ldb)
+                        : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const double ax = fabs(y[u].x), ay = fabs(y[u].y);
+        // a sum of magnitudes is inf/nan iff a component is (or the pair overflows)
+        if (!(ax + ay <= kDblMax)) {
+          bad = true;
+          continue;
+        }
+        const double mx = fmax(ax, ay);
+        if (mx == 0.0) continue;
+        const int e = exp_bits(mx);
+        if (e > E) {
+          if (E != kNoExp) ss = scale2(ss, 2 * (E - e));
+          E = e;
+        }
+        const double a = scale2(y[u].x, -E), b = scale2(y[u].y, -E);
+        ss = fma(a, a, fma(b, b, ss));
+      }
     }
-  red[w][threadIdx.x & 31] = ss;
-  __syncthreads();
+  }
+  se[w][threadIdx.x & 31] = E;
+  sss[w][threadIdx.x & 31] = ss;
+  bad = __syncthreads_or(bad);
   if (w == 0) {
-    for (int t = 1; t < 8; ++t) ss += red[t][threadIdx.x];
-    if (c < s && !finite) atomicExch(nonfinite, 1);
-    part[((size_t)blockIdx.z * F + f) * Sp + c] = ColPart{(c < s && finite && mx != 0.0) ? E : kNoExp, ss};
+    int Eb = kNoExp;
+    for (int t = 0; t < 8; ++t) Eb = max(Eb, se[t][threadIdx.x]);
+    double sb = 0.0;
+    if (Eb != kNoExp)
+      for (int t = 0; t < 8; ++t)
+        if (se[t][threadIdx.x] != kNoExp) sb += scale2(sss[t][threadIdx.x], 2 * (se[t][threadIdx.x] - Eb));
+    if (bad && threadIdx.x == 0) atomicExch(nonfinite, 1);
+    part[((size_t)blockIdx.z * F + f) * Sp + c] = ColPart{(c < s && !bad) ? Eb : kNoExp, sb};
   }
 }
 
@@ -1050,6 +1076,14 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, aslots * Mp, kQ, BM) ||
                            !make_map(&mapB, B.res, Kp, (uint64_t)B.nslots * 2 * Sp, kQ, use_pair() ? BN / 2 : BN)))
     e = cudaErrorInvalidValue;
+  if (e == cudaSuccess && B.all && !B.ready && env_int("QTB_OZAKI_LAZYB", 1) == 0) {  // (experiment switch)
+    if ((e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream)) == cudaSuccess) B.ready = true;
+  }
+  const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
+  // the column exponents of every slot first (a streaming read of B̂ that
+  // would crawl beside the GEMM), the B' residues then batch by batch; before
+  // the fork below, so the aux stream's batches see them
+  if (e == cudaSuccess && lazyB) e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream, kPrepExp);
   cudaStream_t aux = stream;
   std::vector<cudaEvent_t> evs;
   auto mkev = [&]() {
@@ -1071,10 +1105,6 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     f0 = B.s0 + i * F;
     fcur = (int)std::min<uint64_t>(F, B.s0 + ps - f0);
   };
-  if (B.all && !B.ready && env_int("QTB_OZAKI_LAZYB", 1) == 0) {  // (experiment switch) B' first, all slots
-    if ((e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream)) == cudaSuccess) B.ready = true;
-  }
-  const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
   auto residues = [&](uint64_t i, cudaStream_t st) {
     uint64_t f0;
     int fcur;
@@ -1108,9 +1138,6 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     pc.stop();
     count_launches(1);
   };
-  // the column exponents of every slot first (a streaming read of B̂ that
-  // would crawl beside the GEMM), the B' residues then batch by batch
-  if (e == cudaSuccess && lazyB) e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream, kPrepExp);
   if (e == cudaSuccess && (!A || lazyB)) residues(0, stream);
   cudaEvent_t res_ready = nullptr, prev_gemm_done = nullptr;
   for (uint64_t i = 0; i < nbatch && e == cudaSuccess; ++i) {
