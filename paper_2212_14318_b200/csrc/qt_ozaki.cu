@@ -717,17 +717,18 @@ __global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* _
   eB[f * Sp + c] = e;
 }
 
-// B side, pass 2: one CTA per (slot f, 32 columns, 32-row block of Y); writes
+// B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
 // the Re-row [Re Y | -Im Y] and the Im-row [Im Y | Re Y] of each column.  Row
 // order inside a slot: tile t = c / 128 holds its 128 Re-rows, then its 128
-// Im-rows.  Columns c >= s (padding) get zero rows.  The 32 x 32 block is
+// Im-rows.  Columns c >= s (padding) get zero rows.  The 128 x 32 block is
 // transposed through shared memory (column-major, row j at j + j/8 so both the
 // column-wise fill and the 4-consecutive-rows-per-lane reads are conflict
-// free); 8 lanes then write one 32-byte sector of a B' row per store.  19 KB
-// of shared memory, so a CTA fits beside the GEMM's 193 KB on every SM and
-// the B' residues of the next frequency batch run under the current GEMM.
-constexpr int kBRows = 32;
-constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 37 double2 per column
+// free); each warp then writes 128 contiguous bytes of a B' row per store.
+// (Kernels with shared memory are not placed beside the GEMM, whose SMs run
+// the maximum carveout, so this kernel runs between GEMM batches: the larger
+// tile is the faster one there.)
+constexpr int kBRows = 128;
+constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 145 double2 per column
 constexpr size_t kResBSmem = sizeof(double2) * 32 * kBStride;
 __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2,
@@ -747,10 +748,9 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   }
   __syncthreads();
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
-  const int jl = 4 * (tx & 7), jb = j0 + jl;  // this lane's 4 consecutive rows
+  const int jl = 4 * tx, jb = j0 + jl;  // this lane's 4 consecutive rows
   if (jb >= 2 * n) return;
-  {
-    const int cc = ty * 4 + (tx >> 3);
+  for (int cc = ty; cc < 32; cc += 8) {
     const int c = c0 + cc;
     const int e = eB[f * Sp + c];
     const int tcol = c / BNC, ic = c % BNC;
@@ -1110,17 +1110,18 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     int fcur;
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
+    if (!A) {
+      ProfScope pr("k2_int8_residues", st);
+      oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp,
+                                                                   eA + b * F * Mp, flag, (int)m, (int)n, (int)p,
+                                                                   (int)f0, (int)Mp, (int)aslots, B.cbase);
+      pr.stop();
+      count_launches(1);
+    }
     if (lazyB) {
       const cudaError_t eb = prep_b(B, B.bh1, B.bh2, f0, fcur, (int)(f0 - B.s0), flag, st, kPrepRes);
       if (eb != cudaSuccess && e == cudaSuccess) e = eb;
     }
-    if (A) return;
-    ProfScope pr("k2_int8_residues", st);
-    oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp, eA + b * F * Mp,
-                                                                 flag, (int)m, (int)n, (int)p, (int)f0, (int)Mp,
-                                                                 (int)aslots, B.cbase);
-    pr.stop();
-    count_launches(1);
   };
   auto crt = [&](uint64_t i, cudaStream_t st) {
     uint64_t f0;
