@@ -56,6 +56,7 @@ struct ModTable {
   uint32_t p[kQ];
   uint32_t magic[kQ];  // floor(2^32 / p): quotient estimate off by at most one
   uint32_t magic37[kQ];  // ceil(2^37 / p): exact quotient umulhi(v, .) >> 5 for v < 2^28
+  uint32_t negp[kQ];     // -p mod 2^32 (r = v + q (-p): one IMAD, no negation)
   uint32_t c1[kQ];     // 2^18 mod p
   uint32_t c2[kQ];     // 2^36 mod p
   uint32_t bias[kQ];   // multiple of p >= 2^25 (keeps the limb combination non-negative)
@@ -480,7 +481,7 @@ __device__ __forceinline__ uint32_t res_of(const Limbs& l, int q) {
   // v < 2^27 (c2 a2 + bias in [0, 2^26 + 256), c1 a1 < 2^26 - 2^19, a0 < 2^18): the
   // Granlund-Montgomery quotient with a 37-bit reciprocal is exact (error < 2^-9 < 1/p)
   const uint32_t v = (uint32_t)((int)c_mod.c2[q] * l.a2 + (int)c_mod.bias[q]) + c_mod.c1[q] * l.a1 + l.a0;
-  return v - (__umulhi(v, c_mod.magic37[q]) >> 5) * c_mod.p[q];
+  return v + (__umulhi(v, c_mod.magic37[q]) >> 5) * c_mod.negp[q];
 }
 // four bytes (each < 256) into one little-endian word (3 PRMT)
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -891,6 +892,7 @@ ModTable make_table() {
     t.p[q] = p;
     t.magic[q] = (uint32_t)((((uint64_t)1) << 32) / p);
     t.magic37[q] = (uint32_t)(((((uint64_t)1) << 37) + p - 1) / p);
+    t.negp[q] = 0u - (uint32_t)p;
     t.c1[q] = (uint32_t)((((uint64_t)1) << 18) % p);
     t.c2[q] = (uint32_t)((((uint64_t)1) << 36) % p);
     t.bias[q] = (uint32_t)(((((uint64_t)1) << 25) + p - 1) / p * p);
@@ -1080,6 +1082,9 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     if ((e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream)) == cudaSuccess) B.ready = true;
   }
   const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
+  // (experiment switch) the CRT of batch i on the main stream right after its
+  // GEMM instead of on the aux stream beside GEMM i+1: measured equal on config 5
+  const bool crt_main = env_int("QTB_OZAKI_CRT_MAIN", 0) != 0;
   // the column exponents of every slot first (a streaming read of B̂ that
   // would crawl beside the GEMM), the B' residues then batch by batch; before
   // the fork below, so the aux stream's batches see them
@@ -1186,8 +1191,12 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
       }
       res_ready = mkev();
       cudaEventRecord(res_ready, aux);
-      cudaStreamWaitEvent(aux, gemm_done, 0);
-      crt(i, aux);
+      if (crt_main) {
+        crt(i, stream);
+      } else {
+        cudaStreamWaitEvent(aux, gemm_done, 0);
+        crt(i, aux);
+      }
       prev_gemm_done = gemm_done;
     } else {
       crt(i, stream);
