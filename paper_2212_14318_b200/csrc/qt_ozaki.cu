@@ -57,9 +57,9 @@ struct ModTable {
   uint32_t magic[kQ];  // floor(2^32 / p): quotient estimate off by at most one
   uint32_t magic37[kQ];  // ceil(2^37 / p): exact quotient umulhi(v, .) >> 5 for v < 2^28
   uint32_t negp[kQ];     // -p mod 2^32 (r = v + q (-p): one IMAD, no negation)
-  uint32_t c1[kQ];     // 2^18 mod p
-  uint32_t c2[kQ];     // 2^36 mod p
-  uint32_t bias[kQ];   // multiple of p >= 2^25 (keeps the limb combination non-negative)
+  uint32_t wlo[kQ];    // bytes 256^b mod p, b = 0..3 (dp4a weights of the low word)
+  uint32_t whi[kQ];    // bytes 256^b mod p, b = 4..6 (and 0 for b = 7)
+  uint32_t cofs[kQ];   // p - (2^55 mod p): removes the 2^55 offset, keeps the sum non-negative
   uint32_t w[kQ][3];   // round(2^96 * y_q / p_q) mod 2^96, y_q = (M/p_q)^-1 mod p_q (CRT weights)
   double M;            // prod p_q (rounded)
   int ebound;          // T = floor((log2 M - 1) / 2) - margin: ||x'||, ||y'|| < 2^T keeps |x'.y'| < M/2
@@ -465,22 +465,23 @@ __device__ __forceinline__ double scale2(double x, int e) {
   return ldexp(x, e);
 }
 
-// An integer-valued double |x| <= 2^53 as 18-bit limbs: x = a2 2^36 + a1 2^18 + a0
+// An integer-valued double |x| <= 2^53, offset by 2^55 to a non-negative
+// integer < 2^56: its seven bytes, as the low and high 32-bit words
 struct Limbs {
-  uint32_t a0, a1;
-  int a2;
+  uint32_t lo, hi;
 };
 __device__ __forceinline__ Limbs to_limbs(double x, int e) {
-  const long long v = __double2ll_rn(scale2(x, e));
-  return Limbs{(uint32_t)(v & 0x3FFFF), (uint32_t)((v >> 18) & 0x3FFFF), (int)(v >> 36)};
+  const long long v = __double2ll_rn(scale2(x, e)) + (1ll << 55);
+  return Limbs{(uint32_t)v, (uint32_t)(v >> 32)};
 }
 // x mod p_q in [0, p_q); q is a compile-time index after unrolling, so the
-// table entries are constant-bank operands
+// table entries are constant-bank operands.  x + 2^55 = sum_b byte_b 256^b, so
+// x = sum_b byte_b (256^b mod p) - 2^55 (mod p): two byte dot products (dp4a)
+// plus the offset correction give s < 7 * 255^2 + 256 < 2^19, reduced exactly
+// by the 37-bit reciprocal (valid below 2^28).
 __device__ __forceinline__ uint32_t res_of(const Limbs& l, int q) {
-  if (q == 0) return l.a0 & 0xffu;  // p_0 = 256: the low byte (two's complement)
-  // v < 2^27 (c2 a2 + bias in [0, 2^26 + 256), c1 a1 < 2^26 - 2^19, a0 < 2^18): the
-  // Granlund-Montgomery quotient with a 37-bit reciprocal is exact (error < 2^-9 < 1/p)
-  const uint32_t v = (uint32_t)((int)c_mod.c2[q] * l.a2 + (int)c_mod.bias[q]) + c_mod.c1[q] * l.a1 + l.a0;
+  if (q == 0) return l.lo & 0xffu;  // p_0 = 256 divides 2^55: the low byte
+  const uint32_t v = __dp4a(l.lo, c_mod.wlo[q], __dp4a(l.hi, c_mod.whi[q], c_mod.cofs[q]));
   return v + (__umulhi(v, c_mod.magic37[q]) >> 5) * c_mod.negp[q];
 }
 // four bytes (each < 256) into one little-endian word (3 PRMT)
@@ -893,9 +894,18 @@ ModTable make_table() {
     t.magic[q] = (uint32_t)((((uint64_t)1) << 32) / p);
     t.magic37[q] = (uint32_t)(((((uint64_t)1) << 37) + p - 1) / p);
     t.negp[q] = 0u - (uint32_t)p;
-    t.c1[q] = (uint32_t)((((uint64_t)1) << 18) % p);
-    t.c2[q] = (uint32_t)((((uint64_t)1) << 36) % p);
-    t.bias[q] = (uint32_t)(((((uint64_t)1) << 25) + p - 1) / p * p);
+    uint32_t wlo = 0, whi = 0;
+    uint64_t pw = 1;  // 256^b mod p
+    for (int b = 0; b < 7; ++b) {
+      if (b < 4)
+        wlo |= (uint32_t)pw << (8 * b);
+      else
+        whi |= (uint32_t)pw << (8 * (b - 4));
+      pw = pw * 256 % p;
+    }
+    t.wlo[q] = wlo;
+    t.whi[q] = whi;
+    t.cofs[q] = p - (uint32_t)((((uint64_t)1) << 55) % p);
     uint64_t mp = 1;  // (M / p) mod p
     for (int j = 0; j < kQ; ++j)
       if (j != q) mp = mp * (uint64_t)kModuli[j] % p;
