@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   const double2* Qr = a2 + ((size_t)skq * m + i) * n;
   double mx = 0.0;
   bool bad = false;
+#pragma unroll 4
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const double2 x = P[j], y = Qr[j];
     mx = fmax(mx, fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y))));
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   if (mx != 0.0) {
     const int E = exp_of(mx);
     double ss = 0.0;  // sum of squares of the row scaled by 2^-E (each term <= 1)
+#pragma unroll 4
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const double2 x = P[j], y = Qr[j];
       const double a = scale2(x.x, -E), b = scale2(x.y, -E), c = scale2(y.x, -E), d = scale2(y.y, -E);
@@ -741,6 +743,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   const int c0 = blockIdx.x * 32, j0 = blockIdx.z * kBRows, f = blockIdx.y;
   const int k = slot_slice(f0 + f, p, cbase);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
   for (int jj = ty; jj < kBRows; jj += 8) {
     const int j = j0 + jj, c = c0 + tx;
     double2 y = make_double2(0.0, 0.0);
