@@ -77,6 +77,10 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
+    ap.add_argument("--exchange", choices=["auto", "fused", "p2p"], default="auto",
+                    help="frequency-parallel exchange: fused = Â/B̂ stored by K1 and Ĉ loaded by K3 straight "
+                         "from the peers' stage buffers (symmetric memory over NVLink, two device barriers per "
+                         "step); p2p = NCCL send/recv groups; auto = fused when available")
     ap.add_argument("--multi", choices=["auto", "freq", "grid"], default="auto",
                     help="N > 1 decomposition: freq = frequency-parallel (int8 stage 2), grid = 2-D blocks of C; "
                          "auto = freq when the product takes the int8 stage 2")
@@ -268,6 +272,10 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    elif args.sharded and args.exchange == "fused":  # the fused exchange on a one-rank group (exercise it on 1 GPU)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
     L = qt._native.lib()
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -311,18 +319,35 @@ def run_ours(args, cfg):
             # frequency-parallel: K1 of this rank's rows of A and B, Â/B̂ pieces
             # point to point to the owners of their frequency slots, int8 stage 2
             # of this rank's slots, Ĉ pieces back, K3 of this rank's rows of C
-            sharded = FreqParallelTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+            peer = None
+            if args.exchange != "p2p" and dist.is_initialized() and FreqParallelTProduct.routable(cfg.p):
+                try:
+                    from paper_2212_14318_b200.distributed import make_peer_stage
+                    peer = make_peer_stage(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev, dist)
+                except Exception as exc:  # no symmetric memory here: NCCL point-to-point instead
+                    if args.exchange == "fused":
+                        raise
+                    print(f"[bench] fused exchange unavailable ({type(exc).__name__}: {exc}); using p2p",
+                          file=sys.stderr)
+            exchange_kind = "fused" if peer is not None else "p2p"
+            sharded = FreqParallelTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev,
+                                           stage_buffer=peer[0] if peer else None)
             sharded.load_a(a.t1, a.t2)
             sharded.load_b(b.t1, b.t2)
             pin(sharded.a)
             pin(sharded.b)
             exchange = make_exchange(rank, dist if world > 1 else None)
             rows, cols = sharded.rows, cfg.s
+            if peer is not None:
+                sharded.set_peers(peer[1])
             if world > 1:
                 dist.barrier()  # communicator up on every rank before the first point-to-point group
 
             def step():
-                sharded.step(exchange)
+                if peer is not None:
+                    sharded.step_routed(peer[2])
+                else:
+                    sharded.step(exchange)
         else:
             # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
             # block arrive as pieces broadcast (NCCL) from their owners inside the
@@ -681,7 +706,9 @@ def run_ours(args, cfg):
             "fp64_dmma_path": dmma_path,
             "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
                        "parallelism": ((f"freq{world}(frequency slots; rows of A, B, C for the tube FFTs)"
-                                        "+point-to-point exchange" if mode == "freq" else
+                                        + ("+exchange fused into K1 stores / K3 loads (symmetric memory)"
+                                           if exchange_kind == "fused" else "+NCCL point-to-point exchange")
+                                        if mode == "freq" else
                                         f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts")
                                        if sharded_mode else f"rows{world}")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
@@ -695,7 +722,7 @@ def run_ours(args, cfg):
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     return 0

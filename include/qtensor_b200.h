@@ -105,6 +105,25 @@ int qt_qifft3_conj_f64_device(const double* x1, const double* x2,
                               double* y1, double* y2,
                               uint64_t m, uint64_t n, uint64_t p, void* stream);
 
+/* Routed forms of the two transforms for the frequency-parallel multi-GPU
+ * driver: the exchange that follows K1 (or precedes K3) is fused into the
+ * transform's own stores (loads).  rows1/rows2 are DEVICE arrays of p device
+ * pointers, one per slice/frequency, each addressing m*n interleaved complex
+ * doubles and possibly living in a peer GPU's memory (NVLink P2P):
+ *   qfft3 routed:  frequency k of plane X is written to y{X}_rows[k][0..m*n)
+ *   qifft3 routed: frequency k of plane X is read from x{X}_rows[k][0..m*n)
+ * Same arithmetic as the plain forms (bitwise equal results).  Only lengths p
+ * whose transform is one pass support routing (qt_fft_routable(p) == 1; all
+ * p <= 512 and the smooth lengths below 1024); otherwise QT_EINVAL.
+ * Replaces no reference entry point: the reference is single-process. */
+int qt_fft_routable(uint64_t p);
+int qt_qfft3_conj_f64_device_routed(const double* x1, const double* x2,
+                                    double* const* y1_rows, double* const* y2_rows,
+                                    uint64_t m, uint64_t n, uint64_t p, void* stream);
+int qt_qifft3_conj_f64_device_routed(const double* const* x1_rows, const double* const* x2_rows,
+                                     double* y1, double* y2,
+                                     uint64_t m, uint64_t n, uint64_t p, void* stream);
+
 /* Stage 2 alone (the paired-frequency quaternion block GEMM, tproduct.cpp:90-104)
  * on already transformed operands: chat = ahat (.) bhat per frequency pair
  * (k, p-k).  Exposed for profiling and for callers that keep operands in the

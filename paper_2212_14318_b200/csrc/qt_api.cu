@@ -359,6 +359,44 @@ int qt_qifft3_conj_f64_device(const double* x1, const double* x2, double* y1, do
   return transform_device_impl(true, x1, x2, y1, y2, m, n, p, (cudaStream_t)stream);
 }
 
+int qt_fft_routable(uint64_t p) { return p >= 1 && p <= (uint64_t)kIntMax && fft_single_pass((int)p) ? 1 : 0; }
+
+int qt_qfft3_conj_f64_device_routed(const double* x1, const double* x2, double* const* y1_rows,
+                                    double* const* y2_rows, uint64_t m, uint64_t n, uint64_t p, void* stream) {
+  t_err.clear();
+  int rc = check_dims(m, n, 1, p, "qfft3_conj (routed)");
+  if (rc) return rc;
+  if (!qt_fft_routable(p)) return fail(QT_EINVAL, "qfft3_conj (routed): this length is transformed in two passes");
+  if (!y1_rows || !y2_rows) return fail(QT_EINVAL, "qfft3_conj (routed): null row table");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  if (m * n == 0) return QT_OK;
+  TubeBatch b{};
+  add_forward(b, x1, x2, nullptr, nullptr, m * n);
+  b.job[0].out_rows = reinterpret_cast<double2* const*>(y1_rows);
+  b.job[1].out_rows = reinterpret_cast<double2* const*>(y2_rows);
+  cudaError_t e = launch_tube_fft(b, (int)p, (cudaStream_t)stream, dev);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "qfft3_conj (routed)");
+}
+
+int qt_qifft3_conj_f64_device_routed(const double* const* x1_rows, const double* const* x2_rows, double* y1,
+                                     double* y2, uint64_t m, uint64_t n, uint64_t p, void* stream) {
+  t_err.clear();
+  int rc = check_dims(m, n, 1, p, "qifft3_conj (routed)");
+  if (rc) return rc;
+  if (!qt_fft_routable(p)) return fail(QT_EINVAL, "qifft3_conj (routed): this length is transformed in two passes");
+  if (!x1_rows || !x2_rows) return fail(QT_EINVAL, "qifft3_conj (routed): null row table");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  if (m * n == 0) return QT_OK;
+  TubeBatch b{};
+  add_inverse(b, nullptr, nullptr, y1, y2, m * n, p);
+  b.job[0].in_rows = reinterpret_cast<const double2* const*>(x1_rows);
+  b.job[1].in_rows = reinterpret_cast<const double2* const*>(x2_rows);
+  cudaError_t e = launch_tube_fft(b, (int)p, (cudaStream_t)stream, dev);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "qifft3_conj (routed)");
+}
+
 int qt_spectral_product_f64_device(const double* ah1, const double* ah2, const double* bh1, const double* bh2,
                                    double* ch1, double* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                    void* stream) {

@@ -143,6 +143,19 @@ struct FftGeom {
   int L, ig, is, og, os, post_tw, tws;
 };
 
+// Row base pointers (tube t0 of row r), plain or routed through the job's row
+// tables.  Routed launches use only the single-pass geometry (rows = slices).
+template <bool ROUTED>
+__device__ __forceinline__ const double2* in_row(const TubeJob& job, int row, uint64_t t0) {
+  if (ROUTED && job.in_rows) return job.in_rows[row] + t0;
+  return job.in + (uint64_t)row * job.ntubes + t0;
+}
+template <bool ROUTED>
+__device__ __forceinline__ double2* out_row(const TubeJob& job, int row, uint64_t t0) {
+  if (ROUTED && job.out_rows) return job.out_rows[row] + t0;
+  return job.out + (uint64_t)row * job.ntubes + t0;
+}
+
 // One Stockham stage of radix R over an L x T smem tile (tube index fastest).
 // src/dst element (r, t) at [r*T + t].  Ns = product of earlier radices.
 template <int R>
@@ -208,21 +221,21 @@ __device__ __forceinline__ void stage_smem(const double2* src, double2* dst, con
 }
 
 // output store with the four-step twiddle, conj-out and scale fused
-__device__ __forceinline__ void store_out(double2* __restrict__ out, const TubeJob& job, const FftGeom& G,
+template <bool ROUTED>
+__device__ __forceinline__ void store_out(const TubeJob& job, uint64_t t0, const FftGeom& G,
                                           const double2* __restrict__ tw, int g, int kk, int t, double2 v) {
   if (G.post_tw && g != 0) v = cmul(v, __ldg(&tw[g * kk]));
   const double sc = job.scale;
   const double sci = job.conj_out ? -sc : sc;
-  out[(uint64_t)(g * G.og + kk * G.os) * job.ntubes + t] = make_double2(v.x * sc, v.y * sci);
+  out_row<ROUTED>(job, g * G.og + kk * G.os, t0)[t] = make_double2(v.x * sc, v.y * sci);
 }
 
 // stage 0: HBM -> registers -> smem (Ns = 1, so no twiddles)
-template <int R>
+template <int R, bool ROUTED>
 __device__ __forceinline__ void stage_first_global(const TubeJob& job, const FftGeom& G, int g, uint64_t t0,
                                                    int tcount, double2* __restrict__ dst, int logT) {
   const int T = 1 << logT;
   const int pR = G.L / R;
-  const double2* __restrict__ in = job.in + t0;
   for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
     const int j = b >> logT, t = b & (T - 1);
     double2 v[R];
@@ -230,7 +243,7 @@ __device__ __forceinline__ void stage_first_global(const TubeJob& job, const Fft
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int row = g * G.ig + (j + r * pR) * G.is;
-      v[r] = ok ? __ldcs(&in[(uint64_t)row * job.ntubes + t]) : make_double2(0.0, 0.0);
+      v[r] = ok ? __ldcs(&in_row<ROUTED>(job, row, t0)[t]) : make_double2(0.0, 0.0);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
@@ -240,14 +253,13 @@ __device__ __forceinline__ void stage_first_global(const TubeJob& job, const Fft
 }
 
 // last stage: smem -> registers -> HBM with the output ops fused
-template <int R>
+template <int R, bool ROUTED>
 __device__ __forceinline__ void stage_last_global(const double2* __restrict__ src, const TubeJob& job,
                                                   const FftGeom& G, int g, uint64_t t0, int tcount,
                                                   const double2* __restrict__ tw, int logT, int Ns) {
   const int T = 1 << logT;
   const int pR = G.L / R;
   const int twmul = (G.L / (Ns * R)) * G.tws;
-  double2* __restrict__ out = job.out + t0;
   for (int b = threadIdx.x; b < (pR << logT); b += blockDim.x) {
     const int j = b >> logT, t = b & (T - 1);
     const int jm = j % Ns;
@@ -263,33 +275,32 @@ __device__ __forceinline__ void stage_last_global(const double2* __restrict__ sr
     if (t < tcount) {
       const int idxD = (j - jm) * R + jm;
 #pragma unroll
-      for (int k = 0; k < R; ++k) store_out(out, job, G, tw, g, idxD + k * Ns, t, v[k]);
+      for (int k = 0; k < R; ++k) store_out<ROUTED>(job, t0, G, tw, g, idxD + k * Ns, t, v[k]);
     }
   }
 }
 
 // single-stage transform (L in {2, 4, 8}): HBM -> registers -> HBM
-template <int R>
+template <int R, bool ROUTED>
 __device__ __forceinline__ void stage_only_global(const TubeJob& job, const FftGeom& G, int g, uint64_t t0,
                                                   int tcount, const double2* __restrict__ tw, int logT) {
   const int T = 1 << logT;
-  const double2* __restrict__ in = job.in + t0;
-  double2* __restrict__ out = job.out + t0;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     if (t >= tcount) continue;
     double2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      v[r] = __ldcs(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
+      v[r] = __ldcs(&in_row<ROUTED>(job, g * G.ig + r * G.is, t0)[t]);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R>(v);
 #pragma unroll
-    for (int k = 0; k < R; ++k) store_out(out, job, G, tw, g, k, t, v[k]);
+    for (int k = 0; k < R; ++k) store_out<ROUTED>(job, t0, G, tw, g, k, t, v[k]);
   }
 }
 
 // K1 / K3 kernel: grid = (tube tiles, jobs, groups), T = 1 << logT tubes per CTA.
+template <bool ROUTED>
 __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan plan, FftGeom G,
                                                        const double2* __restrict__ tw, int logT) {
   extern __shared__ double2 sm[];
@@ -303,20 +314,19 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   const int tcount = (int)min((uint64_t)T, job.ntubes - t0);
 
   if (S == 0) {  // L == 1: the transform is the identity, ops only
-    const double2* __restrict__ in = job.in + t0;
-    double2* __restrict__ out = job.out + t0;
+    const double2* __restrict__ in = in_row<ROUTED>(job, g * G.ig, t0);
     for (int t = threadIdx.x; t < tcount; t += blockDim.x) {
-      double2 v = __ldcs(&in[(uint64_t)(g * G.ig) * job.ntubes + t]);
+      double2 v = __ldcs(&in[t]);
       if (job.conj_in) v.y = -v.y;
-      store_out(out, job, G, tw, g, 0, t, v);
+      store_out<ROUTED>(job, t0, G, tw, g, 0, t, v);
     }
     return;
   }
   const int R0 = plan.radix[0];
   if (S == 1 && is_reg_radix(R0)) {
-    if (R0 == 8) stage_only_global<8>(job, G, g, t0, tcount, tw, logT);
-    else if (R0 == 4) stage_only_global<4>(job, G, g, t0, tcount, tw, logT);
-    else stage_only_global<2>(job, G, g, t0, tcount, tw, logT);
+    if (R0 == 8) stage_only_global<8, ROUTED>(job, G, g, t0, tcount, tw, logT);
+    else if (R0 == 4) stage_only_global<4, ROUTED>(job, G, g, t0, tcount, tw, logT);
+    else stage_only_global<2, ROUTED>(job, G, g, t0, tcount, tw, logT);
     return;
   }
 
@@ -324,17 +334,16 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   double2* obuf = sm + ((size_t)L << logT);  // other ping-pong buffer
   int s = 0, Ns = 1;
   if (is_reg_radix(R0)) {
-    if (R0 == 8) stage_first_global<8>(job, G, g, t0, tcount, cbuf, logT);
-    else if (R0 == 4) stage_first_global<4>(job, G, g, t0, tcount, cbuf, logT);
-    else stage_first_global<2>(job, G, g, t0, tcount, cbuf, logT);
+    if (R0 == 8) stage_first_global<8, ROUTED>(job, G, g, t0, tcount, cbuf, logT);
+    else if (R0 == 4) stage_first_global<4, ROUTED>(job, G, g, t0, tcount, cbuf, logT);
+    else stage_first_global<2, ROUTED>(job, G, g, t0, tcount, cbuf, logT);
     s = 1;
     Ns = R0;
   } else {  // explicit coalesced tile load, conj fused
-    const double2* __restrict__ in = job.in + t0;
     for (int idx = threadIdx.x; idx < (L << logT); idx += blockDim.x) {
       const int r = idx >> logT, t = idx & (T - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (t < tcount) v = __ldcs(&in[(uint64_t)(g * G.ig + r * G.is) * job.ntubes + t]);
+      if (t < tcount) v = __ldcs(&in_row<ROUTED>(job, g * G.ig + r * G.is, t0)[t]);
       if (job.conj_in) v.y = -v.y;
       cbuf[idx] = v;
     }
@@ -351,14 +360,13 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
   }
   if (last_reg) {
     const int R = plan.radix[S - 1];
-    if (R == 8) stage_last_global<8>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
-    else if (R == 4) stage_last_global<4>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
-    else stage_last_global<2>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
+    if (R == 8) stage_last_global<8, ROUTED>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
+    else if (R == 4) stage_last_global<4, ROUTED>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
+    else stage_last_global<2, ROUTED>(cbuf, job, G, g, t0, tcount, tw, logT, Ns);
   } else {  // generic last stage already ran into cbuf: explicit store
-    double2* __restrict__ out = job.out + t0;
     for (int idx = threadIdx.x; idx < (L << logT); idx += blockDim.x) {
       const int r = idx >> logT, t = idx & (T - 1);
-      if (t < tcount) store_out(out, job, G, tw, g, r, t, cbuf[idx]);
+      if (t < tcount) store_out<ROUTED>(job, t0, G, tw, g, r, t, cbuf[idx]);
     }
   }
 }
@@ -369,7 +377,7 @@ __global__ void __launch_bounds__(256) tube_fft_kernel(TubeBatch batch, FftPlan 
 // so the index math has no divisions and the kernel needs few registers
 // (higher occupancy for the small, latency-bound launches).  Arithmetic per
 // tube is the same Stockham formula as tube_fft_kernel.
-template <int R0, int R1>
+template <int R0, int R1, bool ROUTED>
 __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom G, const double2* __restrict__ tw,
                                                         int logT) {
   constexpr int L = R0 * R1;
@@ -391,7 +399,8 @@ __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom
     const bool ok = t < tcount;
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
-      v[r] = ok ? __ldcs(&in[(uint64_t)(j + r * P0) * istr + t]) : make_double2(0.0, 0.0);
+      v[r] = ok ? __ldcs(ROUTED && job.in_rows ? &job.in_rows[j + r * P0][t0 + t] : &in[(uint64_t)(j + r * P0) * istr + t])
+                : make_double2(0.0, 0.0);
       if (job.conj_in) v[r].y = -v[r].y;
     }
     dft_reg<R0>(v);
@@ -423,8 +432,9 @@ __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom
         double2 y = v[k];
         if (G.post_tw && g != 0) y = cmul(y, __ldg(&tw[g * kk]));
         const double2 o = make_double2(y.x * sc, y.y * sci);
-        if (job.stream_out) __stcs(&out[(uint64_t)kk * ostr + t], o);
-        else out[(uint64_t)kk * ostr + t] = o;
+        double2* dst = ROUTED && job.out_rows ? &job.out_rows[kk][t0 + t] : &out[(uint64_t)kk * ostr + t];
+        if (job.stream_out) __stcs(dst, o);
+        else *dst = o;
       }
     }
   }
@@ -469,6 +479,12 @@ constexpr int kFftThreads = 256;
 constexpr size_t kSmemBudget = 96 * 1024;  // two CTAs per SM
 constexpr size_t kSmemMax = 224 * 1024;    // one CTA per SM
 
+bool batch_routed(const TubeBatch& b) {
+  for (int i = 0; i < b.njobs; ++i)
+    if (b.job[i].in_rows || b.job[i].out_rows) return true;
+  return false;
+}
+
 // shared-memory buffers the kernel needs for a plan (host mirror of the
 // control flow above)
 int fft_smem_buffers(const FftPlan& pl) {
@@ -486,7 +502,10 @@ cudaError_t ensure_smem_attr(int device) {
   static bool attr_set[64] = {};
   std::lock_guard<std::mutex> lk(mu);
   if (device >= 0 && device < 64 && !attr_set[device]) {
-    cudaError_t e = cudaFuncSetAttribute(tube_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaError_t e =
+        cudaFuncSetAttribute(tube_fft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tube_fft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
     if (e != cudaSuccess) return e;
     attr_set[device] = true;
   }
@@ -520,13 +539,19 @@ cudaError_t launch_fft2(const TubeBatch& batch, const FftGeom& G, const double2*
   static std::mutex mu;
   static uint64_t done = 0;
   cudaError_t attr = once_per_device(mu, done, [] {
-    return cudaFuncSetAttribute(tube_fft2_kernel<R0, R1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    cudaError_t r =
+        cudaFuncSetAttribute(tube_fft2_kernel<R0, R1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(tube_fft2_kernel<R0, R1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kSmemMax);
+    return r;
   });
   if (attr != cudaSuccess) return attr;
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
   dim3 grid((unsigned)tiles, njobs, groups);
   ProfScope ps("fft", stream);
-  tube_fft2_kernel<R0, R1><<<grid, kFftThreads, smem, stream>>>(batch, G, tw, logT);
+  if (batch_routed(batch)) tube_fft2_kernel<R0, R1, true><<<grid, kFftThreads, smem, stream>>>(batch, G, tw, logT);
+  else tube_fft2_kernel<R0, R1, false><<<grid, kFftThreads, smem, stream>>>(batch, G, tw, logT);
   ps.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -544,7 +569,8 @@ cudaError_t launch_pass(const TubeBatch& batch, const FftPlan& pl, const FftGeom
   const uint64_t tiles = (maxtubes + (uint64_t(1) << logT) - 1) >> logT;
   dim3 grid((unsigned)tiles, batch.njobs, groups);
   ProfScope ps("fft", stream);
-  tube_fft_kernel<<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
+  if (batch_routed(batch)) tube_fft_kernel<true><<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
+  else tube_fft_kernel<false><<<grid, kFftThreads, smem, stream>>>(batch, pl, G, tw, logT);
   ps.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -566,6 +592,17 @@ void split_length(int p, int* p1, int* p2) {
   *p2 = (int)std::min(a, b);
 }
 }  // namespace
+
+bool fft_single_pass(int p) {
+  if (p <= 0) return false;
+  const FftPlan plan = make_fft_plan(p);
+  const size_t per_tube = (size_t)fft_smem_buffers(plan) * sizeof(double2) * (size_t)p;
+  if (per_tube > kSmemMax) return false;
+  const bool narrow = (per_tube << 3) > kSmemMax;
+  int p1 = 0, p2 = 0;
+  if (narrow) split_length(p, &p1, &p2);
+  return !(narrow && p1 > 1 && p2 > 1 && p1 <= 2048);
+}
 
 cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device) {
   if (batch.njobs == 0) return cudaSuccess;
@@ -593,6 +630,8 @@ cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, 
     const FftGeom G{p, 0, 1, 0, 1, 0, 1};
     return launch_pass(batch, plan, G, tw, maxtubes, 1, logT, smem, stream);
   }
+  // routed rows exist for the single-pass transform only
+  if (batch_routed(batch)) return cudaErrorNotSupported;
 
   // 2) four-step split p = p1 * p2 through a scratch plane per job
   if (split_ok) {

@@ -33,6 +33,13 @@ struct TubeJob {
   int conj_out;
   double scale;
   int stream_out = 0;  // 1: evict-first stores (final pass of the split FFT: keep its L2 scratch resident)
+  // Routed rows (single-pass transforms only): input row r (slice r, ntubes
+  // complex) is read from in_rows[r] instead of in + r*ntubes, output row k
+  // is written to out_rows[k] — device pointer tables, possibly pointing into
+  // peer GPUs' memory, so a transform can scatter its frequency rows straight
+  // to the ranks that own them (or gather them) over NVLink.
+  const double2* const* in_rows = nullptr;
+  double2* const* out_rows = nullptr;
 };
 
 constexpr int kMaxJobs = 4;
@@ -59,6 +66,8 @@ const double2* twiddles_for(int device, int p, cudaStream_t stream);
 // Enqueue the tube transform of every job in `batch` (all jobs share p).
 // Returns cudaSuccess or the launch error.
 cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device);
+// The length-p transform runs as one pass (so routed rows are supported).
+bool fft_single_pass(int p);
 
 // ------------------------------------------------------ paired spectral GEMM
 // chat[k] for all k from ahat, bhat (slice-major CD planes), tproduct.cpp:90-104.

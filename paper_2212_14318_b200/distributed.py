@@ -285,7 +285,8 @@ class FreqParallelTProduct:
     fp64 DMMA decomposition (Grid2DTProduct) handles those.
     """
 
-    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None):
+    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None,
+                 stage_buffer=None):
         import torch
         self.torch = torch
         self.m, self.n, self.s, self.p = m, n, s, p
@@ -305,12 +306,37 @@ class FreqParallelTProduct:
         self.ah = torch.empty_like(self.a)
         self.b = torch.empty((2, p, br, 2 * s), **f64)
         self.bh = torch.empty_like(self.b)
-        self.ac = torch.empty((2, self.ns, m, 2 * n), **f64)
-        self.bc = torch.empty((2, self.ns, n, 2 * s), **f64)
-        self.cc = torch.empty((2, self.ns, m, 2 * s), **f64)
+        # the compact slot tensors Â/B̂/Ĉ of this rank's slots: carved out of
+        # `stage_buffer` (float64, >= stage_doubles(...) elements — e.g. a
+        # symmetric-memory buffer its peers can address) or allocated here
+        sizes = self.stage_sizes(m, n, s, p, world)[rank]
+        if stage_buffer is None:
+            stage_buffer = torch.empty(sum(sizes), **f64)
+        assert stage_buffer.dtype == torch.float64 and stage_buffer.numel() >= sum(sizes)
+        self.stage_buffer = stage_buffer
+        o1, o2 = sizes[0], sizes[0] + sizes[1]
+        self.ac = stage_buffer[:o1].view(2, self.ns, m, 2 * n)
+        self.bc = stage_buffer[o1:o2].view(2, self.ns, n, 2 * s)
+        self.cc = stage_buffer[o2:o2 + sizes[2]].view(2, self.ns, m, 2 * s)
+        self.tables = None  # routed-exchange row tables (set_peers)
         self.c = torch.empty((2, p, self.rows, 2 * s), **f64)
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.L = _native.lib() if self.dev.type == "cuda" else None
+
+    @staticmethod
+    def stage_sizes(m: int, n: int, s: int, p: int, world: int):
+        """Per rank: float64 elements of its (Â, B̂, Ĉ) compact slot tensors,
+        laid out in that order in its stage buffer."""
+        out = []
+        for t0, t1 in shard.slot_ranges(p, world):
+            ns = t1 - t0
+            out.append((2 * ns * m * 2 * n, 2 * ns * n * 2 * s, 2 * ns * m * 2 * s))
+        return out
+
+    @staticmethod
+    def routable(p: int) -> bool:
+        """The tube transforms of length p can route their rows (one pass)."""
+        return bool(_native.lib().qt_fft_routable(p))
 
     @staticmethod
     def eligible(m: int, n: int, s: int, p: int) -> bool:
@@ -404,6 +430,76 @@ class FreqParallelTProduct:
                                                            self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
                                                            self.s, self.p, self._stream(stream)), "qifft3_conj(C rows)")
 
+    # ------------------------------------------ exchange fused into K1 / K3
+    # With every rank's stage buffer addressable (peer_bases: device address of
+    # rank j's stage buffer as seen from this GPU — NVLink P2P through
+    # symmetric memory, or plain addresses on one device), the exchange needs
+    # no messages: K1 stores frequency k of its rows straight into the slot
+    # owner's Â/B̂ tensors, and K3 loads frequency k of its rows of Ĉ straight
+    # from the owner's — one pointer per frequency and plane
+    # (qt_q{i}fft3_conj_f64_device_routed).  The pieces land exactly where the
+    # point-to-point exchange puts them, so results are bitwise the same.
+    def set_peers(self, peer_bases) -> None:
+        torch = self.torch
+        assert len(peer_bases) == self.world
+        sizes = self.stage_sizes(self.m, self.n, self.s, self.p, self.world)
+        slot_of = [0] * self.p
+        for t, k in enumerate(self.freq):
+            slot_of[k] = t
+        owner = [j for j, (t0, t1) in enumerate(self.ranges) for _ in range(t0, t1)]
+        m, n, s = self.m, self.n, self.s
+
+        def table(part, rows_total, width, r0):
+            # part 0/1/2 = Â/B̂/Ĉ of the owner; element (pl, slot - s0, r0, 0)
+            out = [[0] * self.p for _ in range(2)]
+            for k in range(self.p):
+                t = slot_of[k]
+                j = owner[t]
+                ns_j = self.ranges[j][1] - self.ranges[j][0]
+                base = peer_bases[j] + 8 * sum(sizes[j][:part])
+                for pl in (0, 1):
+                    out[pl][k] = base + 16 * (((pl * ns_j + (t - self.ranges[j][0])) * rows_total + r0) * width)
+            return torch.tensor(out, dtype=torch.int64, device=self.dev)
+
+        self.tables = {"a": table(0, m, n, self.a0), "b": table(1, n, s, self.b0), "c": table(2, m, s, self.a0)}
+
+    def k1_routed(self, stream=None) -> None:
+        """K1 with the Â/B̂ exchange fused into its stores."""
+        sh, L, T = self._stream(stream), self.L, self.tables
+        if self.b1 > self.b0:
+            _native.check(L.qt_qfft3_conj_f64_device_routed(self.b[0].data_ptr(), self.b[1].data_ptr(),
+                                                            T["b"][0].data_ptr(), T["b"][1].data_ptr(),
+                                                            self.b1 - self.b0, self.s, self.p, sh),
+                          "qfft3_conj routed (B rows)")
+        if self.rows:
+            _native.check(L.qt_qfft3_conj_f64_device_routed(self.a[0].data_ptr(), self.a[1].data_ptr(),
+                                                            T["a"][0].data_ptr(), T["a"][1].data_ptr(), self.rows,
+                                                            self.n, self.p, sh), "qfft3_conj routed (A rows)")
+
+    def k3_routed(self, stream=None) -> None:
+        """K3 with the Ĉ exchange fused into its loads."""
+        if self.rows:
+            T = self.tables
+            _native.check(self.L.qt_qifft3_conj_f64_device_routed(T["c"][0].data_ptr(), T["c"][1].data_ptr(),
+                                                                  self.c[0].data_ptr(), self.c[1].data_ptr(),
+                                                                  self.rows, self.s, self.p,
+                                                                  self._stream(stream)), "qifft3_conj routed (C rows)")
+
+    def step_routed(self, barrier, stream=None) -> None:
+        """One step with the exchange fused into K1/K3.  `barrier()` is a
+        stream-ordered barrier over the ranks: after it, every rank's earlier
+        kernels (and so their peer stores) are complete.  Two per step: after
+        K1 (the Â/B̂ pieces are in place) and after stage 2 (every Ĉ is
+        complete, and no rank still reads Â/B̂ the next step's K1 overwrites);
+        the next step's first barrier also orders this step's K3 loads before
+        any rank's next stage 2 rewrites its Ĉ."""
+        self.flag.zero_()
+        self.k1_routed(stream)
+        barrier()
+        self.k2_multiply(self.k2_prepare(stream), stream)
+        barrier()
+        self.k3_routed(stream)
+
     def step(self, exchange=None, stream=None) -> None:
         """One step.  `exchange(sends, recvs)` starts the point-to-point
         transfers and returns a list of Works to wait on (make_exchange);
@@ -458,6 +554,43 @@ def make_exchange(rank: int, dist_mod, group=None):
         return dist_mod.batch_isend_irecv(ops) if ops else []
 
     return ex
+
+
+def make_peer_stage(m: int, n: int, s: int, p: int, rank: int, world: int, device, dist_mod, group=None):
+    """Symmetric-memory stage buffer for FreqParallelTProduct plus the peers'
+    base addresses and a device-side barrier: (buffer, peer_bases, barrier).
+    Raises if symmetric memory is unavailable (callers fall back to the
+    point-to-point exchange)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+    sizes = FreqParallelTProduct.stage_sizes(m, n, s, p, world)
+    numel = max(sum(x) for x in sizes)
+    buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
+    grp = group if group is not None else dist_mod.group.WORLD
+    hdl = symm_mem.rendezvous(buf, grp)
+    bases = [int(x) for x in hdl.buffer_ptrs]
+
+    def barrier():
+        hdl.barrier(channel=0)
+
+    return buf, bases, barrier
+
+
+def emulate_freq_parallel_routed(ranks) -> None:
+    """emulate_freq_parallel with the exchange fused into K1/K3: the G
+    instances share one device, each one's row tables point into the others'
+    stage buffers, and lockstep order stands in for the barriers."""
+    bases = [x.stage_buffer.data_ptr() for x in ranks]
+    for x in ranks:
+        if x.tables is None:
+            x.set_peers(bases)
+    for x in ranks:
+        x.flag.zero_()
+        x.k1_routed()
+    for x in ranks:
+        x.k2_multiply(x.k2_prepare())
+    for x in ranks:
+        x.k3_routed()
 
 
 def emulate_freq_parallel(ranks) -> None:

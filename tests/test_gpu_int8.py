@@ -439,6 +439,30 @@ def test_freq_parallel_emulated_bitwise(world):
         assert bits_equal(c1, want.t1[:, x.a0:x.a1]) and bits_equal(c2, want.t2[:, x.a0:x.a1]), (world, x.rank)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_freq_parallel_routed_emulated_bitwise(world):
+    """The frequency-parallel step with the exchange fused into K1/K3 (routed
+    row tables into the other ranks' stage buffers; emulated on one GPU in
+    lockstep): bitwise equal to tprod_fast, and to the point-to-point form."""
+    import torch
+    from paper_2212_14318_b200.distributed import FreqParallelTProduct, emulate_freq_parallel_routed
+    m, n, s, p = 150, 256, 520, 6
+    assert FreqParallelTProduct.routable(p)
+    a = qt.gen_random_tensor(m, n, p, 91)
+    b = qt.gen_random_tensor(n, s, p, 92)
+    want = qt.tprod_fast(a, b)
+    ranks = [FreqParallelTProduct(m, n, s, p, r, world, "cuda:0") for r in range(world)]
+    for x in ranks:
+        x.load_a(a.t1, a.t2)
+        x.load_b(b.t1, b.t2)
+    for _ in range(2):  # the tables are reused across steps
+        emulate_freq_parallel_routed(ranks)
+        torch.cuda.synchronize()
+        for x in ranks:
+            c1, c2 = x.result()
+            assert bits_equal(c1, want.t1[:, x.a0:x.a1]) and bits_equal(c2, want.t2[:, x.a0:x.a1]), (world, x.rank)
+
+
 def test_freq_parallel_single_rank_step_and_nonfinite():
     import torch
     from paper_2212_14318_b200.distributed import FreqParallelTProduct

@@ -11,6 +11,7 @@ import pytest
 
 import oracle as O
 import paper_2212_14318_b200 as qt
+from paper_2212_14318_b200 import _native
 from conftest import RefRng
 
 pytestmark = pytest.mark.gpu
@@ -199,6 +200,45 @@ def test_transforms_against_oracle(p):
     for gpu_fn, orc_fn in ((qt.qfft3_conj, O.qfft3_conj), (qt.qifft3_conj, O.qifft3_conj)):
         got = as_pair(gpu_fn(to_cd(x)))
         assert O.rel_frob_error(got, orc_fn(x)) <= TOL, p
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 16, 24, 32, 64, 97, 128, 256, 512])
+def test_routed_transforms_bitwise(p):
+    """qt_q{i}fft3_conj_f64_device_routed: frequency rows scattered to (gathered
+    from) arbitrary places through per-row pointer tables equal the plain
+    transforms bitwise."""
+    import torch
+    L = _native.lib()
+    assert L.qt_fft_routable(p) == 1
+    m, n = 7, 9
+    x = torch.randn((2, p, m, 2 * n), dtype=torch.float64, device="cuda")
+    plain = torch.empty_like(x)
+    _native.check(L.qt_qfft3_conj_f64_device(x[0].data_ptr(), x[1].data_ptr(), plain[0].data_ptr(),
+                                             plain[1].data_ptr(), m, n, p, None), "qfft3")
+    perm = torch.randperm(p).tolist()  # row k lands in slice perm[k] of a scratch tensor
+    scat = torch.full_like(x, float("nan"))
+    tab = torch.tensor([[scat[pl, perm[k]].data_ptr() for k in range(p)] for pl in (0, 1)], dtype=torch.int64,
+                       device="cuda")
+    _native.check(L.qt_qfft3_conj_f64_device_routed(x[0].data_ptr(), x[1].data_ptr(), tab[0].data_ptr(),
+                                                    tab[1].data_ptr(), m, n, p, None), "qfft3 routed")
+    assert torch.equal(scat[:, perm].view(torch.int64), plain.view(torch.int64))
+    inv = torch.empty_like(x)
+    _native.check(L.qt_qifft3_conj_f64_device(plain[0].data_ptr(), plain[1].data_ptr(), inv[0].data_ptr(),
+                                              inv[1].data_ptr(), m, n, p, None), "qifft3")
+    inv_r = torch.empty_like(x)
+    _native.check(L.qt_qifft3_conj_f64_device_routed(tab[0].data_ptr(), tab[1].data_ptr(), inv_r[0].data_ptr(),
+                                                     inv_r[1].data_ptr(), m, n, p, None), "qifft3 routed")
+    assert torch.equal(inv_r.view(torch.int64), inv.view(torch.int64))
+
+
+def test_routed_transforms_reject_two_pass_lengths():
+    L = _native.lib()
+    assert L.qt_fft_routable(4096) == 0 and L.qt_fft_routable(0) == 0
+    import torch
+    x = torch.zeros((2, 4096, 1, 2), dtype=torch.float64, device="cuda")
+    tab = torch.zeros((2, 4096), dtype=torch.int64, device="cuda")
+    assert L.qt_qfft3_conj_f64_device_routed(x[0].data_ptr(), x[1].data_ptr(), tab[0].data_ptr(), tab[1].data_ptr(),
+                                             1, 1, 4096, None) == _native.QT_EINVAL
 
 
 # -------------------------------------------------------------- properties

@@ -355,3 +355,51 @@ def test_slot_ranges_keep_pairs_whole():
             assert all(not (b & 1 and b < pair_end) for r in rs for b in r)
             sizes = [t1 - t0 for t0, t1 in rs]
             assert max(sizes) - min(sizes) <= 2, (p, world, rs)
+
+
+@pytest.mark.parametrize("m,n,s,p,world", [(9, 5, 6, 8, 2), (7, 3, 4, 7, 3), (5, 6, 3, 4, 3), (11, 4, 5, 6, 4),
+                                           (3, 2, 2, 2, 2), (6, 4, 3, 5, 1)])
+def test_freq_parallel_routing_tables(m, n, s, p, world):
+    """The row tables of the fused exchange (FreqParallelTProduct.set_peers):
+    every rank's frequency rows of Â/B̂, stored to the addresses its tables
+    give (a memmove per row stands in for the routed K1 stores into the
+    peers' stage buffers), and its rows of Ĉ, loaded from the addresses of
+    its K3 table, reproduce the point-to-point exchange — so the stitched C
+    equals the one-rank product bitwise."""
+    import ctypes
+    import oracle as O
+    from paper_2212_14318_b200 import shard
+    A = O.gen_random_tensor(m, n, p, 43)
+    B = O.gen_random_tensor(n, s, p, 44)
+    cls = _cpu_freq_class()
+    ranks = [cls(m, n, s, p, r, world, device="cpu") for r in range(world)]
+    bases = [x.stage_buffer.data_ptr() for x in ranks]
+    for x in ranks:
+        x.load_a(*A)
+        x.load_b(*B)
+        x.set_peers(bases)
+        x.k1()  # into x.ah / x.bh, then "stored" row by row through the tables
+        for key, src in (("a", x.ah), ("b", x.bh)):
+            rowbytes = src[0, 0].numel() * 8
+            if rowbytes == 0:
+                continue
+            for pl in (0, 1):
+                for k in range(p):
+                    ctypes.memmove(int(x.tables[key][pl][k]), src[pl, k].data_ptr(), rowbytes)
+    for x in ranks:
+        x.k2_multiply(x.k2_prepare())
+    for x in ranks:
+        rowbytes = x.c[0, 0].numel() * 8
+        if rowbytes:
+            for pl in (0, 1):
+                for k in range(p):
+                    ctypes.memmove(x.c[pl, k].data_ptr(), int(x.tables["c"][pl][k]), rowbytes)
+        x.k3()
+    one = cls(m, n, s, p, 0, 1, device="cpu")
+    one.load_a(*A)
+    one.load_b(*B)
+    one.step()
+    want = one.c.numpy().view(np.uint64)
+    for x in ranks:
+        r0, r1 = shard.row_slab(m, world, x.rank)
+        assert np.array_equal(x.c.numpy().view(np.uint64), want[:, :, r0:r1]), x.rank
