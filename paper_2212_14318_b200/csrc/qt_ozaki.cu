@@ -160,7 +160,38 @@ struct GemmParams {
   int bslot0;        // slot of this batch's first frequency in the B' buffer
   int nt, fcur;      // n tiles, slots in this batch (persistent pair kernel)
   int aslot0;        // slot of this batch's first frequency in the X' buffer
+  int slot0;         // absolute frequency slot of the batch's first slot
+  int share_end;     // slots below this share X': an odd one reads its even partner's (0: off)
 };
+
+// The odd slot 2j+1 (frequency sk) of a pair reuses the X' of its partner 2j
+// (frequency k): X_sk's rows are X_k's with the row halves swapped, the K
+// quarters permuted and some signs flipped (X_sk top = M(X_k bottom), X_sk
+// bottom = -M(X_k top), M[q0 q1 q2 q3] = [q1 -q0 -q3 q2]), so
+//   X_sk . Y_sk = [X_k bottom . Y''; -(X_k top . Y'')],  Y'' = M*(Y_sk),
+// M*[q0 q1 q2 q3] = [-q1 q0 q3 -q2] applied to every Y row.  The residue
+// kernels then write each X' row once instead of twice, the odd slot's B'
+// holds Y'' instead of Y, and its CRT reads the R rows in swapped order with
+// the top half negated — every integer is the same, so results are bitwise
+// the same as with a separate X_sk.
+__device__ __forceinline__ bool shares_x(int slot, int share_end) { return slot < share_end && (slot & 1); }
+
+// (slot, modulus) of the persistent GEMM's fq-th (slot, modulus) plane.  With
+// shared X' the two slots of a pair take turns per modulus, (2j, q), (2j+1, q),
+// (2j, q+1), ..., so the X' plane both read is still in L2 for the second;
+// otherwise slot-major.  (Batches start at an even slot: pairs stay together.)
+__device__ __forceinline__ void item_slot_mod(int fq, const GemmParams& P, int& f, int& q) {
+  const int fe = P.share_end > P.slot0 ? min(P.fcur, P.share_end - P.slot0) & ~1 : 0;  // shared slots of the batch
+  if (fq < fe * P.Q) {
+    const int pr = fq / (2 * P.Q), rem = fq - pr * 2 * P.Q;
+    q = rem >> 1;
+    f = 2 * pr + (rem & 1);
+  } else {
+    const int r = fq - fe * P.Q;
+    f = fe + r / P.Q;
+    q = r % P.Q;
+  }
+}
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -198,7 +229,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      const int arow = (P.aslot0 + f) * P.Mp + mtile * BM, brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN;
+      const int af = f - (shares_x(P.slot0 + f, P.share_end) ? 1 : 0);
+      const int arow = (P.aslot0 + af) * P.Mp + mtile * BM, brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN;
       uint32_t it = 0;
       for (int q = 0; q < P.Q; ++q)
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
@@ -363,9 +395,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {  // ---- TMA producer (both CTAs)
       uint32_t it = 0;
       for (int item = cl; item < nitems; item += ncl) {
-        const int t = item % tiles, fq = item / tiles, q = fq % P.Q, f = fq / P.Q;
+        const int t = item % tiles;
+        int f, q;
+        item_slot_mod(item / tiles, P, f, q);
         const int mtile2 = t % mt2, ntile = t / mt2;
-        const int arow = (P.aslot0 + f) * P.Mp + mtile2 * 256 + rank * BM;
+        const int af = f - (shares_x(P.slot0 + f, P.share_end) ? 1 : 0);
+        const int arow = (P.aslot0 + af) * P.Mp + mtile2 * 256 + rank * BM;
         const int brow = (P.bslot0 + f) * 2 * P.Sp + ntile * BN + rank * (BN / 2);
         for (int kb = 0; kb < P.KB; ++kb, ++it) {
           const int s = it % STAGES2;
@@ -402,7 +437,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const int row = quarter * 32 + lane;
     const size_t plane = (size_t)P.F * P.Mp * P.Sp * 2;
     for (int item = cl, li = 0; item < nitems; item += ncl, ++li) {
-      const int t = item % tiles, fq = item / tiles, q = fq % P.Q, f = fq / P.Q;
+      const int t = item % tiles;
+      int f, q;
+      item_slot_mod(item / tiles, P, f, q);
       const int mtile2 = t % mt2, ntile = t / mt2;
       const int b = li & 1;
       mbar_wait(&tfull[b], (li >> 1) & 1);
@@ -542,7 +579,7 @@ constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32
 __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __restrict__ a1,
                                                            const double2* __restrict__ a2, uint8_t* __restrict__ out,
                                                            int* __restrict__ eA, int* nonfinite, int m, int n, int p,
-                                                           int f0, int Mp, int F, int cbase) {
+                                                           int f0, int Mp, int F, int cbase, int share_end) {
   __shared__ double red[8];
   const int i = blockIdx.x, f = blockIdx.y;
   const int slot = f0 + f;
@@ -585,6 +622,10 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * Mp * Kp;
   uint8_t* up = out + (size_t)(f * Mp + i) * Kp;
   uint8_t* lo = out + (size_t)(fpart * Mp + m + i) * Kp;
+  // with shared X' (shares_x) a pair keeps only the even slot's X': its row i
+  // comes from the even CTA, its row m + i from the odd one
+  const bool pair_shared = fpart != f && slot < share_end;
+  const bool wu = !(pair_shared && (slot & 1)), wl = !(pair_shared && !(slot & 1));
   // work unit: 4 consecutive elements of ONE source row (P = A1_k[i] or Q = A2_sk[i]);
   // each residue goes to two places (one per output row)
   const int nq = n / kAVec;
@@ -619,10 +660,14 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
       const uint32_t wa = pack4(a[0], a[1], a[2], a[3]), wb = pack4(b[0], b[1], b[2], b[3]);
       const uint32_t wna = pack4(na[0], na[1], na[2], na[3]), wnb = pack4(nb[0], nb[1], nb[2], nb[3]);
       const size_t off = (size_t)q * plane;
-      *reinterpret_cast<uint32_t*>(pa + off) = wa;
-      *reinterpret_cast<uint32_t*>(pb + off) = isP ? wa : wna;
-      *reinterpret_cast<uint32_t*>(pc + off) = wb;
-      *reinterpret_cast<uint32_t*>(pd + off) = isP ? wnb : wb;
+      if (isP ? wu : wl) {
+        *reinterpret_cast<uint32_t*>(pa + off) = wa;
+        *reinterpret_cast<uint32_t*>(pc + off) = wb;
+      }
+      if (isP ? wl : wu) {
+        *reinterpret_cast<uint32_t*>(pb + off) = isP ? wa : wna;
+        *reinterpret_cast<uint32_t*>(pd + off) = isP ? wnb : wb;
+      }
     }
   }
 }
@@ -738,7 +783,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
                                                            const double2* __restrict__ b2,
                                                            const int* __restrict__ eB, uint8_t* __restrict__ out,
                                                            int n, int s, int p, int f0, int Sp, int F, uint64_t ldb,
-                                                           uint64_t bslice, int cbase) {
+                                                           uint64_t bslice, int cbase, int share_end) {
   extern __shared__ double2 tile[];  // [32][kBStride]
   const int c0 = blockIdx.x * 32, j0 = blockIdx.z * kBRows, f = blockIdx.y;
   const int k = slot_slice(f0 + f, p, cbase);
@@ -755,11 +800,16 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
   const int jl = 4 * tx, jb = j0 + jl;  // this lane's 4 consecutive rows
   if (jb >= 2 * n) return;
+  // odd slot of a shared-X' pair: Y'' = M*(Y), i.e. the halves of Y swapped
+  // (position jj) and, per half, its own sign pattern (see shares_x)
+  const bool yy = shares_x(f0 + f, share_end);
+  const bool top = jb < n;  // rows of B1 (else B2); 4 rows never straddle n (n % 32 == 0)
+  const int pos = yy ? (top ? jb + n : jb - n) : jb;
   for (int cc = ty; cc < 32; cc += 8) {
     const int c = c0 + cc;
     const int e = eB[f * Sp + c];
     const int tcol = c / BNC, ic = c % BNC;
-    uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp + jb;
+    uint8_t* re_row = out + ((size_t)f * 2 * Sp + tcol * BN + ic) * Kp + pos;
     uint8_t* im_row = re_row + (size_t)BNC * Kp;
     Limbs lr[4], li[4];
 #pragma unroll
@@ -771,19 +821,29 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
-      uint32_t a[4], b[4], nb[4];
+      uint32_t a[4], b[4], na[4], nb[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         a[t] = res_of(lr[t], q);
         b[t] = res_of(li[t], q);
+        na[t] = neg_res(a[t], pq);
         nb[t] = neg_res(b[t], pq);
       }
       const uint32_t wr = pack4(a[0], a[1], a[2], a[3]), wi = pack4(b[0], b[1], b[2], b[3]);
       const uint32_t wni = pack4(nb[0], nb[1], nb[2], nb[3]);
-      *reinterpret_cast<uint32_t*>(re_row) = wr;           // Re-row: Re Y
-      *reinterpret_cast<uint32_t*>(re_row + 2 * n) = wni;  // Re-row: -Im Y
-      *reinterpret_cast<uint32_t*>(im_row) = wi;           // Im-row: Im Y
-      *reinterpret_cast<uint32_t*>(im_row + 2 * n) = wr;   // Im-row: Re Y
+      if (!yy) {
+        *reinterpret_cast<uint32_t*>(re_row) = wr;           // Re-row: Re Y
+        *reinterpret_cast<uint32_t*>(re_row + 2 * n) = wni;  // Re-row: -Im Y
+        *reinterpret_cast<uint32_t*>(im_row) = wi;           // Im-row: Im Y
+        *reinterpret_cast<uint32_t*>(im_row + 2 * n) = wr;   // Im-row: Re Y
+      } else {
+        const uint32_t wnr = pack4(na[0], na[1], na[2], na[3]);
+        // Re-row'' = [-Re B2, Re B1, -Im B2, Im B1], Im-row'' = [-Im B2, Im B1, Re B2, -Re B1]
+        *reinterpret_cast<uint32_t*>(re_row) = top ? wr : wnr;
+        *reinterpret_cast<uint32_t*>(re_row + 2 * n) = top ? wi : wni;
+        *reinterpret_cast<uint32_t*>(im_row) = top ? wi : wni;
+        *reinterpret_cast<uint32_t*>(im_row + 2 * n) = top ? wnr : wr;
+      }
       re_row += plane;
       im_row += plane;
     }
@@ -812,7 +872,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
                                                      const int* __restrict__ eB, const int* nonfinite,
                                                      double2* __restrict__ c1, double2* __restrict__ c2, int m,
                                                      int s, int p, int f0, int bslot0, int Mp, int Sp, int F,
-                                                     uint64_t ldc, uint64_t cslice, int cbase) {
+                                                     uint64_t ldc, uint64_t cslice, int cbase, int share_end) {
   if (*nonfinite) return;
   const int cb = (blockIdx.x * blockDim.x + threadIdx.x) * kCrtVec;
   const int f = blockIdx.z;
@@ -824,8 +884,13 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
   }
   const int k = slot_slice(f0 + f, p, cbase);
   const size_t plane = (size_t)F * Mp * Sp * 2;  // bytes
+  // odd slot of a shared-X' pair: R row r < m is -C2[r], R row m + r is C1[r],
+  // with the row exponents of the even partner's X'
+  const bool sx = shares_x(f0 + f, share_end);
+  const int fa = sx ? f - 1 : f;
   for (int r = blockIdx.y; r < 2 * m; r += gridDim.y) {
     const uint8_t* ptr = R + ((size_t)(f * Mp + r) * Sp + cb) * 2;
+    const bool neg = sx && r < m;
     uint64_t acc[kCrtVec][2][3];
 #pragma unroll
     for (int t = 0; t < kCrtVec; ++t)
@@ -836,21 +901,24 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
       const uint2 v = __ldg(reinterpret_cast<const uint2*>(ptr));  // (re, im) bytes of 4 columns
       ptr += plane;
       const uint32_t w0 = c_mod.w[q][0], w1 = c_mod.w[q][1], w2 = c_mod.w[q][2];
+      const uint32_t pq = c_mod.p[q];
 #pragma unroll
       for (int t = 0; t < kCrtVec; ++t) {
         const uint32_t word = t < 2 ? v.x : v.y;
         const int sh = (t & 1) * 16;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t rr = (word >> (sh + 8 * h)) & 0xffu;
+          uint32_t rr = (word >> (sh + 8 * h)) & 0xffu;
+          if (neg) rr = neg_res(rr, pq);
           acc[t][h][0] += (uint64_t)rr * w0;
           acc[t][h][1] += (uint64_t)rr * w1;
           acc[t][h][2] += (uint64_t)rr * w2;
         }
       }
     }
-    const int ea = eA[f * Mp + r];
-    double2* dst = (r < m) ? c1 + k * cslice + (size_t)r * ldc : c2 + k * cslice + (size_t)(r - m) * ldc;
+    const int ea = eA[fa * Mp + r];
+    double2* dst = ((r < m) != sx) ? c1 + k * cslice + (size_t)(sx ? r - m : r) * ldc
+                                   : c2 + k * cslice + (size_t)(sx ? r : r - m) * ldc;
 #pragma unroll
     for (int t = 0; t < kCrtVec; ++t) {
       if (cb + t >= s) break;
@@ -993,6 +1061,12 @@ uint64_t a_slot_bytes(uint64_t m, uint64_t n, uint64_t s) {
 }
 uint64_t env_mb(const char* name, uint64_t dflt_mb) { return (uint64_t)oz::env_int(name, (int)dflt_mb) << 20; }
 
+// slots below this share X' within their pair (shares_x); QTB_OZAKI_SHAREX=0 turns it off
+int share_end(uint64_t p) {
+  static const bool on = oz::env_int("QTB_OZAKI_SHAREX", 1) != 0;
+  return on ? (int)(2 * ((p - 1) / 2)) : 0;
+}
+
 // slots per batch: even (pairs stay together), balanced over the batches
 uint64_t batch_slots(uint64_t p, uint64_t per_slot, uint64_t budget) {
   // (slots are a grid dimension of the residue / CRT kernels: <= 65534)
@@ -1032,7 +1106,8 @@ residues:
   ProfScope pb("k2_int8_residues_b", stream);
   oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
                         stream>>>(
-      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase);
+      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase,
+      share_end(B.p));
   pb.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -1048,7 +1123,7 @@ cudaError_t prep_a(const OzakiA& A, const double2* ah1, const double2* ah2, int*
   if (e != cudaSuccess) return e;
   ProfScope pr("k2_int8_residues", stream);
   oz_residue_a_kernel<<<dim3((unsigned)A.m, (unsigned)A.p), 256, 0, stream>>>(
-      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p, -1);
+      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p, -1, share_end(A.p));
   pr.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -1132,7 +1207,8 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
       ProfScope pr("k2_int8_residues", st);
       oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp,
                                                                    eA + b * F * Mp, flag, (int)m, (int)n, (int)p,
-                                                                   (int)f0, (int)Mp, (int)aslots, B.cbase);
+                                                                   (int)f0, (int)Mp, (int)aslots, B.cbase,
+                                                                   share_end(p));
       pr.stop();
       count_launches(1);
     }
@@ -1153,7 +1229,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     ProfScope pc("k2_int8_crt", st);
     oz_crt_kernel<<<cgrid, 256, 0, st>>>(ws + offR + b * bytesR, eA + aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m,
                                          (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice,
-                                         B.cbase);
+                                         B.cbase, share_end(p));
     pc.stop();
     count_launches(1);
   };
@@ -1174,7 +1250,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     if (res_ready) cudaStreamWaitEvent(stream, res_ready, 0);
     ProfScope pg("k2_int8_gemm", stream);
     GemmParams gp{ws + offR + b * bytesR, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0,
-                  (int)(Sp / BNC), fcur, (int)(A ? f0 : b * F)};
+                  (int)(Sp / BNC), fcur, (int)(A ? f0 : b * F), (int)f0, share_end(p)};
     if (use_pair()) {
       const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
       const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
