@@ -821,12 +821,11 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
       const uint32_t pq = c_mod.p[q];
-      uint32_t a[4], b[4], na[4], nb[4];
+      uint32_t a[4], b[4], nb[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         a[t] = res_of(lr[t], q);
         b[t] = res_of(li[t], q);
-        na[t] = neg_res(a[t], pq);
         nb[t] = neg_res(b[t], pq);
       }
       const uint32_t wr = pack4(a[0], a[1], a[2], a[3]), wi = pack4(b[0], b[1], b[2], b[3]);
@@ -837,7 +836,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
         *reinterpret_cast<uint32_t*>(im_row) = wi;           // Im-row: Im Y
         *reinterpret_cast<uint32_t*>(im_row + 2 * n) = wr;   // Im-row: Re Y
       } else {
-        const uint32_t wnr = pack4(na[0], na[1], na[2], na[3]);
+        const uint32_t wnr = pack4(neg_res(a[0], pq), neg_res(a[1], pq), neg_res(a[2], pq), neg_res(a[3], pq));
         // Re-row'' = [-Re B2, Re B1, -Im B2, Im B1], Im-row'' = [-Im B2, Im B1, Re B2, -Re B1]
         *reinterpret_cast<uint32_t*>(re_row) = top ? wr : wnr;
         *reinterpret_cast<uint32_t*>(re_row + 2 * n) = top ? wi : wni;
