@@ -526,6 +526,10 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
   return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
 __device__ __forceinline__ uint32_t neg_res(uint32_t r, uint32_t p) { return r ? p - r : 0u; }
+// -r mod p for an MMA operand byte: p - r in [1, p] (p itself stands for 0: the
+// GEMM only needs the value mod p, and 255^2 * 4n still bounds its sums), and
+// for p = 256 the packed low byte of 256 - r is -r mod 256.  One operation.
+__device__ __forceinline__ uint32_t neg_op(uint32_t r, uint32_t p) { return p - r; }
 
 __device__ __forceinline__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -646,27 +650,45 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
     uint8_t* pb = (isP ? lo + n : up + n) + j0;     // Re (P) / -Re (Q)
     uint8_t* pc = (isP ? up : lo) + 2 * n + j0;     // Im, plain
     uint8_t* pd = (isP ? lo : up) + 3 * n + j0;     // -Im (P) / Im (Q)
+    if (!pair_shared) {  // both output rows (self-paired frequency, or X' not shared)
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) {
-      const uint32_t pq = c_mod.p[q];
-      uint32_t a[kAVec], b[kAVec], na[kAVec], nb[kAVec];
+      for (int q = 0; q < kQ; ++q) {
+        const uint32_t pq = c_mod.p[q];
+        uint32_t a[kAVec], b[kAVec], na[kAVec], nb[kAVec];
 #pragma unroll
-      for (int t = 0; t < kAVec; ++t) {
-        a[t] = res_of(re[t], q);
-        b[t] = res_of(im[t], q);
-        na[t] = neg_res(a[t], pq);
-        nb[t] = neg_res(b[t], pq);
-      }
-      const uint32_t wa = pack4(a[0], a[1], a[2], a[3]), wb = pack4(b[0], b[1], b[2], b[3]);
-      const uint32_t wna = pack4(na[0], na[1], na[2], na[3]), wnb = pack4(nb[0], nb[1], nb[2], nb[3]);
-      const size_t off = (size_t)q * plane;
-      if (isP ? wu : wl) {
+        for (int t = 0; t < kAVec; ++t) {
+          a[t] = res_of(re[t], q);
+          b[t] = res_of(im[t], q);
+          na[t] = neg_op(a[t], pq);
+          nb[t] = neg_op(b[t], pq);
+        }
+        const uint32_t wa = pack4(a[0], a[1], a[2], a[3]), wb = pack4(b[0], b[1], b[2], b[3]);
+        const uint32_t wna = pack4(na[0], na[1], na[2], na[3]), wnb = pack4(nb[0], nb[1], nb[2], nb[3]);
+        const size_t off = (size_t)q * plane;
         *reinterpret_cast<uint32_t*>(pa + off) = wa;
         *reinterpret_cast<uint32_t*>(pc + off) = wb;
-      }
-      if (isP ? wl : wu) {
         *reinterpret_cast<uint32_t*>(pb + off) = isP ? wa : wna;
         *reinterpret_cast<uint32_t*>(pd + off) = isP ? wnb : wb;
+      }
+    } else {  // one output row: (Re, Im) at (pa, pc), or (Re | -Re, -Im | Im) at (pb, pd)
+      const bool first = isP ? wu : wl;
+      const bool nre = !first && !isP, nim = !first && isP;
+      uint8_t* p0 = first ? pa : pb;
+      uint8_t* p1 = first ? pc : pd;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const uint32_t pq = c_mod.p[q];
+        uint32_t a[kAVec], b[kAVec];
+#pragma unroll
+        for (int t = 0; t < kAVec; ++t) {
+          a[t] = res_of(re[t], q);
+          b[t] = res_of(im[t], q);
+          if (nre) a[t] = neg_op(a[t], pq);
+          if (nim) b[t] = neg_op(b[t], pq);
+        }
+        const size_t off = (size_t)q * plane;
+        *reinterpret_cast<uint32_t*>(p0 + off) = pack4(a[0], a[1], a[2], a[3]);
+        *reinterpret_cast<uint32_t*>(p1 + off) = pack4(b[0], b[1], b[2], b[3]);
       }
     }
   }
@@ -826,7 +848,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
       for (int t = 0; t < 4; ++t) {
         a[t] = res_of(lr[t], q);
         b[t] = res_of(li[t], q);
-        nb[t] = neg_res(b[t], pq);
+        nb[t] = neg_op(b[t], pq);
       }
       const uint32_t wr = pack4(a[0], a[1], a[2], a[3]), wi = pack4(b[0], b[1], b[2], b[3]);
       const uint32_t wni = pack4(nb[0], nb[1], nb[2], nb[3]);
@@ -836,7 +858,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
         *reinterpret_cast<uint32_t*>(im_row) = wi;           // Im-row: Im Y
         *reinterpret_cast<uint32_t*>(im_row + 2 * n) = wr;   // Im-row: Re Y
       } else {
-        const uint32_t wnr = pack4(neg_res(a[0], pq), neg_res(a[1], pq), neg_res(a[2], pq), neg_res(a[3], pq));
+        const uint32_t wnr = pack4(neg_op(a[0], pq), neg_op(a[1], pq), neg_op(a[2], pq), neg_op(a[3], pq));
         // Re-row'' = [-Re B2, Re B1, -Im B2, Im B1], Im-row'' = [-Im B2, Im B1, Re B2, -Re B1]
         *reinterpret_cast<uint32_t*>(re_row) = top ? wr : wnr;
         *reinterpret_cast<uint32_t*>(re_row + 2 * n) = top ? wi : wni;

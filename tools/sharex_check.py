@@ -1,11 +1,19 @@
-"""Bitwise check of the shared-X' int8 stage 2 against the separate-X' form:
-run twice (QTB_OZAKI_SHAREX=1 / 0), the second run compares with the first's output."""
+"""Bitwise check of the int8 stage 2 between two runs: the first saves its
+outputs, later runs compare against them — e.g. QTB_OZAKI_SHAREX=0 vs 1 (shared
+X' within a pair), or QTB_CHECK_LIB=<another build of the library> vs this one."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2212_14318_b200 import _native
-L = _native.lib()
+if os.environ.get("QTB_CHECK_LIB"):  # compare another build of the library (e.g. the previous commit's)
+    import ctypes
+    L = ctypes.CDLL(os.environ["QTB_CHECK_LIB"])
+    for name, (res, args) in _native.SIGNATURES.items():
+        if hasattr(L, name):
+            getattr(L, name).restype, getattr(L, name).argtypes = res, args
+else:
+    L = _native.lib()
 out = sys.argv[1]
 res = {}
 for (m, n, s, p) in [(150, 256, 520, 6), (64, 256, 256, 5), (300, 512, 384, 8), (33, 256, 130, 2), (2048, 2048, 2048, 4)]:
