@@ -16,3 +16,8 @@ echo "ncu list rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"oz_gemm2" -c 1 -o gpurun_out/rf_ncu_gemm \
   python bench.py --config 5 --no-cpu-baseline --steps 1 --warmup 1 --e2e-steps 0 > gpurun_out/rf_ncu2.log 2>&1
 echo "ncu full rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/rf_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 300 python tools/timeline.py > gpurun_out/rf_timeline.log 2>&1; echo "timeline rc=$?"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"oz_residue_b|oz_residue_a|oz_crt" -c 3 -o gpurun_out/rf_ncu_aux \
+  python bench.py --config 5 --no-cpu-baseline --steps 1 --warmup 1 --e2e-steps 0 > gpurun_out/rf_ncu3.log 2>&1
+echo "ncu aux rc=$?"
