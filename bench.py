@@ -655,7 +655,7 @@ def run_ours(args, cfg):
             t0 = time.perf_counter()
             e2e_step()  # synchronous: returns once C is in host memory
             calls.append(time.perf_counter() - t0)
-        e2e_s = float(np.median(calls))
+        e2e_s = float(statistics.median(calls))
         e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
