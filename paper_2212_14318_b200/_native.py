@@ -87,12 +87,16 @@ def lib() -> ctypes.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
+            # QTB_LIB_PATH: another build of this library (A/B timing of two builds on one box)
+            path = os.environ.get("QTB_LIB_PATH") or LIB_PATH
+            if not os.path.exists(path):
                 raise ImportError(
-                    f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                    f"{path} is missing: build it with `make` or __graft_entry__.build(); "
                     "there is no CPU fallback")
-            handle = ctypes.CDLL(LIB_PATH)
+            handle = ctypes.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
+                if path != LIB_PATH and not hasattr(handle, name):
+                    continue  # an older build without this entry point
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args
