@@ -800,23 +800,26 @@ __global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* _
 // tile is the faster one there.)
 constexpr int kBRows = 128;
 constexpr int kBStride = kBRows + kBRows / 8 + 1;  // 145 double2 per column
-constexpr size_t kResBSmem = sizeof(double2) * 32 * kBStride;
+// BC columns per CTA (32, or 16 for more CTAs per SM: smem BC * 145 * 16 B)
+constexpr size_t res_b_smem(int bc) { return sizeof(double2) * bc * kBStride; }
+template <int BC>
 __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2,
                                                            const int* __restrict__ eB, uint8_t* __restrict__ out,
                                                            int n, int s, int p, int f0, int Sp, int F, uint64_t ldb,
                                                            uint64_t bslice, int cbase, int share_end) {
-  extern __shared__ double2 tile[];  // [32][kBStride]
-  const int c0 = blockIdx.x * 32, j0 = blockIdx.z * kBRows, f = blockIdx.y;
+  extern __shared__ double2 tile[];  // [BC][kBStride]
+  const int c0 = blockIdx.x * BC, j0 = blockIdx.z * kBRows, f = blockIdx.y;
   const int k = slot_slice(f0 + f, p, cbase);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr int RPI = 32 / BC;  // rows per warp load
 #pragma unroll
-  for (int jj = ty; jj < kBRows; jj += 8) {
-    const int j = j0 + jj, c = c0 + tx;
+  for (int jj = ty * RPI + tx / BC; jj < kBRows; jj += 8 * RPI) {
+    const int j = j0 + jj, cl = tx % BC, c = c0 + cl;
     double2 y = make_double2(0.0, 0.0);
     if (c < s && j < 2 * n)
       y = (j < n ? b1 + k * bslice + (size_t)j * ldb : b2 + k * bslice + (size_t)(j - n) * ldb)[c];
-    tile[tx * kBStride + jj + (jj >> 3)] = y;
+    tile[cl * kBStride + jj + (jj >> 3)] = y;
   }
   __syncthreads();
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * 2 * Sp * Kp;
@@ -827,7 +830,7 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   const bool yy = shares_x(f0 + f, share_end);
   const bool top = jb < n;  // rows of B1 (else B2); 4 rows never straddle n (n % 32 == 0)
   const int pos = yy ? (top ? jb + n : jb - n) : jb;
-  for (int cc = ty; cc < 32; cc += 8) {
+  for (int cc = ty; cc < BC; cc += 8) {
     const int c = c0 + cc;
     const int e = eB[f * Sp + c];
     const int tcol = c / BNC, ic = c % BNC;
@@ -1046,7 +1049,9 @@ cudaError_t oz_init() {
     const ModTable t = make_table();
     cudaError_t r = cudaMemcpyToSymbol(c_mod, &t, sizeof(t));
     if (r != cudaSuccess) return r;
-    r = cudaFuncSetAttribute(oz_residue_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResBSmem);
+    r = cudaFuncSetAttribute(oz_residue_b_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_b_smem(32));
+    if (r != cudaSuccess) return r;
+    r = cudaFuncSetAttribute(oz_residue_b_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_b_smem(16));
     if (r != cudaSuccess) return r;
     for (auto [k, st] : {std::pair{oz_gemm2_kernel<4>, 4}, std::pair{oz_gemm2_kernel<5>, 5},
                          std::pair{oz_gemm2_kernel<6>, 6}})
@@ -1125,8 +1130,10 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   }
 residues:
   ProfScope pb("k2_int8_residues_b", stream);
-  oz_residue_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, kResBSmem,
-                        stream>>>(
+  static const int bc = env_int("QTB_RESB_COLS", 16) == 32 ? 32 : 16;  // 16: 4 CTAs per SM (measured faster)
+  auto kern = bc == 16 ? oz_residue_b_kernel<16> : oz_residue_b_kernel<32>;
+  kern<<<dim3((unsigned)(Sp / bc), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, res_b_smem(bc),
+         stream>>>(
       bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase,
       share_end(B.p));
   pb.stop();
