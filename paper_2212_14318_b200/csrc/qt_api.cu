@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -216,7 +217,19 @@ int d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
 
 }  // namespace
 
-void count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+namespace {
+// set while a stream capture records a small product's launches into a graph:
+// those launches are counted when the graph runs, not when it is recorded
+thread_local uint64_t* t_capture_count = nullptr;
+}  // namespace
+
+void count_launches(uint64_t k) {
+  if (t_capture_count) {
+    *t_capture_count += k;
+    return;
+  }
+  g_launches.fetch_add(k, std::memory_order_relaxed);
+}
 
 namespace {
 std::atomic<bool> g_prof{false};
@@ -341,10 +354,103 @@ int qt_prof_read(const char* tag, double* ms, uint64_t* launches) {
   return rc;
 }
 
+// ----------------------------------------------- CUDA graphs for small products
+// A small product (<= 256 MB, fp64 DMMA stage 2, one- or two-pass tube FFTs) is three to five
+// short launches whose launch gaps rival their run time.  The device entry
+// point records such a call once into a CUDA graph (stream capture on a
+// private stream, after one ordinary run that also creates the twiddle tables)
+// keyed by (device, the six pointers, m, n, s, p) and replays it on the
+// caller's stream afterwards: the same kernels with the same arguments, so the
+// results are bitwise the same.  QTB_GRAPH=0 disables it; profiling
+// (qt_prof_enable) bypasses it.
+namespace {
+struct GraphKey {
+  int dev;
+  uintptr_t ptr[6];
+  uint64_t m, n, s, p;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(dev, ptr[0], ptr[1], ptr[2], ptr[3], ptr[4], ptr[5], m, n, s, p) <
+           std::tie(o.dev, o.ptr[0], o.ptr[1], o.ptr[2], o.ptr[3], o.ptr[4], o.ptr[5], o.m, o.n, o.s, o.p);
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;  // null: capture failed, run directly
+  uint64_t kernels = 0;
+};
+std::mutex g_graph_mu;
+std::map<GraphKey, GraphEntry> g_graphs;
+constexpr size_t kMaxGraphs = 64;
+
+bool graph_eligible(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
+  static const bool on = [] {
+    const char* v = getenv("QTB_GRAPH");
+    return !(v && *v == '0');
+  }();
+  if (!on || prof_on() || m == 0 || n == 0 || s == 0 || p == 0 || p > kIntMax) return false;
+  if ((m * n + n * s + m * s) * p * 32 > (256ull << 20)) return false;
+  // the int8 stage 2 forks streams of its own; the one-launch-per-stage path
+  // for long prime lengths is left out as well
+  return choose_gemm_algo(n, s, p) == kAlgoDmma && (fft_single_pass((int)p) || fft_split_length((int)p));
+}
+
+cudaStream_t capture_stream(int device) {
+  thread_local cudaStream_t streams[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  return streams[device];
+}
+}  // namespace
+
 int qt_tprod_f64_device(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                         double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream) {
   t_err.clear();
-  return tprod_device_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (check_dims(m, n, s, p, "tprod_fast") != QT_OK || !graph_eligible(m, n, s, p)) {
+    t_err.clear();
+    return tprod_device_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, st);
+  }
+  int dev = 0;
+  int rc = current_device(&dev);
+  if (rc) return rc;
+  const GraphKey key{dev, {(uintptr_t)a1, (uintptr_t)a2, (uintptr_t)b1, (uintptr_t)b2, (uintptr_t)c1, (uintptr_t)c2},
+                     m, n, s, p};
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graphs.find(key);
+    if (it != g_graphs.end()) {
+      if (!it->second.exec) return tprod_device_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, st);
+      const cudaError_t e = cudaGraphLaunch(it->second.exec, st);
+      if (e != cudaSuccess) return cuda_fail(e, "tprod_fast (graph launch)");
+      count_launches(it->second.kernels);
+      return QT_OK;
+    }
+  }
+  // first call with this key: run it, then record it for the next ones
+  if ((rc = tprod_device_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, st)) != QT_OK) return rc;
+  GraphEntry ent;
+  cudaStream_t cs = capture_stream(dev);
+  if (cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    t_capture_count = &ent.kernels;
+    const int crc = tprod_device_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, cs);
+    t_capture_count = nullptr;
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(cs, &g);
+    if (crc == QT_OK && ee == cudaSuccess && g && cudaGraphInstantiate(&ent.exec, g, 0) != cudaSuccess)
+      ent.exec = nullptr;
+    if (g) cudaGraphDestroy(g);
+    if (!ent.exec) ent.kernels = 0;
+  }
+  (void)cudaGetLastError();  // a failed capture leaves nothing behind: that key runs directly
+  t_err.clear();
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  if (g_graphs.size() >= kMaxGraphs) {
+    for (auto& kv : g_graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    g_graphs.clear();
+  }
+  auto ins = g_graphs.emplace(key, ent);
+  if (!ins.second && ent.exec) cudaGraphExecDestroy(ent.exec);  // another thread recorded it first
+  return QT_OK;
 }
 
 int qt_qfft3_conj_f64_device(const double* x1, const double* x2, double* y1, double* y2, uint64_t m, uint64_t n,

@@ -604,6 +604,19 @@ bool fft_single_pass(int p) {
   return !(narrow && p1 > 1 && p2 > 1 && p1 <= 2048);
 }
 
+bool fft_split_length(int p) {
+  if (p <= 0 || fft_single_pass(p)) return false;
+  const FftPlan plan = make_fft_plan(p);
+  const size_t per_tube = (size_t)fft_smem_buffers(plan) * sizeof(double2) * (size_t)p;
+  const bool narrow = per_tube > kSmemMax || (per_tube << 3) > kSmemMax;
+  int p1 = 0, p2 = 0;
+  if (narrow) split_length(p, &p1, &p2);
+  if (!(p1 > 1 && p2 > 1 && p1 <= 2048)) return false;
+  const FftPlan pl1 = make_fft_plan(p1), pl2 = make_fft_plan(p2);
+  size_t sm = 0;
+  return choose_logT(pl1, p1, 1, 1, 1, &sm) >= 0 && choose_logT(pl2, p2, 1, 1, 1, &sm) >= 0;
+}
+
 cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device) {
   if (batch.njobs == 0) return cudaSuccess;
   uint64_t maxtubes = 0;

@@ -68,6 +68,8 @@ const double2* twiddles_for(int device, int p, cudaStream_t stream);
 cudaError_t launch_tube_fft(const TubeBatch& batch, int p, cudaStream_t stream, int device);
 // The length-p transform runs as one pass (so routed rows are supported).
 bool fft_single_pass(int p);
+// The length-p transform runs as the two-pass four-step split.
+bool fft_split_length(int p);
 
 // ------------------------------------------------------ paired spectral GEMM
 // chat[k] for all k from ahat, bhat (slice-major CD planes), tproduct.cpp:90-104.

@@ -241,6 +241,41 @@ def test_routed_transforms_reject_two_pass_lengths():
                                              1, 1, 4096, None) == _native.QT_EINVAL
 
 
+@pytest.mark.parametrize("m,n,s,p,kernels", [(32, 32, 32, 16, 3), (8, 8, 8, 4096, 5)])
+def test_small_product_graph_replay(m, n, s, p, kernels):
+    """qt_tprod_f64_device records a small product into a CUDA graph on its
+    first call and replays it afterwards: every call is bitwise equal to the
+    host entry point, a replay reads the buffers' current contents, and it
+    still counts its three kernels."""
+    import torch
+    L = _native.lib()
+    dev = torch.device("cuda", 0)
+    a = qt.gen_random_tensor(m, n, p, 501)
+    b = qt.gen_random_tensor(n, s, p, 502)
+    da = [torch.from_numpy(x.view(np.float64)).to(dev) for x in (a.t1, a.t2)]
+    db = [torch.from_numpy(x.view(np.float64)).to(dev) for x in (b.t1, b.t2)]
+    dc = [torch.empty((p, m, 2 * s), dtype=torch.float64, device=dev) for _ in range(2)]
+
+    def call():
+        _native.check(L.qt_tprod_f64_device(da[0].data_ptr(), da[1].data_ptr(), db[0].data_ptr(), db[1].data_ptr(),
+                                            dc[0].data_ptr(), dc[1].data_ptr(), m, n, s, p, None), "tprod")
+        torch.cuda.synchronize()
+        return [x.cpu().numpy().view(np.complex128) for x in dc]
+
+    want = qt.tprod_fast(a, b)
+    for i in range(3):  # direct + capture, then replays
+        before = L.qt_kernel_launches()
+        got = call()
+        assert bits_equal(got[0], want.t1) and bits_equal(got[1], want.t2), i
+        assert L.qt_kernel_launches() - before == kernels, i
+    a2 = qt.gen_random_tensor(m, n, p, 503)  # new contents, same buffers
+    da[0].copy_(torch.from_numpy(a2.t1.view(np.float64)))
+    da[1].copy_(torch.from_numpy(a2.t2.view(np.float64)))
+    got = call()
+    want2 = qt.tprod_fast(a2, b)
+    assert bits_equal(got[0], want2.t1) and bits_equal(got[1], want2.t2)
+
+
 # -------------------------------------------------------------- properties
 def test_determinism_and_row_shard_invariance():
     """Repeated calls are bitwise identical, and row slabs computed separately
