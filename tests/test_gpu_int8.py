@@ -483,3 +483,25 @@ def test_freq_parallel_single_rank_step_and_nonfinite():
     x.step()
     with pytest.raises(FloatingPointError):
         x.result()
+
+
+@pytest.mark.parametrize("env", [{"QTB_OZAKI_SHAREX": "0"}, {"QTB_RESB_COLS": "32"}, {"QTB_OZAKI_2SM": "0"}])
+def test_implementation_switches_bitwise(tmp_path, env):
+    """The int8 stage 2 is the same integer computation whatever the layout
+    switch: shared X' within a frequency pair on/off, 16- or 32-column B'
+    residue tiles, CTA-pair or 1-CTA GEMM — bitwise equal outputs (the
+    switches are read once per process, so the other setting runs in a
+    subprocess: tools/sharex_check.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "ref.npz")
+    tool = os.path.join(root, "tools", "sharex_check.py")
+    r1 = subprocess.run([sys.executable, tool, out], capture_output=True, text=True, cwd=root, timeout=600)
+    assert r1.returncode == 0 and "saved" in r1.stdout, r1.stderr[-2000:]
+    r2 = subprocess.run([sys.executable, tool, out], capture_output=True, text=True, cwd=root, timeout=600,
+                        env={**os.environ, **env})
+    assert r2.returncode == 0, r2.stderr[-2000:]
+    lines = [x for x in r2.stdout.splitlines() if x.strip()]
+    assert len(lines) == 5 and all(x.endswith("bitwise equal") for x in lines), r2.stdout
