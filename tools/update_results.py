@@ -36,7 +36,7 @@ rows = ["| cfg | step | eff. TF/s | K2 kernel (roofline) | K1 / K3 vs HBM 6552 G
         fmt(2, "2 (256³, p=64)"), fmt(3, "3 (16³, p=4096)"), fmt(1, "1 (32³, p=16)")]
 s = open(P("DESIGN.md")).read()
 a = s.index("| cfg | step | eff. TF/s | K2 kernel (roofline)")
-b = s.index("Config 5 before the int8 path")
+b = min(s.index(t) for t in ("**Boxes differ", "Config 5 before the int8 path") if t in s)
 s = s[:a] + "\n".join(rows) + "\n\n" + s[b:]
 s = re.sub(r"speed-up ≈ \d+×, e2e ≈ \d+×", f"speed-up ≈ {d[5]['value'] / ref:.0f}×, e2e ≈ {d[5]['e2e']['value'] / ref:.0f}×", s)
 open(P("DESIGN.md"), "w").write(s)
