@@ -276,6 +276,37 @@ def test_small_product_graph_replay(m, n, s, p, kernels):
     assert bits_equal(got[0], want2.t1) and bits_equal(got[1], want2.t2)
 
 
+def test_graph_cache_many_keys_and_shapes():
+    """More than the cache holds (64) distinct (pointers, shape) keys, several
+    shapes incl. p = 1 and a prime length, revisited in a different order:
+    every call equals the host entry point bitwise."""
+    import torch
+    L = _native.lib()
+    dev = torch.device("cuda", 0)
+    shapes = [(5, 3, 4, 1), (6, 4, 5, 7), (9, 8, 7, 12), (4, 6, 3, 97)]
+    bufs = []
+    for i in range(70):
+        m, n, s, p = shapes[i % len(shapes)]
+        a = qt.gen_random_tensor(m, n, p, 700 + i)
+        b = qt.gen_random_tensor(n, s, p, 800 + i)
+        da = [torch.from_numpy(x.view(np.float64)).to(dev) for x in (a.t1, a.t2)]
+        db = [torch.from_numpy(x.view(np.float64)).to(dev) for x in (b.t1, b.t2)]
+        dc = [torch.empty((p, m, 2 * s), dtype=torch.float64, device=dev) for _ in range(2)]
+        bufs.append(((m, n, s, p), a, b, da, db, dc))
+    for rnd in range(2):
+        order = range(len(bufs)) if rnd == 0 else reversed(range(len(bufs)))
+        for i in order:
+            (m, n, s, p), a, b, da, db, dc = bufs[i]
+            _native.check(L.qt_tprod_f64_device(da[0].data_ptr(), da[1].data_ptr(), db[0].data_ptr(),
+                                                db[1].data_ptr(), dc[0].data_ptr(), dc[1].data_ptr(), m, n, s, p,
+                                                None), "tprod")
+        torch.cuda.synchronize()
+        for (m, n, s, p), a, b, da, db, dc in bufs[::7]:
+            want = qt.tprod_fast(a, b)
+            got = [x.cpu().numpy().view(np.complex128) for x in dc]
+            assert bits_equal(got[0], want.t1) and bits_equal(got[1], want.t2), (rnd, m, n, s, p)
+
+
 # -------------------------------------------------------------- properties
 def test_determinism_and_row_shard_invariance():
     """Repeated calls are bitwise identical, and row slabs computed separately
