@@ -78,9 +78,11 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
     ap.add_argument("--exchange", choices=["auto", "fused", "p2p"], default="auto",
-                    help="frequency-parallel exchange: fused = Â/B̂ stored by K1 and Ĉ loaded by K3 straight "
-                         "from the peers' stage buffers (symmetric memory over NVLink, two device barriers per "
-                         "step); p2p = NCCL send/recv groups; auto = fused when available")
+                    help="N > 1 exchange: fused = the transfers done by the tube FFTs' own stores/loads into "
+                         "the peers' stage buffers (symmetric memory over NVLink, two device barriers per step) — "
+                         "frequency-parallel: Â/B̂ stored by K1, Ĉ loaded by K3; 2-D grid: each piece transformed "
+                         "once by its owner and stored into its whole row/column group; p2p = NCCL (send/recv "
+                         "groups, piece broadcasts); auto = fused when available")
     ap.add_argument("--multi", choices=["auto", "freq", "grid"], default="auto",
                     help="N > 1 decomposition: freq = frequency-parallel (int8 stage 2), grid = 2-D blocks of C; "
                          "auto = freq when the product takes the int8 stage 2")
@@ -352,7 +354,20 @@ def run_ours(args, cfg):
             # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
             # block arrive as pieces broadcast (NCCL) from their owners inside the
             # step, overlapping K1 / stage 2 (paper_2212_14318_b200/distributed.py)
-            sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev)
+            peer = None
+            if args.exchange != "p2p" and dist.is_initialized() and FreqParallelTProduct.routable(cfg.p):
+                try:
+                    from paper_2212_14318_b200.distributed import make_peer_grid_stage
+                    peer = make_peer_grid_stage(cfg.m, cfg.n, cfg.s, cfg.p, rank, world,
+                                                shard.grid_shape(world, cfg.m, cfg.s), dev, dist)
+                except Exception as exc:  # no symmetric memory here: NCCL broadcasts instead
+                    if args.exchange == "fused":
+                        raise
+                    print(f"[bench] fused broadcasts unavailable ({type(exc).__name__}: {exc}); using NCCL",
+                          file=sys.stderr)
+            exchange_kind = "fused" if peer is not None else "p2p"
+            sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev,
+                                     stage_buffer=peer[0] if peer else None)
             gr, gc = sharded.gr, sharded.gc
             sharded.load_a(a.t1, a.t2)
             sharded.load_b(b.t1, b.t2)
@@ -373,8 +388,16 @@ def run_ours(args, cfg):
                 if gr > 1:
                     bcast_col = lambda t, src: dist.broadcast(t, src, group=col_groups[sharded.j], async_op=True)
 
+            if peer is not None:
+                sharded.set_peers(peer[1])
+                if world > 1:
+                    dist.barrier()
+
             def step():
-                sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
+                if peer is not None:
+                    sharded.step_fused(peer[2])
+                else:
+                    sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
         del a, b
         # stage-timing operands of this rank's block shape
         da1 = torch.randn((cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
@@ -713,7 +736,9 @@ def run_ours(args, cfg):
                                         + ("+exchange fused into K1 stores / K3 loads (symmetric memory)"
                                            if exchange_kind == "fused" else "+NCCL point-to-point exchange")
                                         if mode == "freq" else
-                                        f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)+piece broadcasts")
+                                        f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)"
+                                        + ("+piece broadcasts fused into the owners' K1 stores (symmetric memory)"
+                                           if exchange_kind == "fused" else "+NCCL piece broadcasts"))
                                        if sharded_mode else f"rows{world}")
                        + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
                        "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",

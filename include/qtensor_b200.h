@@ -120,6 +120,14 @@ int qt_fft_routable(uint64_t p);
 int qt_qfft3_conj_f64_device_routed(const double* x1, const double* x2,
                                     double* const* y1_rows, double* const* y2_rows,
                                     uint64_t m, uint64_t n, uint64_t p, void* stream);
+/* The forward routed transform with a broadcast fused into its stores:
+ * y{X}_rows holds ndst tables of p pointers (destination d's table at
+ * y{X}_rows + d * p), and frequency k of plane X is written to every
+ * y{X}_rows[d * p + k] (the 2-D multi-GPU decomposition: a piece transformed
+ * once by its owner, stored into every rank of its row / column group). */
+int qt_qfft3_conj_f64_device_routed_n(const double* x1, const double* x2,
+                                      double* const* y1_rows, double* const* y2_rows, int ndst,
+                                      uint64_t m, uint64_t n, uint64_t p, void* stream);
 int qt_qifft3_conj_f64_device_routed(const double* const* x1_rows, const double* const* x2_rows,
                                      double* y1, double* y2,
                                      uint64_t m, uint64_t n, uint64_t p, void* stream);

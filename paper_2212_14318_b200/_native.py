@@ -35,6 +35,7 @@ SIGNATURES = {
     "qt_fft_routable": (ctypes.c_int, [_u64]),
     "qt_qfft3_conj_f64_device_routed": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),
     "qt_qifft3_conj_f64_device_routed": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [_vp]),
+    "qt_qfft3_conj_f64_device_routed_n": (ctypes.c_int, [_dp] * 4 + [ctypes.c_int] + [_u64] * 3 + [_vp]),
     "qt_spectral_product_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_spectral_product_f64_device_ld": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [_vp]),
     "qt_spectral_product_f64_device_ld_algo": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [ctypes.c_int, _vp]),

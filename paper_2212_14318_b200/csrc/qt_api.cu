@@ -485,6 +485,28 @@ int qt_qfft3_conj_f64_device_routed(const double* x1, const double* x2, double* 
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "qfft3_conj (routed)");
 }
 
+int qt_qfft3_conj_f64_device_routed_n(const double* x1, const double* x2, double* const* y1_rows,
+                                      double* const* y2_rows, int ndst, uint64_t m, uint64_t n, uint64_t p,
+                                      void* stream) {
+  t_err.clear();
+  int rc = check_dims(m, n, 1, p, "qfft3_conj (routed, n destinations)");
+  if (rc) return rc;
+  if (!qt_fft_routable(p)) return fail(QT_EINVAL, "qfft3_conj (routed): this length is transformed in two passes");
+  if (!y1_rows || !y2_rows || ndst < 1 || ndst > 64) return fail(QT_EINVAL, "qfft3_conj (routed): bad row tables");
+  int dev = 0;
+  if ((rc = current_device(&dev))) return rc;
+  if (m * n == 0) return QT_OK;
+  TubeBatch b{};
+  add_forward(b, x1, x2, nullptr, nullptr, m * n);
+  for (int i = 0; i < 2; ++i) {
+    b.job[i].out_rows = reinterpret_cast<double2* const*>(i ? y2_rows : y1_rows);
+    b.job[i].out_ndst = ndst;
+    b.job[i].out_rows_stride = (int)p;
+  }
+  cudaError_t e = launch_tube_fft(b, (int)p, (cudaStream_t)stream, dev);
+  return e == cudaSuccess ? QT_OK : cuda_fail(e, "qfft3_conj (routed)");
+}
+
 int qt_qifft3_conj_f64_device_routed(const double* const* x1_rows, const double* const* x2_rows, double* y1,
                                      double* y2, uint64_t m, uint64_t n, uint64_t p, void* stream) {
   t_err.clear();

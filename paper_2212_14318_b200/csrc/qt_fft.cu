@@ -227,7 +227,13 @@ __device__ __forceinline__ void store_out(const TubeJob& job, uint64_t t0, const
   if (G.post_tw && g != 0) v = cmul(v, __ldg(&tw[g * kk]));
   const double sc = job.scale;
   const double sci = job.conj_out ? -sc : sc;
-  out_row<ROUTED>(job, g * G.og + kk * G.os, t0)[t] = make_double2(v.x * sc, v.y * sci);
+  const double2 o = make_double2(v.x * sc, v.y * sci);
+  const int row = g * G.og + kk * G.os;
+  if (ROUTED && job.out_rows) {
+    for (int d = 0; d < job.out_ndst; ++d) job.out_rows[d * job.out_rows_stride + row][t0 + t] = o;
+  } else {
+    out_row<ROUTED>(job, row, t0)[t] = o;
+  }
 }
 
 // stage 0: HBM -> registers -> smem (Ns = 1, so no twiddles)
@@ -432,9 +438,13 @@ __global__ void __launch_bounds__(256) tube_fft2_kernel(TubeBatch batch, FftGeom
         double2 y = v[k];
         if (G.post_tw && g != 0) y = cmul(y, __ldg(&tw[g * kk]));
         const double2 o = make_double2(y.x * sc, y.y * sci);
-        double2* dst = ROUTED && job.out_rows ? &job.out_rows[kk][t0 + t] : &out[(uint64_t)kk * ostr + t];
-        if (job.stream_out) __stcs(dst, o);
-        else *dst = o;
+        if (ROUTED && job.out_rows) {
+          for (int d = 0; d < job.out_ndst; ++d) job.out_rows[d * job.out_rows_stride + kk][t0 + t] = o;
+        } else {
+          double2* dst = &out[(uint64_t)kk * ostr + t];
+          if (job.stream_out) __stcs(dst, o);
+          else *dst = o;
+        }
       }
     }
   }

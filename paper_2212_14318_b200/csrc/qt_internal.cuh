@@ -40,6 +40,10 @@ struct TubeJob {
   // to the ranks that own them (or gather them) over NVLink.
   const double2* const* in_rows = nullptr;
   double2* const* out_rows = nullptr;
+  // several destinations per output row (a broadcast fused into the stores):
+  // destination d's table at out_rows + d * out_rows_stride
+  int out_ndst = 1;
+  int out_rows_stride = 0;
 };
 
 constexpr int kMaxJobs = 4;

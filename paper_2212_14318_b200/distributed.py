@@ -143,7 +143,8 @@ class Grid2DTProduct:
     stitched C is bitwise identical for every grid.
     """
 
-    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None, grid=None):
+    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None, grid=None,
+                 stage_buffer=None):
         import torch
         self.torch = torch
         self.m, self.n, self.s, self.p = m, n, s, p
@@ -163,12 +164,85 @@ class Grid2DTProduct:
         f64 = dict(dtype=torch.float64, device=self.dev)
         self.a = [torch.empty((2, p, hi - lo, 2 * n), **f64) for lo, hi, _ in self.apieces]
         self.ah_p = [torch.empty_like(t) for t in self.a]
-        self.ah = torch.empty((2, p, self.rows, 2 * n), **f64)
         self.b = [torch.empty((2, p, n, 2 * (hi - lo)), **f64) for lo, hi, _ in self.bpieces]
-        self.bh = [torch.empty_like(t) for t in self.b]
+        # Â block and B̂ pieces: carved out of `stage_buffer` (e.g. symmetric
+        # memory the group's owners store into) or allocated here
+        sizes = self.stage_sizes(m, n, s, p, world, (self.gr, self.gc))[rank]
+        if stage_buffer is None:
+            stage_buffer = torch.empty(sum(sizes), **f64)
+        assert stage_buffer.dtype == torch.float64 and stage_buffer.numel() >= sum(sizes)
+        self.stage_buffer = stage_buffer
+        self.ah = stage_buffer[:sizes[0]].view(2, p, self.rows, 2 * n)
+        self.bh, off = [], sizes[0]
+        for lo, hi, _ in self.bpieces:
+            e = 2 * p * n * 2 * (hi - lo)
+            self.bh.append(stage_buffer[off:off + e].view(2, p, n, 2 * (hi - lo)))
+            off += e
         self.c = torch.empty((2, p, self.rows, 2 * self.cols), **f64)
         self.L = _native.lib()
         self.algo = self.L.qt_gemm_algo(m, n, s, p)
+        self.tables = None
+
+    @staticmethod
+    def stage_sizes(m: int, n: int, s: int, p: int, world: int, grid):
+        """Per rank: float64 elements of (its Â block, all its B̂ pieces)."""
+        gr, gc = grid
+        out = []
+        for r in range(world):
+            i, j = divmod(r, gc)
+            r0, r1 = shard.row_slab(m, gr, i)
+            c0, c1 = shard.split_range(0, s, gc, tile=16)[j]
+            out.append((2 * p * (r1 - r0) * 2 * n, 2 * p * n * 2 * (c1 - c0)))
+        return out
+
+    # ------------------------------------------------ broadcast fused into K1
+    # With every rank's stage buffer addressable (peer_bases, as seen from this
+    # GPU), an owner transforms its piece ONCE and K1's stores put every
+    # frequency row of it straight into the Â block (B̂ piece) of each rank of
+    # its row (column) group — qt_qfft3_conj_f64_device_routed_n, one table per
+    # destination — instead of broadcasting the raw piece for every rank of the
+    # group to transform again.
+    def set_peers(self, peer_bases) -> None:
+        torch, p, n = self.torch, self.p, self.n
+        sizes = self.stage_sizes(self.m, n, self.s, p, self.world, (self.gr, self.gc))
+        self.tables = {}
+        for k, (lo, hi, owner) in enumerate(self.apieces):
+            if owner != self.rank or hi == lo:
+                continue
+            dsts = [self.i * self.gc + jj for jj in range(self.gc)]
+            tab = [[peer_bases[d] + 16 * (((pl * p + r) * self.rows + (lo - self.r0)) * n)
+                    for d in dsts for r in range(p)] for pl in (0, 1)]
+            self.tables[("a", k)] = (torch.tensor(tab, dtype=torch.int64, device=self.dev), len(dsts))
+        for k, (lo, hi, owner) in enumerate(self.bpieces):
+            if owner != self.rank or hi == lo:
+                continue
+            dsts = [ii * self.gc + self.j for ii in range(self.gr)]
+            before = sum(2 * p * n * 2 * (h - l) for l, h, _ in self.bpieces[:k])
+            cols = hi - lo
+            tab = [[peer_bases[d] + 8 * (sizes[d][0] + before) + 16 * ((pl * p + r) * n * cols)
+                    for d in dsts for r in range(p)] for pl in (0, 1)]
+            self.tables[("b", k)] = (torch.tensor(tab, dtype=torch.int64, device=self.dev), len(dsts))
+
+    def k1_fused(self, stream=None) -> None:
+        """K1 of this rank's own pieces, stored into every rank of their groups."""
+        st = self.torch.cuda.current_stream() if stream is None else stream
+        for (kind, k), (tab, nd) in self.tables.items():
+            x = self.a[k] if kind == "a" else self.b[k]
+            lo, hi, _ = (self.apieces if kind == "a" else self.bpieces)[k]
+            rows, width = (hi - lo, self.n) if kind == "a" else (self.n, hi - lo)
+            _native.check(self.L.qt_qfft3_conj_f64_device_routed_n(
+                x[0].data_ptr(), x[1].data_ptr(), tab[0].data_ptr(), tab[1].data_ptr(), nd, rows, width, self.p,
+                st.cuda_stream), f"qfft3_conj routed ({kind} piece)")
+
+    def step_fused(self, barrier, stream=None) -> None:
+        """One step with the piece broadcasts fused into the owners' K1:
+        K1 of own pieces → barrier → stage 2 of every B̂ piece → barrier → K3
+        (the second barrier: no rank still reads the Â/B̂ the next K1 rewrites)."""
+        self.k1_fused(stream)
+        barrier()
+        self._stage2(stream)
+        barrier()
+        self._k3(stream)
 
     # ---------------------------------------------------------------- inputs
     def owns_a(self, k: int) -> bool:
@@ -216,6 +290,16 @@ class Grid2DTProduct:
                           "qfft3_conj(A piece)")
             if not one:
                 self.ah[:, :, lo - self.r0:hi - self.r0].copy_(self.ah_p[k])
+        self._stage2(stream, wb=wb, transform_b=True)
+        self._k3(stream)
+
+    def _stage2(self, stream=None, wb=None, transform_b=False) -> None:
+        """Stage 2 of every B̂ piece into its columns of the C block (after
+        transforming the arrived raw piece when transform_b)."""
+        torch = self.torch
+        st = torch.cuda.current_stream() if stream is None else stream
+        sh = st.cuda_stream
+        L, n, p = self.L, self.n, self.p
         plan = None
         if self.rows and self.algo == 1:
             h = ctypes.c_void_p()
@@ -228,9 +312,10 @@ class Grid2DTProduct:
             if hi == lo or not self.rows:
                 continue
             cols = hi - lo
-            _native.check(L.qt_qfft3_conj_f64_device(self.b[k][0].data_ptr(), self.b[k][1].data_ptr(),
-                                                     self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), n, cols, p,
-                                                     sh), "qfft3_conj(B piece)")
+            if transform_b:
+                _native.check(L.qt_qfft3_conj_f64_device(self.b[k][0].data_ptr(), self.b[k][1].data_ptr(),
+                                                         self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), n, cols,
+                                                         p, sh), "qfft3_conj(B piece)")
             off = 16 * (lo - self.c0)
             if plan is not None:
                 _native.check(L.qt_int8_plan_multiply(
@@ -244,10 +329,13 @@ class Grid2DTProduct:
                     cols, self.cols, n * cols, self.rows * self.cols, self.algo, sh), "spectral_product(piece)")
         if plan is not None:
             _native.check(L.qt_int8_plan_destroy(plan, sh), "int8 plan destroy")
+
+    def _k3(self, stream=None) -> None:
+        st = self.torch.cuda.current_stream() if stream is None else stream
         if self.rows and self.cols:
-            _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
-                                                      self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
-                                                      self.cols, p, sh), "qifft3_conj(C block)")
+            _native.check(self.L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
+                                                           self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
+                                                           self.cols, self.p, st.cuda_stream), "qifft3_conj(C block)")
 
     def result(self):
         """(c1, c2) of this rank's block as host complex128 (p, rows, cols)."""
@@ -591,6 +679,40 @@ def emulate_freq_parallel_routed(ranks) -> None:
         x.k2_multiply(x.k2_prepare())
     for x in ranks:
         x.k3_routed()
+
+
+def emulate_grid_fused(ranks) -> None:
+    """One step of G Grid2DTProduct instances (rank r = ranks[r]) with the
+    piece broadcasts fused into the owners' K1, in lockstep on one device: the
+    row tables point into the other instances' stage buffers, and lockstep
+    order stands in for the barriers."""
+    bases = [x.stage_buffer.data_ptr() for x in ranks]
+    for x in ranks:
+        if x.tables is None:
+            x.set_peers(bases)
+    for x in ranks:
+        x.k1_fused()
+    for x in ranks:
+        x._stage2()
+    for x in ranks:
+        x._k3()
+
+
+def make_peer_grid_stage(m: int, n: int, s: int, p: int, rank: int, world: int, grid, device, dist_mod,
+                         group=None):
+    """Symmetric-memory stage buffer for Grid2DTProduct, the peers' base
+    addresses and a device barrier (as make_peer_stage)."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+    numel = max(sum(x) for x in Grid2DTProduct.stage_sizes(m, n, s, p, world, grid))
+    buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
+    hdl = symm_mem.rendezvous(buf, group if group is not None else dist_mod.group.WORLD)
+    bases = [int(x) for x in hdl.buffer_ptrs]
+
+    def barrier():
+        hdl.barrier(channel=0)
+
+    return buf, bases, barrier
 
 
 def emulate_freq_parallel(ranks) -> None:

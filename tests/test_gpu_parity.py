@@ -496,3 +496,32 @@ def test_grid2d_pipeline_bitwise(m, n, s, p, grid):
         assert bits_equal(c2, want.t2[:, g.r0:g.r1, g.c0:g.c1]), (grid, r)
         covered[g.r0:g.r1, g.c0:g.c1] = True
     assert covered.all()
+
+
+@pytest.mark.parametrize("m,n,s,p,grid", [(150, 40, 70, 12, (2, 2)), (150, 40, 70, 12, (1, 3)), (97, 33, 50, 5, (3, 2)),
+                                          (150, 256, 520, 6, (4, 2)), (64, 288, 512, 4, (1, 1)),
+                                          (120, 48, 64, 16, (4, 1))])
+def test_grid2d_fused_broadcast_bitwise(m, n, s, p, grid):
+    """The 2-D decomposition with the piece broadcasts fused into the owners'
+    K1 (routed stores into every group member's stage buffer; ranks emulated
+    in lockstep on one GPU): each block equals tprod_fast bitwise, twice
+    (the row tables are reused)."""
+    import torch
+    from paper_2212_14318_b200.distributed import Grid2DTProduct, emulate_grid_fused
+    a = qt.gen_random_tensor(m, n, p, 63)
+    b = qt.gen_random_tensor(n, s, p, 64)
+    want = qt.tprod_fast(a, b)
+    world = grid[0] * grid[1]
+    ranks = [Grid2DTProduct(m, n, s, p, r, world, "cuda:0", grid=grid) for r in range(world)]
+    for g in ranks:
+        g.load_a(a.t1, a.t2)  # owned pieces only: the rest arrives through the fused stores
+        g.load_b(b.t1, b.t2)
+    for _ in range(2):
+        for g in ranks:
+            g.c.fill_(float("nan"))
+        emulate_grid_fused(ranks)
+        torch.cuda.synchronize()
+        for g in ranks:
+            c1, c2 = g.result()
+            assert bits_equal(c1, want.t1[:, g.r0:g.r1, g.c0:g.c1]), (grid, g.rank)
+            assert bits_equal(c2, want.t2[:, g.r0:g.r1, g.c0:g.c1]), (grid, g.rank)
