@@ -170,10 +170,74 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
   };
 
   // 2) B chunks: chunk j is uploaded by device owner(j) = j mod ndev (so each
-  //    device moves ~1/ndev of B over its own PCIe link) and broadcast from it
-  //    (one NCCL group per chunk)
+  //    device moves ~1/ndev of B over its own PCIe link).  Fused form (every
+  //    device pair has peer access; QTB_MULTI_FUSED=0 turns it off): the owner
+  //    transforms the chunk once and K1's stores put each frequency row of B̂
+  //    straight into every device's chunk buffer over NVLink
+  //    (qt_qfft3_conj_f64_device_routed_n) — the broadcast and the replicated
+  //    K1 of the chunk disappear.  Otherwise the raw chunk is broadcast (one
+  //    NCCL group per chunk) and every device transforms it.
+  bool fused = qt_fft_routable(p) == 1 && [] {
+    const char* v = getenv("QTB_MULTI_FUSED");
+    return !(v && *v == '0');
+  }();
+  for (int a = 0; a < ndev && fused; ++a)
+    for (int b = 0; b < ndev && fused; ++b) {
+      if (a == b) continue;
+      int ok = 0;
+      if (cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]) != cudaSuccess || !ok) {
+        fused = false;
+        break;
+      }
+      cudaSetDevice(devices[a]);
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(devices[b], 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) fused = false;
+      (void)cudaGetLastError();
+    }
+  std::vector<void*> tabs;  // per chunk: device row tables (in the owner's memory)
   std::vector<std::vector<cudaEvent_t>> arrived(ndev, std::vector<cudaEvent_t>(NJ, nullptr));
-  for (uint64_t j = 0; j < NJ && !rc; ++j) {
+  for (uint64_t j = 0; j < NJ && !rc && fused; ++j) {
+    const uint64_t cols = chunk_cols(j);
+    const int own = (int)(j % (uint64_t)ndev);
+    cudaSetDevice(st[own].dev);
+    const size_t pitch = s * cx, width = cols * cx;
+    if (cudaMemcpy2DAsync(chunk_ptr(own, j, 0), width, b1 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[own].comm) ||
+        cudaMemcpy2DAsync(chunk_ptr(own, j, 1), width, b2 + 2 * j * Q, pitch, width, p * n, cudaMemcpyHostToDevice,
+                          st[own].comm)) {
+      rc = QT_ECUDA;
+      break;
+    }
+    // row tables [plane][device][frequency]: frequency k of device g's chunk j
+    std::vector<double*> h(2 * (size_t)ndev * p);
+    for (int pl = 0; pl < 2; ++pl)
+      for (int g = 0; g < ndev; ++g)
+        for (uint64_t k = 0; k < p; ++k) h[((size_t)pl * ndev + g) * p + k] = chunk_ptr(g, j, pl) + 2 * k * n * cols;
+    double** dt = nullptr;
+    if (cudaMallocAsync((void**)&dt, h.size() * sizeof(double*), st[own].comm) != cudaSuccess ||
+        cudaMemcpyAsync(dt, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, st[own].comm) != cudaSuccess ||
+        cudaStreamSynchronize(st[own].comm) != cudaSuccess) {  // (h is a host temporary)
+      rc = QT_ECUDA;
+      break;
+    }
+    tabs.push_back(dt);
+    // in place on the owner: each tube tile is read whole before it is written
+    rc = qt_qfft3_conj_f64_device_routed_n(chunk_ptr(own, j, 0), chunk_ptr(own, j, 1), dt, dt + (size_t)ndev * p,
+                                           ndev, n, cols, p, st[own].comm);
+    if (rc) break;
+    cudaEvent_t done;
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    cudaEventRecord(done, st[own].comm);
+    for (int g = 0; g < ndev; ++g) arrived[g][j] = g == own ? done : nullptr;
+    for (int g = 0; g < ndev; ++g)
+      if (g != own) {  // every device waits on the owner's event (cross-device waits are legal in one process)
+        cudaSetDevice(st[g].dev);
+        cudaEventCreateWithFlags(&arrived[g][j], cudaEventDisableTiming);
+        cudaStreamWaitEvent(st[g].comm, done, 0);
+        cudaEventRecord(arrived[g][j], st[g].comm);
+      }
+  }
+  for (uint64_t j = 0; j < NJ && !rc && !fused; ++j) {
     const uint64_t cols = chunk_cols(j);
     const int own = (int)(j % (uint64_t)ndev);
     cudaSetDevice(st[own].dev);
@@ -222,15 +286,18 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     for (uint64_t j = 0; j < NJ && r == QT_OK; ++j) {
       const uint64_t cols = chunk_cols(j);
       cudaStreamWaitEvent(d.comp, arrived[g][j], 0);
-      r = qt_qfft3_conj_f64_device(chunk_ptr(g, j, 0), chunk_ptr(g, j, 1), bhat_ptr(g, 0), bhat_ptr(g, 1), n, cols,
-                                   p, d.comp);
+      // fused: chunk j already holds B̂ (stored by its owner's K1)
+      const double* bh1 = fused ? chunk_ptr(g, j, 0) : bhat_ptr(g, 0);
+      const double* bh2 = fused ? chunk_ptr(g, j, 1) : bhat_ptr(g, 1);
+      if (!fused)
+        r = qt_qfft3_conj_f64_device(chunk_ptr(g, j, 0), chunk_ptr(g, j, 1), bhat_ptr(g, 0), bhat_ptr(g, 1), n,
+                                     cols, p, d.comp);
       if (r == QT_OK && plan)
-        r = qt_int8_plan_multiply(plan, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q, C2 + 2 * j * Q, cols, cols, s,
-                                  n * cols, rows[g] * s, d.comp);
+        r = qt_int8_plan_multiply(plan, bh1, bh2, C1 + 2 * j * Q, C2 + 2 * j * Q, cols, cols, s, n * cols,
+                                  rows[g] * s, d.comp);
       else if (r == QT_OK)
-        r = qt_spectral_product_f64_device_ld_algo(Ah1, Ah2, bhat_ptr(g, 0), bhat_ptr(g, 1), C1 + 2 * j * Q,
-                                                   C2 + 2 * j * Q, rows[g], n, cols, p, cols, s, n * cols,
-                                                   rows[g] * s, algo, d.comp);
+        r = qt_spectral_product_f64_device_ld_algo(Ah1, Ah2, bh1, bh2, C1 + 2 * j * Q, C2 + 2 * j * Q, rows[g], n,
+                                                   cols, p, cols, s, n * cols, rows[g] * s, algo, d.comp);
     }
     if (plan) {
       const int dr = qt_int8_plan_destroy(plan, d.comp);
@@ -252,6 +319,12 @@ int qt_tprod_f64_multi(const double* a1, const double* a2, const double* b1, con
     for (int g = 0; g < ndev; ++g) rc = rc ? rc : st[g].rc;
   }
 
+  for (uint64_t j = 0; j < tabs.size(); ++j) {  // row tables: on chunk j's owner, freed after its stream drains
+    const int own = (int)(j % (uint64_t)ndev);
+    cudaSetDevice(st[own].dev);
+    cudaFreeAsync(tabs[j], st[own].comm);
+    cudaStreamSynchronize(st[own].comm);
+  }
   for (int g = 0; g < ndev; ++g) {
     DevState& d = st[g];
     if (!d.comp) continue;

@@ -338,11 +338,17 @@ def test_linearity_at_full_size():
     assert O.rel_frob_error(as_pair(lhs), (r1.t1 + r2.t1, r1.t2 + r2.t2)) <= 1e-13
 
 
-@pytest.mark.parametrize("m,n,s,p", [(40, 24, 20, 12), (130, 33, 70, 16), (300, 64, 200, 64), (17, 16, 16, 4096)])
-def test_multi_driver_single_device_matches(m, n, s, p):
-    """qt_tprod_f64_multi on one device runs the whole NCCL pipeline (column-
-    chunked ncclBroadcast of B, per-chunk K1 + strided K2, K3) and must equal
-    the single-GPU host path bitwise."""
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("m,n,s,p", [(40, 24, 20, 12), (130, 33, 70, 16), (300, 64, 200, 64), (17, 16, 16, 4096),
+                                     (64, 256, 512, 4)])
+def test_multi_driver_single_device_matches(m, n, s, p, fused, monkeypatch):
+    """qt_tprod_f64_multi on one device runs the whole pipeline — column chunks
+    of B transformed once by their owner and stored into every device's chunk
+    buffer by K1's routed stores (fused, peer access), or broadcast raw with
+    ncclBroadcast and transformed per device — then strided K2 and K3; it must
+    equal the single-GPU host path bitwise (the last shape takes the int8
+    stage 2 through a reused plan; p = 4096 is never fused)."""
+    monkeypatch.setenv("QTB_MULTI_FUSED", fused)
     a = qt.gen_random_tensor(m, n, p, 8)
     b = qt.gen_random_tensor(n, s, p, 9)
     c = qt.tprod_fast(a, b)
