@@ -5,11 +5,14 @@
 //   * rows of A and C are split into contiguous slabs of ceil(m/G) rows — row i
 //     of C depends only on row i of A and all of B, so slabs are independent;
 //   * B is the only exchange: column chunk j is uploaded by device j mod G
-//     (each device moves ~1/G of B over its own PCIe link) and broadcast from
-//     it over NVLink / NVSwitch with ncclBroadcast on a communication stream; every device's compute stream
-//     waits only for the chunk it needs, transforms it (K1) and multiplies it
-//     into the matching columns of its C slab (strided K2), so the broadcast of
-//     chunk j+1 overlaps the compute of chunk j;
+//     (each device moves ~1/G of B over its own PCIe link); with peer access
+//     the owner transforms it once and K1's routed stores write B̂ into every
+//     device's chunk buffer over NVLink (the broadcast fused into the
+//     transform), else it is broadcast raw with ncclBroadcast on a
+//     communication stream and every device transforms it; each compute
+//     stream waits only for the chunk it needs and multiplies it into the
+//     matching columns of its C slab (strided K2), so the transfer of chunk
+//     j+1 overlaps the compute of chunk j;
 //   * one inverse transform (K3) per slab, then the slab goes back to the host.
 // Every element is computed with the same kernels and arithmetic as the
 // single-GPU path, so the result is bitwise identical for every G (and equal to
