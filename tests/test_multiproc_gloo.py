@@ -403,3 +403,44 @@ def test_freq_parallel_routing_tables(m, n, s, p, world):
     for x in ranks:
         r0, r1 = shard.row_slab(m, world, x.rank)
         assert np.array_equal(x.c.numpy().view(np.uint64), want[:, :, r0:r1]), x.rank
+
+
+@pytest.mark.parametrize("m,n,s,p,grid", [(9, 5, 40, 6, (2, 2)), (9, 5, 40, 6, (1, 2)), (13, 4, 50, 5, (3, 2)),
+                                          (12, 3, 33, 4, (4, 1)), (7, 6, 20, 3, (1, 1))])
+def test_grid2d_fused_broadcast_tables(m, n, s, p, grid):
+    """The row tables of the 2-D decomposition's fused broadcasts
+    (Grid2DTProduct.set_peers): every owner's transformed piece (the oracle's
+    qfft3_conj), stored row by row to the addresses its tables give (a
+    memmove per destination standing in for the routed K1 stores), leaves in
+    every rank exactly the Â block and B̂ pieces it needs, bitwise."""
+    import ctypes
+    import oracle as O
+    from paper_2212_14318_b200 import distributed
+    A = O.gen_random_tensor(m, n, p, 45)
+    B = O.gen_random_tensor(n, s, p, 46)
+    Ah = O.qfft3_conj(A)
+    Bh = O.qfft3_conj(B)
+    world = grid[0] * grid[1]
+    ranks = [distributed.Grid2DTProduct(m, n, s, p, r, world, device="cpu", grid=grid) for r in range(world)]
+    bases = [x.stage_buffer.data_ptr() for x in ranks]
+    for x in ranks:
+        x.stage_buffer.fill_(float("nan"))
+    for x in ranks:
+        x.set_peers(bases)
+        for (kind, k), (tab, nd) in x.tables.items():
+            lo, hi, _ = (x.apieces if kind == "a" else x.bpieces)[k]
+            src = [np.ascontiguousarray(h[:, lo:hi]) for h in Ah] if kind == "a" else \
+                [np.ascontiguousarray(h[:, :, lo:hi]) for h in Bh]
+            for pl in (0, 1):
+                for d in range(nd):
+                    for f in range(p):
+                        row = src[pl][f]
+                        ctypes.memmove(int(tab[pl][d * p + f]), row.ctypes.data, row.nbytes)
+    for x in ranks:
+        ah = x.ah.numpy().view(np.complex128)
+        for pl in (0, 1):
+            assert np.array_equal(ah[pl].view(np.uint64), Ah[pl][:, x.r0:x.r1].view(np.uint64)), (grid, x.rank)
+        for k, (lo, hi, _) in enumerate(x.bpieces):
+            bh = x.bh[k].numpy().view(np.complex128)
+            for pl in (0, 1):
+                assert np.array_equal(bh[pl].view(np.uint64), Bh[pl][:, :, lo:hi].view(np.uint64)), (grid, x.rank, k)
