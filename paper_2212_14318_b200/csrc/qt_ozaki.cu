@@ -1174,7 +1174,7 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   const bool pipe = B.all && env_int("QTB_OZAKI_PIPE", 1) != 0;
   const uint64_t nbuf = pipe ? 2 : 1;
   const uint64_t ps = B.ns ? (uint64_t)B.ns : p;  // slots [B.s0, B.s0 + ps) of the p
-  uint64_t F = B.all ? batch_slots(ps, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 6144)) : B.nslots;
+  uint64_t F = B.all ? batch_slots(ps, per_slot * nbuf, env_mb("QTB_OZAKI_WS_MB", 3072)) : B.nslots;
   // at least 4 batches when pipelining, so residues/CRT have a GEMM to hide behind
   if (pipe && ps >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((ps + 3) / 4 + 1) & ~uint64_t(1)));
   const uint64_t nbatch = (ps + F - 1) / F;
@@ -1355,7 +1355,7 @@ cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, 
   B.ns = (int)p;
   B.cbase = -1;
   B.all = require_all || per_b * p <= env_mb("QTB_OZAKI_B_MB", 24576);
-  B.nslots = B.all ? (int)p : (int)batch_slots(p, a_slot_bytes(m, n, s) + per_b, env_mb("QTB_OZAKI_WS_MB", 6144));
+  B.nslots = B.all ? (int)p : (int)batch_slots(p, a_slot_bytes(m, n, s) + per_b, env_mb("QTB_OZAKI_WS_MB", 3072));
   if ((uint64_t)B.nslots * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
   const size_t bytes = (size_t)oz::kQ * B.nslots * 2 * pad_cols(s) * 4 * n;
   if ((e = cudaMallocAsync(&B.res, bytes + (size_t)B.nslots * pad_cols(s) * sizeof(int), stream)) != cudaSuccess)
