@@ -168,13 +168,13 @@ def time_reference(cfg, a, b, tile: int, threads: int):
     tile is bitwise the matching block of the reference's full result (rows
     of C depend only on rows of A, columns only on columns of B), so
     (tile fraction of F_eff) / wall time is the reference's throughput on the
-    workload with all host cores busy."""
+    workload with `threads` host cores busy.  a, b: (t1, t2) host planes."""
     import oracle as O
     tiles, total = reference_tiles(cfg, tile, threads)
     jobs = []
     for (r0, r1, c0, c1) in tiles:
-        at = (np.ascontiguousarray(a.t1[:, r0:r1, :]), np.ascontiguousarray(a.t2[:, r0:r1, :]))
-        bt = (np.ascontiguousarray(b.t1[:, :, c0:c1]), np.ascontiguousarray(b.t2[:, :, c0:c1]))
+        at = (np.ascontiguousarray(a[0][:, r0:r1, :]), np.ascontiguousarray(a[1][:, r0:r1, :]))
+        bt = (np.ascontiguousarray(b[0][:, :, c0:c1]), np.ascontiguousarray(b[1][:, :, c0:c1]))
         jobs.append((at, bt))
     th = [threading.Thread(target=O.ref_tprod_fast, args=j) for j in jobs]
     t0 = time.perf_counter()
@@ -185,14 +185,54 @@ def time_reference(cfg, a, b, tile: int, threads: int):
     wall = time.perf_counter() - t0
     frac = sum((r1 - r0) * (c1 - c0) for (r0, r1, c0, c1) in tiles) / float(cfg.m * cfg.s)
     gflops = frac * cfg.flops_eff / wall / 1e9
-    sample = (f"{len(tiles)} tiles of {tiles[0][1] - tiles[0][0]} rows x {tiles[0][3] - tiles[0][2]} cols "
+    sample = (f"{len(tiles)} tile(s) of {tiles[0][1] - tiles[0][0]} rows x {tiles[0][3] - tiles[0][2]} cols "
               f"({frac * 100:.3f}% of C), one tile per thread, reference tprod_fast unmodified")
-    return gflops, wall, sample
+    return gflops, wall, sample, len(tiles)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_reference(cfg, a, b, tile: int, threads: int):
+    """The reference's CPU path on this host: all cores (tile-parallel) and
+    one core (one tile, one thread), plus the CPU model."""
+    g, w, sample, used = time_reference(cfg, a, b, tile, threads)
+    g1, w1, sample1, _ = time_reference(cfg, a, b, tile, 1)
+    return {"value": g, "unit": "GFLOP/s", "cores": used, "kind": "reference", "sample": sample, "wall_s": w,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "single_core": {"value": g1, "unit": "GFLOP/s", "cores": 1, "sample": sample1, "wall_s": w1}}
+
+
+def load_configs():
+    """The BASELINE config table (paper_2212_14318_b200/configs.py) loaded by
+    path: standalone, so the reference arm never imports the product package
+    or loads its library."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("qt_bench_configs",
+                                                  os.path.join(ROOT, "paper_2212_14318_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # (dataclasses resolve annotations through sys.modules)
+    spec.loader.exec_module(mod)
+    return mod.CONFIGS
+
+
+def config_dict(cfg):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    return {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p}
 
 
 def auto_tile(cfg):
     # ~10-25 s of single-thread reference work per tile on a ~3 GHz Xeon
-    return {1: 32, 2: 128, 3: 16, 4: 64, 5: 128}.get(cfg.idx, 64)
+    return {1: 8, 2: 128, 3: 16, 4: 64, 5: 128}.get(cfg.idx, 64)
 
 
 def host_inputs(cfg, pinned: bool, need_b: bool = True):
@@ -224,6 +264,11 @@ def host_inputs(cfg, pinned: bool, need_b: bool = True):
 
 
 def run_reference(args, cfg):
+    """The reference's own CPU tprod_fast (oracle/_ref, compiled from
+    /root/reference's sources, unmodified) on this host's cores.  Inputs come
+    from the oracle's generators (the reference's gen_random_tensor and the
+    restated normal / pure-quaternion ones) — this arm imports neither the
+    product package nor its library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -232,27 +277,33 @@ def run_reference(args, cfg):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqtref.so not built "
                           "(make -C oracle ref needs /root/reference)"}))
         return 0
-    a, b, _ = host_inputs(cfg, pinned=False)
+    sa, sb = cfg.seeds()
+    a = O.gen_tensor(cfg.dist_a, cfg.m, cfg.n, cfg.p, sa, cfg.scale_a)
+    b = O.gen_tensor(cfg.dist_b, cfg.n, cfg.s, cfg.p, sb, cfg.scale_b)
     threads = os.cpu_count() or 1
     tile = args.cpu_tile or auto_tile(cfg)
     for _ in range(args.warmup):
         time_reference(cfg, a, b, max(8, tile // 4), threads)
     vals, walls = [], []
     for _ in range(args.steps):
-        g, w, sample = time_reference(cfg, a, b, tile, threads)
+        g, w, sample, used = time_reference(cfg, a, b, tile, threads)
         vals.append(g)
         walls.append(w)
     value = statistics.median(vals)
+    g1, w1, sample1, _ = time_reference(cfg, a, b, tile, 1)
     line = {
         "impl": "reference",
         "metric": "T-product throughput (effective fp64 GFLOP/s)",
         "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, reference generator)",
-        "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                   "parallelism": f"{threads} host threads, tile-parallel"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; reference generator / SURVEY §8d distributions)",
+        "config": config_dict(cfg),
+        "parallelism": f"{used} host threads, tile-parallel (one (row x column) tile of C per thread)",
+        "flops_eff_per_step": cfg.flops_eff,
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": used, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                         "single_core": {"value": g1, "unit": "GFLOP/s", "cores": 1, "sample": sample1,
+                                         "wall_s": w1}},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -714,10 +765,8 @@ def run_ours(args, cfg):
     if rank == 0 and not sharded_mode and not args.no_cpu_baseline:
         import oracle as O
         if O.ref_available():
-            threads = os.cpu_count() or 1
-            g, w, sample = time_reference(cfg, a, b, args.cpu_tile or auto_tile(cfg), threads)
-            cpu = {"value": g, "unit": "GFLOP/s", "cores": threads, "kind": "reference", "sample": sample,
-                   "wall_s": w}
+            cpu = cpu_reference(cfg, (a.t1, a.t2), (b.t1, b.t2), args.cpu_tile or auto_tile(cfg),
+                                os.cpu_count() or 1)
 
     if rank == 0:
         line = {
@@ -731,18 +780,15 @@ def run_ours(args, cfg):
                            "fp64 throughout (tube FFTs; stage 2 on the fp64 DMMA tensor pipe)"),
             "accuracy": accuracy,
             "fp64_dmma_path": dmma_path,
-            "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "s": cfg.s, "p": cfg.p,
-                       "parallelism": ((f"freq{world}(frequency slots; rows of A, B, C for the tube FFTs)"
-                                        + ("+exchange fused into K1 stores / K3 loads (symmetric memory)"
-                                           if exchange_kind == "fused" else "+NCCL point-to-point exchange")
-                                        if mode == "freq" else
-                                        f"grid{sharded.gr}x{sharded.gc}(rows x cols of C)"
-                                        + ("+piece broadcasts fused into the owners' K1 stores (symmetric memory)"
-                                           if exchange_kind == "fused" else "+NCCL piece broadcasts"))
-                                       if sharded_mode else f"rows{world}")
-                       + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
-                       "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
-                       "flops_eff_per_step": cfg.flops_eff},
+            "config": config_dict(cfg),
+            "parallelism": ((f"freq{world}(frequency slots; rows of A, B, C for the tube FFTs)"
+                             + ("+exchange fused into K1 stores / K3 loads (symmetric memory)"
+                                if exchange_kind == "fused" else "+NCCL point-to-point exchange")
+                             if mode == "freq" else "?")
+                            if sharded_mode else f"rows{world}")
+            + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
+            "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
+            "flops_eff_per_step": cfg.flops_eff,
             "roofline": roof,
             "stages": stages,
             "cpu_baseline": cpu,
@@ -759,8 +805,7 @@ def run_ours(args, cfg):
 
 def main():
     args = parse_args()
-    from paper_2212_14318_b200.configs import CONFIGS
-    cfg = CONFIGS[args.config]
+    cfg = load_configs()[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define QT_B200_ABI_VERSION 1
+#define QT_B200_ABI_VERSION 2
 
 enum qt_status {
   QT_OK = 0,
@@ -174,18 +174,15 @@ int qt_spectral_product_f64_device_ld_algo(const double* ahat1, const double* ah
                                            uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                            int algo, void* stream);
 
-/* Exact-int8 stage 2 against a fixed Â, for callers that feed B̂ in column
- * chunks (the chunked multi-GPU pipeline): the 15 modular residues of Â are
- * built once by qt_int8_plan_create and reused by every
- * qt_int8_plan_multiply (same strides as qt_spectral_product_f64_device_ld;
- * Â must stay valid until qt_int8_plan_destroy).  Bitwise identical to one
- * qt_spectral_product_f64_device_ld_algo(..., QT_GEMM_INT8_EXACT) call on the
- * whole B̂.  Requires n % 32 == 0 and n <= 8192. */
-int qt_int8_plan_create(const double* ahat1, const double* ahat2, uint64_t m, uint64_t n, uint64_t p,
-                        void* stream, void** plan);
-int qt_int8_plan_multiply(void* plan, const double* bhat1, const double* bhat2, double* chat1, double* chat2,
-                          uint64_t s, uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream);
-int qt_int8_plan_destroy(void* plan, void* stream);
+/* Accuracy guard of the int8 stage 2: before anything is
+ * rounded every contraction index j of frequency pair (k, p-k) is balanced by
+ * an exact power of two (row j of B̂ scaled to a maximum in [1/2, 1), column j
+ * of Â by the inverse), and after the CRT each pair's rigorous error bound is
+ * compared with its |Ĉ|: pairs whose relative Frobenius error cannot be
+ * certified below 2^-42 ($QTB_OZAKI_GUARD_LOG2) are recomputed by the fp64
+ * DMMA kernels.  This counter is the number of pairs sent to DMMA so far on
+ * the current device (tests; $QTB_OZAKI_GUARD=force sends every pair). */
+uint64_t qt_int8_guard_fallbacks(void);
 
 /* Frequency slots (multi-GPU plumbing; no reference counterpart — the
  * reference's tprod_fast is single-process, tproduct.cpp:75-111).  Stage 2
@@ -198,10 +195,13 @@ int qt_slot_frequency(uint64_t p, uint64_t slot);
  * frequency-parallel multi-GPU driver: one range per rank).  B̂ (nslots, n, s),
  * and the Â (nslots, m, n) / Ĉ (nslots, m, s) of every multiply, hold slice t
  * = slot slot0 + t (two complex128 planes each, dense).  Neither end of the
- * range may split a pair (an odd boundary below 2 * ((p - 1) / 2)).  `nonfinite` is a device
- * int the caller zeroes: it becomes non-zero if Â or B̂ held an inf/NaN, and
- * then Ĉ is NOT written (the caller must use the DMMA path for that product).
- * Bitwise identical to the same slots of a full-range int8 product. */
+ * range may split a pair (an odd boundary below 2 * ((p - 1) / 2)).  B̂ must stay
+ * valid until qt_int8_slots_destroy (the fp64 fallback reads it).  Non-finite
+ * inputs and pairs the accuracy guard does not certify are recomputed by the
+ * fp64 DMMA kernels on the compact tensors, as in the full-range product;
+ * `nonfinite` (optional device int) receives 1 after a multiply whose Â or B̂
+ * held an inf/NaN.  Bitwise identical to the same slots of a full-range int8
+ * product. */
 int qt_int8_slots_create(const double* bhat1, const double* bhat2, uint64_t n, uint64_t s, uint64_t p, int slot0,
                          int nslots, int* nonfinite, void* stream, void** handle);
 int qt_int8_slots_multiply(void* handle, const double* ahat1, const double* ahat2, uint64_t m, double* chat1,

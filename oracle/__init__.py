@@ -41,6 +41,7 @@ def _load_oracle():
         L.orc_derive_seed.argtypes = [_u64, _u64]
         for nm, args in {
             "orc_gen_random_tensor": [_u64, _u64, _u64, _u64, _p, _p],
+            "orc_gen_tensor": [ctypes.c_int, _u64, _u64, _u64, _u64, ctypes.c_double, _p, _p],
             "orc_rng_sym_stream": [_u64, _u64, _p],
             "orc_rng_u64_stream": [_u64, _u64, _p],
             "orc_dft_vec_naive": [_p, _u64, _p],
@@ -119,6 +120,17 @@ def gen_random_tensor(m, n, p, seed):
     t1 = np.empty((p, m, n), np.complex128)
     t2 = np.empty((p, m, n), np.complex128)
     _chk(_load_oracle().orc_gen_random_tensor(m, n, p, seed, t1.ctypes.data, t2.ctypes.data), "gen_random_tensor")
+    return t1, t2
+
+
+def gen_tensor(dist: int, m, n, p, seed, scale: float = 1.0):
+    """The BASELINE input distributions (0 uniform = gen_random_tensor,
+    1 normal, 2 pure-quaternion RGB), restated for the reference arm of
+    bench.py; bitwise equal to the product library's qt_gen_tensor_f64."""
+    t1 = np.empty((p, m, n), np.complex128)
+    t2 = np.empty((p, m, n), np.complex128)
+    _chk(_load_oracle().orc_gen_tensor(int(dist), m, n, p, seed, ctypes.c_double(scale), t1.ctypes.data,
+                                       t2.ctypes.data), "gen_tensor")
     return t1, t2
 
 

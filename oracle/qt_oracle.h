@@ -10,6 +10,8 @@ extern "C" {
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_ENOMEM = 3 };
 uint64_t orc_derive_seed(uint64_t base, uint64_t stream);
 int orc_gen_random_tensor(uint64_t m, uint64_t n, uint64_t p, uint64_t seed, double* t1, double* t2);
+int orc_gen_tensor(int dist, uint64_t m, uint64_t n, uint64_t p, uint64_t seed, double scale, double* t1,
+                   double* t2);
 int orc_rng_sym_stream(uint64_t seed, uint64_t count, double* out);
 int orc_rng_u64_stream(uint64_t seed, uint64_t count, uint64_t* out);
 int orc_dft_vec_naive(const double* x, uint64_t n, double* y);

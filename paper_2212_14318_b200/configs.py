@@ -5,15 +5,30 @@ Seeds mirror run_bench (/root/reference/proj/src/bench.cpp:66-69): base seed
 S = 42 (bench.hpp:19); config c uses seedA = derive_seed(S, 2(c-1)) and
 seedB = derive_seed(S, 2(c-1)+1).  The datasets are synthetic by definition
 (BASELINE.json describes distributions, not files).
+
+This module is standalone (no package import, no library): bench.py's
+reference arm loads it by path so that arm never loads the product library.
 """
 from __future__ import annotations
 
 import math
 from dataclasses import dataclass
 
-from . import _native
-
 BASE_SEED = 42
+_M64 = (1 << 64) - 1
+
+
+def derive_seed(base: int, stream: int) -> int:
+    """derive_seed of rng.cpp:15-19 (splitmix64 chain), restated; equal to
+    qt_derive_seed (tests/test_abi.py)."""
+    state, out = base & _M64, 0
+    for _ in range(stream + 1):
+        state = (state + 0x9E3779B97F4A7C15) & _M64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        out = z ^ (z >> 31)
+    return out
 
 
 @dataclass(frozen=True)
@@ -31,7 +46,6 @@ class Config:
     note: str
 
     def seeds(self):
-        from .tproduct import derive_seed
         return derive_seed(BASE_SEED, 2 * (self.idx - 1)), derive_seed(BASE_SEED, 2 * (self.idx - 1) + 1)
 
     # algorithmic work; the same figures the roofline uses
@@ -64,7 +78,7 @@ class Config:
         return self.bytes_tensor(self.m, self.n) + self.bytes_tensor(self.n, self.s) + self.bytes_tensor(self.m, self.s)
 
 
-U, N, P = _native.QT_DIST_UNIFORM_SYM, _native.QT_DIST_NORMAL, _native.QT_DIST_PURE_UNIT
+U, N, P = 0, 1, 2  # QT_DIST_UNIFORM_SYM, QT_DIST_NORMAL, QT_DIST_PURE_UNIT (include/qtensor_b200.h)
 
 CONFIGS = {
     1: Config(1, "cfg1_32x32x32_p16", 32, 32, 32, 16, U, 1.0, U, 1.0,

@@ -809,7 +809,7 @@ static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const doub
   OzakiB B;
   auto a256 = [](size_t x) { return (x + 255) / 256 * 256; };
   // B staging (2 planes) + B̂ (2) + A staging (2 x 2) + Â slab (2 x 2) + C slab (2 x 2) + flag
-  const size_t total = 2 * a256(bpl) * 2 + 4 * a256(stA) * 2 + 4 * a256(stC) + 256;
+  const size_t total = 2 * a256(bpl) * 2 + 4 * a256(stA) * 2 + 4 * a256(stC) + a256(int8_flag_ints(p) * sizeof(int));
   auto cleanup = [&](int code) {
     for (cudaStream_t x : {sin, scomp, sout})
       if (x) cudaStreamSynchronize(x);
@@ -840,11 +840,12 @@ static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const doub
   double* SA[2][2] = {{take(stA), take(stA)}, {take(stA), take(stA)}};
   double* AH[2][2] = {{take(stA), take(stA)}, {take(stA), take(stA)}};
   double* CS[2][2] = {{take(stC), take(stC)}, {take(stC), take(stC)}};
-  int* flag = (int*)take(sizeof(int));
+  int* flag = (int*)take(int8_flag_ints(p) * sizeof(int));
   PhaseTrace tr(hc.st);
 
   // phase 1: B in ~8 chunks per plane, then K1 and the B' residues
-  if ((e = cudaMemsetAsync(flag, 0, sizeof(int), scomp)) != cudaSuccess) return cleanup(cuda_fail(e, "memset"));
+  if ((e = cudaMemsetAsync(flag, 0, int8_flag_ints(p) * sizeof(int), scomp)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "memset"));
   const size_t bchunk = std::max<size_t>(size_t(64) << 20, (bpl + 7) / 8);
   for (int plane = 0; plane < 2; ++plane)
     for (size_t off = 0; off < bpl; off += bchunk)
@@ -903,7 +904,8 @@ static int tprod_host_slabs_ozaki(const double* a1, const double* a2, const doub
     if ((e = ozaki_multiply(B, ah1, ah2, (const double2*)Bh1, (const double2*)Bh2, rows, cc1, cc2, s, rows * s, flag,
                             scomp)) != cudaSuccess)
       return cleanup(cuda_fail(e, "K2 int8 GEMM"));
-    // non-finite inputs: the fp64 DMMA kernels recompute the slab (no-op otherwise)
+    // non-finite inputs / pairs the accuracy guard did not certify: the fp64
+    // DMMA kernels recompute them (no-op otherwise)
     if ((e = dmma_spectral_gemm(ah1, ah2, (const double2*)Bh1, (const double2*)Bh2, cc1, cc2, rows, n, s, p, s, s,
                                 n * s, rows * s, scomp, flag)) != cudaSuccess)
       return cleanup(cuda_fail(e, "K2 fallback"));
@@ -960,89 +962,12 @@ int qt_spectral_product_f64_device_ld(const double* ah1, const double* ah2, cons
 }
 
 namespace {
-struct Int8Plan {
-  OzakiA A;
-  const double2* ah1 = nullptr;
-  const double2* ah2 = nullptr;
-  int* flags = nullptr;  // [0] non-finite in Â (from create), [1] per multiply (Â or B̂ chunk)
-  int device = 0;
-};
-}  // namespace
-
-int qt_int8_plan_create(const double* ah1, const double* ah2, uint64_t m, uint64_t n, uint64_t p, void* stream,
-                        void** plan) {
-  t_err.clear();
-  if (!plan) return fail(QT_EINVAL, "int8 plan: null plan pointer");
-  *plan = nullptr;
-  int rc = check_dims(m, n, 1, p, "int8 plan");
-  if (rc) return rc;
-  if (m == 0 || n == 0 || n % 32 != 0 || n > 8192 || p > 65534)
-    return fail(QT_EINVAL, "int8 plan: needs m > 0, n %% 32 == 0, 0 < n <= 8192 and p <= 65534");
-  int dev = 0;
-  if ((rc = current_device(&dev))) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  Int8Plan* P = new Int8Plan;
-  P->ah1 = (const double2*)ah1;
-  P->ah2 = (const double2*)ah2;
-  P->device = dev;
-  cudaError_t e = cudaMallocAsync(&P->flags, 2 * sizeof(int), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(P->flags, 0, 2 * sizeof(int), st);
-  if (e == cudaSuccess) e = ozaki_prepare_a(P->ah1, P->ah2, m, n, p, P->flags, &P->A, st);
-  if (e != cudaSuccess) {
-    if (P->flags) cudaFreeAsync(P->flags, st);
-    delete P;
-    return cuda_fail(e, "int8 plan: residues of A");
-  }
-  *plan = P;
-  return QT_OK;
-}
-
-int qt_int8_plan_multiply(void* plan, const double* bh1, const double* bh2, double* ch1, double* ch2, uint64_t s,
-                          uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, void* stream) {
-  t_err.clear();
-  Int8Plan* P = (Int8Plan*)plan;
-  if (!P) return fail(QT_EINVAL, "int8 plan: null plan");
-  const uint64_t m = P->A.m, n = P->A.n, p = P->A.p;
-  int rc = check_dims(m, n, s, p, "int8 plan multiply");
-  if (rc) return rc;
-  if (s == 0) return QT_OK;
-  if (ldb < s || ldc < s || bslice < n * ldb || cslice < m * ldc || ldb > kIntMax || ldc > kIntMax)
-    return fail(QT_EINVAL, "int8 plan multiply: leading dimensions smaller than the matrices");
-  cudaStream_t st = (cudaStream_t)stream;
-  int* flag = P->flags + 1;
-  cudaError_t e = cudaMemcpyAsync(flag, P->flags, sizeof(int), cudaMemcpyDeviceToDevice, st);
-  OzakiB B;
-  if (e == cudaSuccess)
-    e = ozaki_prepare_b((const double2*)bh1, (const double2*)bh2, m, n, s, p, ldb, bslice, flag, true, &B, st, true);
-  if (e == cudaSuccess)
-    e = ozaki_multiply_prepared(P->A, B, (double2*)ch1, (double2*)ch2, ldc, cslice, flag, st);
-  if (B.res) {
-    const cudaError_t fe = ozaki_release(B, st);
-    if (e == cudaSuccess) e = fe;
-  }
-  // non-finite inputs: the fp64 DMMA kernels recompute this chunk (no-op otherwise)
-  if (e == cudaSuccess)
-    e = dmma_spectral_gemm(P->ah1, P->ah2, (const double2*)bh1, (const double2*)bh2, (double2*)ch1, (double2*)ch2,
-                           m, n, s, p, ldb, ldc, bslice, cslice, st, flag);
-  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 plan multiply");
-}
-
-int qt_int8_plan_destroy(void* plan, void* stream) {
-  t_err.clear();
-  Int8Plan* P = (Int8Plan*)plan;
-  if (!P) return QT_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = ozaki_release_a(P->A, st);
-  const cudaError_t fe = cudaFreeAsync(P->flags, st);
-  delete P;
-  if (e == cudaSuccess) e = fe;
-  return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 plan destroy");
-}
-
-namespace {
 struct Int8Slots {
   OzakiB B;
   int* nonfinite = nullptr;
+  int* flags = nullptr;  // int8_flag_ints(p): [0] non-finite (sticky), [1 + k] pair k to recompute
+  const double2* bh1 = nullptr;
+  const double2* bh2 = nullptr;
   int device = 0;
 };
 }  // namespace
@@ -1061,7 +986,6 @@ int qt_int8_slots_create(const double* bh1, const double* bh2, uint64_t n, uint6
   *handle = nullptr;
   int rc = check_dims(1, n, s, p, "int8 slots");
   if (rc) return rc;
-  if (!nonfinite) return fail(QT_EINVAL, "int8 slots: null non-finite flag");
   if (n == 0 || s == 0 || n % 32 != 0 || n > 8192 || p > 65534)
     return fail(QT_EINVAL, "int8 slots: needs s > 0, n %% 32 == 0, 0 < n <= 8192 and p <= 65534");
   const uint64_t pair_end = 2 * ((p - 1) / 2);  // slots [0, pair_end) hold pairs (2j, 2j+1)
@@ -1074,9 +998,16 @@ int qt_int8_slots_create(const double* bh1, const double* bh2, uint64_t n, uint6
   Int8Slots* H = new Int8Slots;
   H->nonfinite = nonfinite;
   H->device = dev;
-  cudaError_t e = ozaki_prepare_b_slots((const double2*)bh1, (const double2*)bh2, n, s, p, slot0, nslots, nonfinite,
-                                        &H->B, (cudaStream_t)stream);
+  H->bh1 = (const double2*)bh1;
+  H->bh2 = (const double2*)bh2;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t fb = int8_flag_ints(p) * sizeof(int);
+  cudaError_t e = cudaMallocAsync(&H->flags, fb, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(H->flags, 0, fb, st);
+  if (e == cudaSuccess)
+    e = ozaki_prepare_b_slots((const double2*)bh1, (const double2*)bh2, n, s, p, slot0, nslots, H->flags, &H->B, st);
   if (e != cudaSuccess) {
+    if (H->flags) cudaFreeAsync(H->flags, st);
     delete H;
     return cuda_fail(e, "int8 slots: residues of B");
   }
@@ -1092,9 +1023,17 @@ int qt_int8_slots_multiply(void* handle, const double* ah1, const double* ah2, u
   int rc = check_dims(m, H->B.n, H->B.s, H->B.p, "int8 slots multiply");
   if (rc) return rc;
   if (m == 0) return QT_OK;
-  const uint64_t s = H->B.s;
+  const uint64_t n = H->B.n, s = H->B.s, p = H->B.p;
+  cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = ozaki_multiply(H->B, (const double2*)ah1, (const double2*)ah2, nullptr, nullptr, m, (double2*)ch1,
-                                 (double2*)ch2, s, m * s, H->nonfinite, (cudaStream_t)stream);
+                                 (double2*)ch2, s, m * s, H->flags, st);
+  // non-finite inputs / uncertified pairs: the fp64 DMMA kernels recompute
+  // them on the compact slot tensors (no-op otherwise)
+  if (e == cudaSuccess)
+    e = dmma_spectral_gemm_slots((const double2*)ah1, (const double2*)ah2, H->bh1, H->bh2, (double2*)ch1,
+                                 (double2*)ch2, m, n, s, p, H->B.s0, H->B.ns, st, H->flags);
+  // the caller's flag reports non-finite inputs (the result is the DMMA one then)
+  if (e == cudaSuccess && H->nonfinite) e = cudaMemcpyAsync(H->nonfinite, H->flags, sizeof(int), cudaMemcpyDeviceToDevice, st);
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 slots multiply");
 }
 
@@ -1102,10 +1041,14 @@ int qt_int8_slots_destroy(void* handle, void* stream) {
   t_err.clear();
   Int8Slots* H = (Int8Slots*)handle;
   if (!H) return QT_OK;
-  const cudaError_t e = ozaki_release(H->B, (cudaStream_t)stream);
+  cudaError_t e = ozaki_release(H->B, (cudaStream_t)stream);
+  const cudaError_t fe = cudaFreeAsync(H->flags, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = fe;
   delete H;
   return e == cudaSuccess ? QT_OK : cuda_fail(e, "int8 slots destroy");
 }
+
+uint64_t qt_int8_guard_fallbacks(void) { return int8_guard_fallbacks(); }
 
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
   (void)m;

@@ -236,6 +236,34 @@ __device__ __forceinline__ PairArgs pair_args(const double2* ah1, const double2*
   return P;
 }
 
+// Work unit u of a launch -> the slices of its pair (ka, kb; ka == kb for a
+// self-paired frequency) and its flag key min(k, p - k).  Frequency mode
+// (s0 < 0): u = k in [0, p/2], slices are frequencies.  Compact mode: the
+// operands hold the frequency slots [s0, s0 + ns) (slice t = slot s0 + t) and
+// u walks that range's pair / self-paired units (qt_int8_slots_*).
+struct PairMap {
+  int s0 = -1, ns = 0;
+};
+__device__ __forceinline__ void map_unit(int u, const PairMap& M, int p, int& ka, int& kb, int& key) {
+  if (M.s0 < 0) {
+    ka = u;
+    kb = (p - u) % p;
+    key = u;
+    return;
+  }
+  int sa, sb;
+  unit_slots(u, M.s0, M.ns, p, sa, sb);
+  ka = sa - M.s0;
+  kb = sb - M.s0;
+  const int f = slot_frequency(sa, p);
+  key = min(f, p - f);
+}
+// int8 fallback: the CTA's pair runs only if the inputs were non-finite or the
+// accuracy guard flagged it (only_if[0] / only_if[1 + key]); nullptr: always
+__device__ __forceinline__ bool skip_unit(const int* only_if, int key) {
+  return only_if != nullptr && only_if[0] == 0 && only_if[1 + key] == 0;
+}
+
 // Persistent variant for many tiny slices whose whole K fits one stage
 // (n <= BK, e.g. m = n = s = 16 with p = 4096): each CTA walks work items
 // (pair, tile) with a two-deep cp.async ring ACROSS items, so the loads of item
@@ -248,22 +276,32 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_small_persistent_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                    const double2* __restrict__ bh1, const double2* __restrict__ bh2,
                                    double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
-                                   int ldb, int ldc, long long bslice, long long cslice, const int* only_if) {
-  if (only_if != nullptr && *only_if == 0) return;  // Ozaki path succeeded (qt_ozaki.cu)
+                                   int ldb, int ldc, long long bslice, long long cslice, const int* only_if,
+                                   PairMap map, int units) {
   extern __shared__ double2 smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int wm = warp % C::WM, wn = warp / C::WM;
   const int ntm = (m + C::BM - 1) / C::BM, ntn = (s + C::BN - 1) / C::BN;
   const long long tiles = (long long)ntm * ntn;
-  const long long items = (long long)(p / 2 + 1) * tiles;
+  const long long items = (long long)units * tiles;
   const size_t amn = (size_t)m * n;
   auto item_args = [&](long long w, int* row0, int* col0) {
-    const int k = (int)(w / tiles);
-    const int t = (int)(w - (long long)k * tiles);
+    const int u = (int)(w / tiles);
+    const int t = (int)(w - (long long)u * tiles);
     *row0 = (t % ntm) * C::BM;
     *col0 = (t / ntm) * C::BN;
-    return pair_args(ah1, ah2, bh1, bh2, ch1, ch2, k, (p - k) % p, amn, (size_t)bslice, (size_t)cslice);
+    int ka, kb, key;
+    map_unit(u, map, p, ka, kb, key);
+    return pair_args(ah1, ah2, bh1, bh2, ch1, ch2, ka, kb, amn, (size_t)bslice, (size_t)cslice);
+  };
+  // int8 fallback: only the flagged pairs' items run (the others are skipped
+  // wholesale; the ring then just prefetches fewer items)
+  auto live = [&](long long w) {
+    if (only_if == nullptr) return true;
+    int ka, kb, key;
+    map_unit((int)(w / tiles), map, p, ka, kb, key);
+    return !skip_unit(only_if, key);
   };
   constexpr int D = C::STAGES;  // ring depth: items prefetched D - 1 ahead
   const long long G = gridDim.x;
@@ -272,7 +310,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 #pragma unroll
   for (int d = 0; d < D - 1; ++d) {
     const long long wd = w + d * G;
-    if (wd < items) {
+    if (wd < items && live(wd)) {
       int lr, lc;
       const PairArgs Pd = item_args(wd, &lr, &lc);
       load_stage<C, false>(smem + d * C::STAGE_ELEMS, Pd, 0, lr, lc, m, n, s, ldb);
@@ -282,7 +320,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
   for (int it = 0; w < items; ++it, w += G) {
     {
       const long long wp = w + (D - 1) * G;
-      if (wp < items) {
+      if (wp < items && live(wp)) {
         int lr, lc;
         const PairArgs Pp = item_args(wp, &lr, &lc);
         load_stage<C, false>(smem + ((it + D - 1) % D) * C::STAGE_ELEMS, Pp, 0, lr, lc, m, n, s, ldb);
@@ -291,6 +329,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     }
     cp_async_wait<D - 1>();
     __syncthreads();
+    if (!live(w)) {  // (block-uniform) nothing was loaded for this item
+      __syncthreads();
+      continue;
+    }
     int r0, c0;
     const PairArgs P = item_args(w, &r0, &c0);
     const double2* sa = smem + (it % D) * C::STAGE_ELEMS;
@@ -328,10 +370,11 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     paired_spectral_gemm_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
                                 const double2* __restrict__ bh1, const double2* __restrict__ bh2,
                                 double2* __restrict__ ch1, double2* __restrict__ ch2, int m, int n, int s, int p,
-                                int pair0, int ldb, int ldc, long long bslice, long long cslice, const int* only_if) {
-  if (only_if != nullptr && *only_if == 0) return;  // Ozaki path succeeded (qt_ozaki.cu)
-  const int k = pair0 + blockIdx.y;
-  const int sg = (p - k) % p;
+                                int pair0, int ldb, int ldc, long long bslice, long long cslice, const int* only_if,
+                                PairMap map) {
+  int k, sg, key;
+  map_unit(pair0 + blockIdx.y, map, p, k, sg, key);
+  if (skip_unit(only_if, key)) return;  // int8 path certified this pair (qt_ozaki.cu)
   const int ntm = (m + C::BM - 1) / C::BM, ntn = (s + C::BN - 1) / C::BN;
   const int bid = blockIdx.x;
   const int per_group = GROUP_M * ntn;
@@ -355,7 +398,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 template <class C>
 cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2, double2* ch1,
                        double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc,
-                       uint64_t bslice, uint64_t cslice, cudaStream_t stream, const int* only_if = nullptr) {
+                       uint64_t bslice, uint64_t cslice, cudaStream_t stream, const int* only_if = nullptr,
+                       PairMap map = PairMap{}) {
   static std::mutex mu;
   static uint64_t done = 0;
   const cudaError_t attr_err = once_per_device(mu, done, [] {
@@ -363,7 +407,7 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
                                 (int)C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const uint64_t npairs = p / 2 + 1;
+  const uint64_t npairs = map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
   // a K that fits one stage (e.g. n <= 16 on the small tile) needs one buffer only
   const uint64_t ktiles = (n + C::BK - 1) / C::BK;
@@ -375,7 +419,7 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
     ProfScope ps(only_if ? "k2_dmma_guard" : "k2_dmma", stream);
     paired_spectral_gemm_kernel<C><<<grid, C::NTHREADS, smem, stream>>>(
         ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)k0, (int)ldb, (int)ldc, (long long)bslice,
-        (long long)cslice, only_if);
+        (long long)cslice, only_if, map);
     ps.stop();
     count_launches(1);
     cudaError_t e = cudaGetLastError();
@@ -399,7 +443,7 @@ template <class C>
 cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
-                                    cudaStream_t stream, const int* only_if = nullptr) {
+                                    cudaStream_t stream, const int* only_if = nullptr, PairMap map = PairMap{}) {
   auto kern = paired_small_persistent_kernel<C>;
   const size_t smem = (size_t)C::STAGES * C::STAGE_ELEMS * 16;
   static std::mutex mu;
@@ -415,12 +459,14 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
   });
   if (attr_err != cudaSuccess) return attr_err;
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
-  const uint64_t items = (p / 2 + 1) * tiles;
+  const uint64_t units = map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
+  const uint64_t items = units * tiles;
+  if (items == 0) return cudaSuccess;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)std::max(1, per_sm) * sms);
   ProfScope ps(only_if ? "k2_dmma_guard" : "k2_dmma", stream);
   kern<<<(unsigned)grid, C::NTHREADS, smem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n, (int)s, (int)p,
                                                        (int)ldb, (int)ldc, (long long)bslice, (long long)cslice,
-                                                       only_if);
+                                                       only_if, map, (int)units);
   ps.stop();
   count_launches(1);
   return cudaGetLastError();
@@ -428,30 +474,46 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
 
 }  // namespace
 
-// DMMA (fp64 tensor-core) paired product; with only_if != nullptr every CTA
-// exits at once unless *only_if != 0 (the Ozaki path's non-finite fallback).
-cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
-                               double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
-                               uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
-                               const int* only_if) {
+// DMMA (fp64 tensor-core) paired product; with an int8 flag array in only_if
+// a CTA runs only for the pairs the int8 path did not certify (qt_ozaki.cu).
+static cudaError_t dmma_impl(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                             double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                             uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
+                             const int* only_if, PairMap map) {
   // Small slices (m, s <= 32): the 64-row tile would waste >= half its DMMAs
   // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
   const bool gauss = gauss_enabled();
   if (m <= 32 && s <= 32) {
     if (n <= (uint64_t)SmallCfg::BK)
       return gauss ? launch_small_persistent<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc,
-                                                            bslice, cslice, stream, only_if)
+                                                            bslice, cslice, stream, only_if, map)
                    : launch_small_persistent<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice,
-                                                       cslice, stream, only_if);
+                                                       cslice, stream, only_if, map);
     return gauss ? launch_cfg<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice,
-                                             stream, only_if)
+                                             stream, only_if, map)
                  : launch_cfg<SmallCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream,
-                                        only_if);
+                                        only_if, map);
   }
   if (gauss)
-    return launch_cfg<GaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream,
-                                only_if);
-  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if);
+    return launch_cfg<GaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if,
+                                map);
+  return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, map);
+}
+
+cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                               double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                               uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
+                               const int* only_if) {
+  return dmma_impl(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, PairMap{});
+}
+
+cudaError_t dmma_spectral_gemm_slots(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                     int s0, int ns, cudaStream_t stream, const int* only_if) {
+  PairMap map;
+  map.s0 = s0;
+  map.ns = ns;
+  return dmma_impl(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, s, s, n * s, m * s, stream, only_if, map);
 }
 
 cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
@@ -466,9 +528,10 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
   // exact int8 tensor-core path (qt_ozaki.cu); the DMMA kernels run only if
   // the inputs held a non-finite value
   int* flag = nullptr;
-  cudaError_t e = cudaMallocAsync(&flag, sizeof(int), stream);
+  const size_t fb = int8_flag_ints(p) * sizeof(int);
+  cudaError_t e = cudaMallocAsync(&flag, fb, stream);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
+  e = cudaMemsetAsync(flag, 0, fb, stream);
   if (e == cudaSuccess)
     e = launch_spectral_gemm_ozaki(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, flag, stream);
   if (e == cudaErrorMemoryAllocation) {

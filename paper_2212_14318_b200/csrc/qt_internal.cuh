@@ -91,10 +91,42 @@ cudaError_t launch_spectral_gemm_ld(const double2* ah1, const double2* ah2, cons
                                     uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice,
                                     cudaStream_t stream, int algo = -1);
 
+// Frequency slots of the stage-2 schedule: slot 2j, 2j+1 hold the pair
+// (j+1, p-j-1); the self-paired 0 and p/2 come last.
+__host__ __device__ __forceinline__ int slot_frequency(int slot, int p) {
+  const int npairs = (p - 1) / 2;
+  if (slot < 2 * npairs) return (slot & 1) ? p - (slot / 2 + 1) : slot / 2 + 1;
+  return slot == 2 * npairs ? 0 : p / 2;
+}
+// Units of a slot range [s0, s0 + ns) that keeps pairs whole: the pairs
+// (2j, 2j+1) below pair_end first, then the self-paired slots (one each).
+__host__ __device__ __forceinline__ int slot_units(int s0, int ns, int p) {
+  const int pe = 2 * ((p - 1) / 2);
+  const int lo = s0 < pe ? s0 : pe, hi = s0 + ns < pe ? s0 + ns : pe;
+  const int np = (hi - lo) / 2;
+  const int from = s0 > pe ? s0 : pe;
+  return np + (s0 + ns > from ? s0 + ns - from : 0);
+}
+__host__ __device__ __forceinline__ void unit_slots(int u, int s0, int ns, int p, int& sa, int& sb) {
+  const int pe = 2 * ((p - 1) / 2);
+  const int lo = s0 < pe ? s0 : pe, hi = s0 + ns < pe ? s0 + ns : pe;
+  const int np = (hi - lo) / 2;
+  if (u < np) {
+    sa = s0 + 2 * u;
+    sb = sa + 1;
+  } else {
+    sa = sb = (s0 > pe ? s0 : pe) + (u - np);
+  }
+}
+
 // Exact int8 tensor-core (Ozaki-II / CRT) evaluation of the same product
-// (qt_ozaki.cu).  *flag (device int, zeroed by the caller) is set to 1 if the
-// inputs hold a non-finite value, in which case C is left untouched.
+// (qt_ozaki.cu).  `flag` is a device int array of int8_flag_ints(p) entries,
+// zeroed by the caller: flag[0] is set to 1 if the inputs hold a non-finite
+// value (C is then left untouched), flag[1 + min(k, p - k)] to 1 if the
+// accuracy guard could not certify pair k (C of that pair is then to be
+// recomputed by dmma_spectral_gemm with only_if = flag).
 enum GemmAlgo { kAlgoAuto = -1, kAlgoDmma = 0, kAlgoOzaki = 1 };
+inline uint64_t int8_flag_ints(uint64_t p) { return p / 2 + 2; }
 bool ozaki_supported(uint64_t n, uint64_t s, uint64_t p);
 // the algorithm a product of this shape uses (callers that split one product
 // into row slabs or column chunks decide once, on the full shape)
@@ -110,6 +142,9 @@ cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, c
 struct OzakiB {
   uint8_t* res = nullptr;
   int* eB = nullptr;
+  double* yl1 = nullptr;  // L1 norms of the scaled B' columns (accuracy guard)
+  int* bdel = nullptr;    // contraction balancing exponents, [p][n] by frequency
+  int* bmin = nullptr;    // smallest column exponent per B' slot (accuracy guard weights)
   uint64_t n = 0, s = 0, p = 0, ldb = 0, bslice = 0;
   int nslots = 0;
   bool all = false;
@@ -131,23 +166,19 @@ cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, co
 cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream);
 cudaError_t ozaki_prepare_b_slots(const double2* bh1, const double2* bh2, uint64_t n, uint64_t s, uint64_t p, int s0,
                                   int ns, int* flag, OzakiB* out, cudaStream_t stream);
-// X' residues of every frequency, prepared once and reused against many B'
-// (column chunks of B: the chunked multi-GPU pipeline, the e2e wavefront)
-struct OzakiA {
-  uint8_t* res = nullptr;
-  int* eA = nullptr;
-  uint64_t m = 0, n = 0, p = 0;
-};
-cudaError_t ozaki_prepare_a(const double2* ah1, const double2* ah2, uint64_t m, uint64_t n, uint64_t p, int* flag,
-                            OzakiA* out, cudaStream_t stream);
-cudaError_t ozaki_multiply_prepared(const OzakiA& A, OzakiB& B, double2* ch1, double2* ch2, uint64_t ldc,
-                                    uint64_t cslice, int* flag, cudaStream_t stream);
-cudaError_t ozaki_release_a(OzakiA& A, cudaStream_t stream);
-// DMMA kernels that run only if *only_if != 0 (nullptr: always)
+// pairs the accuracy guard has sent to the DMMA kernels since load (all devices' counters summed: this device's)
+uint64_t int8_guard_fallbacks();
+// DMMA kernels that run only if *only_if != 0 (nullptr: always); with an
+// int8 flag array (see above) a CTA of pair k runs if flag[0] or flag[1 + k]
 cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
                                const int* only_if);
+// the same on compact slot tensors (slice t = frequency slot s0 + t, the
+// slot range keeping pairs whole; qt_int8_slots_*)
+cudaError_t dmma_spectral_gemm_slots(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                                     double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                                     int s0, int ns, cudaStream_t stream, const int* only_if);
 
 // Definitional product C_k = sum_r A_{(k-r) mod p} (.) B_r (qt_naive.cu).
 cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,

@@ -484,11 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 // Frequencies are processed in slots: slot 2j, 2j+1 hold the pair (j+1,
 // p-j-1); the self-paired 0 and p/2 come last.  A batch is a run of slots with
 // an even start, so a pair never straddles two batches.
-__device__ __forceinline__ int slot_freq(int slot, int p) {
-  const int npairs = (p - 1) / 2;
-  if (slot < 2 * npairs) return (slot & 1) ? p - (slot / 2 + 1) : slot / 2 + 1;
-  return slot == 2 * npairs ? 0 : p / 2;
-}
+__device__ __forceinline__ int slot_freq(int slot, int p) { return slot_frequency(slot, p); }
 
 // Slice of a frequency slot in the operand tensors: the frequency itself, or
 // (compact tensors holding slots [cbase, ...) in slot order) slot - cbase.
@@ -531,14 +527,14 @@ __device__ __forceinline__ uint32_t neg_res(uint32_t r, uint32_t p) { return r ?
 // for p = 256 the packed low byte of 256 - r is -r mod 256.  One operation.
 __device__ __forceinline__ uint32_t neg_op(uint32_t r, uint32_t p) { return p - r; }
 
-__device__ __forceinline__ double block_max(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+__device__ __forceinline__ int block_max_int(int v, int* red) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
   if (lane == 0) red[warp] = v;
   __syncthreads();
   v = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = max(v, red[w]);
   return v;
 }
 
@@ -562,6 +558,95 @@ __device__ __forceinline__ int exp_of(double mx) {
 }
 constexpr double kDblMax = 1.7976931348623157e308;
 constexpr int kNoExp = (int)0xC0C0C0C0;  // no nonzero value seen (cudaMemset byte 0xC0); below every exponent
+// binary exponent E of |v| > 0 finite (|v| < 2^E, |v| >= 2^(E-1)), from the bits
+__device__ __forceinline__ int exp_bits(double v) {
+  const int f = (int)((__double_as_longlong(v) >> 52) & 0x7ff);
+  return f ? f - 1022 : exp_of(v);  // subnormal: frexp
+}
+
+// ------------------------------------------------ contraction balancing
+// X_k Y_k = (X_k D^-1)(D Y_k) for any diagonal D of powers of two along the
+// contraction index, exactly.  Row j of Y_k is B̂1_k[j] (j < n) or B̂2_k[j-n]
+// (and the matching column of X_k multiplies it); one exponent per n-index j
+// and frequency PAIR (k, p-k), shared by both CD parts and both slots so the
+// shared X' of a pair stays valid: d_j = -E_j, E_j the binary exponent of the
+// largest |re|, |im| of row j of B̂1/B̂2 at frequencies k and p-k (over every
+// column).  Each row of D Y then has its maximum in [1/2, 1) and X's column j
+// absorbs the scale, so a contraction index scaled up in A and down in B (or
+// the reverse) — which the per-row / per-column exponents alone would turn into
+// lost low-order bits — is balanced back before anything is rounded.  The
+// balanced values are never formed: each kernel folds d_j into the one
+// power-of-two scale it already applies (exponent arithmetic, so nothing
+// overflows or underflows on the way).  bdel: [p][n] ints, indexed by frequency
+// (decomposition-independent: row slabs, compact slot ranges and the
+// one-shot product see the same d for the same B̂).
+__device__ __forceinline__ int bal_delta(const int* __restrict__ bdel, int k, int n, int j) {
+  return bdel ? __ldg(bdel + (size_t)k * n + j) : 0;
+}
+
+// bdel for the slot units of [f0, f0 + units): one warp per (unit, row j)
+// reads row j of both CD planes at both frequencies of the unit.
+__global__ void __launch_bounds__(256) oz_balance_b_kernel(const double2* __restrict__ b1,
+                                                           const double2* __restrict__ b2, int* __restrict__ bdel,
+                                                           int n, int s, int p, int f0, int ns, uint64_t ldb,
+                                                           uint64_t bslice, int cbase) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + w;
+  if (j >= n) return;
+  int sa, sb;
+  unit_slots(blockIdx.y, f0, ns, p, sa, sb);
+  const int ka = slot_freq(sa, p), kb = slot_freq(sb, p);
+  const int la = slot_slice(sa, p, cbase), lb = slot_slice(sb, p, cbase);
+  int E = kNoExp;
+  for (int t = 0; t < 4; ++t) {
+    const double2* row = (t & 1 ? b2 : b1) + (size_t)(t < 2 ? la : lb) * bslice + (size_t)j * ldb;
+    if (t >= 2 && la == lb) break;
+    constexpr int kU = 4;
+    for (int c0 = lane; c0 < s; c0 += 32 * kU) {
+      double2 y[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = c0 + 32 * u;
+        y[u] = c < s ? __ldcs(row + c) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const double mx = fmax(fabs(y[u].x), fabs(y[u].y));
+        // inf / nan: the colexp pass raises the non-finite flag; any d is fine then
+        if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx));
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) E = max(E, __shfl_xor_sync(0xffffffffu, E, o));
+  if (lane == 0) {
+    const int d = E == kNoExp ? 0 : -E;
+    bdel[(size_t)ka * n + j] = d;
+    bdel[(size_t)kb * n + j] = d;
+  }
+}
+
+// ------------------------------------------------------ accuracy guard
+// The only approximation of the int8 path is rounding the scaled operands to
+// integers (|dx|, |dy| <= 1/2 in scaled units); the integer product and the
+// CRT are exact.  Per real output element, in scaled units,
+//   |err| <= 1/2 ||y''_c||_1 + 1/2 ||x''_r||_1 + K/4 (+ 2^42 CRT weights, + final rounding),
+// with x''_r, y''_c the unrounded scaled row of X (real form, K = 4n) and
+// column of Y (an all-zero row or column is exact: no term).  The residue
+// kernels record those L1 norms (xl1 per X' row, yl1 per B' column) and the
+// smallest row / column exponent of each slot (amin, bmin); the CRT kernel
+// accumulates, per frequency slot, the squared bound and |C|^2 with the
+// element weights 2^-2(e_row - amin) 2^-2(e_col - bmin) <= 1 (the true
+// weights 2^-2(e_row + e_col) up to one common factor), and the guard kernel
+// certifies each pair with sum bound^2 <= tol^2 sum |C|^2 (tol = 2^-42 by
+// default), i.e. a relative Frobenius error of the pair's stage-2 result
+// below tol.  A pair that is not certified (or whose sums under/overflowed)
+// gets flag[1 + min(k, p - k)] and the fp64 DMMA kernels recompute it
+// (qt_gemm.cu, launched behind every int8 product).
+struct GuardAcc {
+  double sb;  // sum of bound^2 * weight
+  double sc;  // sum of |C'|^2 * weight
+};
+__device__ unsigned long long g_guard_fallbacks = 0;  // pairs sent to the DMMA kernels (qt_int8_guard_fallbacks)
 
 // Scale exponent of a row / column with max < 2^E and ||v|| / 2^E = ns (the
 // scaled Euclidean norm, >= 1/2): e = min(53 - E, T - E_ns - E) with
@@ -582,9 +667,12 @@ __device__ __forceinline__ int scale_exponent(int E, double ns) {
 constexpr int kAVec = 4;  // consecutive K elements per thread and store (one 32-bit word)
 __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __restrict__ a1,
                                                            const double2* __restrict__ a2, uint8_t* __restrict__ out,
-                                                           int* __restrict__ eA, int* nonfinite, int m, int n, int p,
-                                                           int f0, int Mp, int F, int cbase, int share_end) {
+                                                           int* __restrict__ eA, double* __restrict__ xl1,
+                                                           int* __restrict__ amin, const int* __restrict__ bdel,
+                                                           int* nonfinite, int m, int n, int p, int f0, int Mp, int F,
+                                                           int cbase, int share_end) {
   __shared__ double red[8];
+  __shared__ int ired[8];
   const int i = blockIdx.x, f = blockIdx.y;
   const int slot = f0 + f;
   const int k = slot_freq(slot, p), sk = (p - k) % p;
@@ -592,36 +680,49 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   const int kq = slot_slice(slot, p, cbase), skq = slot_slice((k == sk) ? slot : (slot ^ 1), p, cbase);
   const double2* P = a1 + ((size_t)kq * m + i) * n;
   const double2* Qr = a2 + ((size_t)skq * m + i) * n;
-  double mx = 0.0;
+  // column j of this row pair multiplies Y rows j and n + j: balanced by 2^-d_j
+  int E = kNoExp;
   bool bad = false;
 #pragma unroll 4
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const double2 x = P[j], y = Qr[j];
-    mx = fmax(mx, fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y))));
+    const double mx = fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y)));
     bad |= !(fabs(x.x) + fabs(x.y) + fabs(y.x) + fabs(y.y) <= kDblMax);
+    if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx) - bal_delta(bdel, k, n, j));
   }
   bad = __syncthreads_or(bad);
-  mx = block_max(mx, red);
+  E = block_max_int(E, ired);
   if (bad) {
     if (threadIdx.x == 0) atomicExch(nonfinite, 1);
     return;
   }
   int e = 0;
-  if (mx != 0.0) {
-    const int E = exp_of(mx);
-    double ss = 0.0;  // sum of squares of the row scaled by 2^-E (each term <= 1)
+  double l1s = 0.0;  // L1 norm of the scaled (unrounded) real-form row
+  if (E != kNoExp) {
+    double ss = 0.0;  // sum of squares of the balanced row scaled by 2^-E (each term <= 1)
+    double l1 = 0.0;
 #pragma unroll 4
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const double2 x = P[j], y = Qr[j];
-      const double a = scale2(x.x, -E), b = scale2(x.y, -E), c = scale2(y.x, -E), d = scale2(y.y, -E);
+      const int sh = -bal_delta(bdel, k, n, j) - E;
+      const double a = scale2(x.x, sh), b = scale2(x.y, sh), c = scale2(y.x, sh), d = scale2(y.y, sh);
       ss = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ss))));
+      l1 += (fabs(a) + fabs(b)) + (fabs(c) + fabs(d));
     }
     ss = block_sum(ss, red);
+    l1 = block_sum(l1, red);
     e = scale_exponent(E, sqrt(ss));
+    l1s = scale2(l1 * (1.0 + 0x1p-40), E + e);
   }
   if (threadIdx.x == 0) {
     eA[f * Mp + i] = e;
     eA[fpart * Mp + m + i] = e;
+    xl1[f * Mp + i] = l1s;
+    xl1[fpart * Mp + m + i] = l1s;
+    if (E != kNoExp) {  // (the row is in both slots of the pair)
+      atomicMin(amin + f, e);
+      if (fpart != f) atomicMin(amin + fpart, e);
+    }
   }
   const size_t Kp = 4 * (size_t)n, plane = (size_t)F * Mp * Kp;
   uint8_t* up = out + (size_t)(f * Mp + i) * Kp;
@@ -641,8 +742,9 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
 #pragma unroll
     for (int t = 0; t < kAVec; ++t) {
       const double2 x = src[j0 + t];
-      re[t] = to_limbs(x.x, e);
-      im[t] = to_limbs(x.y, e);
+      const int et = e - bal_delta(bdel, k, n, j0 + t);
+      re[t] = to_limbs(x.x, et);
+      im[t] = to_limbs(x.y, et);
     }
     // P: up[0n] = Re, lo[1n] = Re, up[2n] = Im, lo[3n] = -Im
     // Q: lo[0n] = Re, up[1n] = -Re, lo[2n] = Im, up[3n] = Im
@@ -703,23 +805,21 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
 struct ColPart {
   int E;      // kNoExp: the block is all zeros
   double ss;  // sum of (|re|^2 + |im|^2) 2^-2E over the block
+  double l1;  // sum of (|re| + |im|) 2^-E over the block
 };
-// binary exponent E of |v| > 0 finite (|v| < 2^E, |v| >= 2^(E-1)), from the bits
-__device__ __forceinline__ int exp_bits(double v) {
-  const int f = (int)((__double_as_longlong(v) >> 52) & 0x7ff);
-  return f ? f - 1022 : exp_of(v);  // subnormal: frexp
-}
 __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restrict__ b1,
                                                           const double2* __restrict__ b2, ColPart* __restrict__ part,
-                                                          int* nonfinite, int n, int s, int p, int f0, int Sp, int F,
-                                                          uint64_t ldb, uint64_t bslice, int cbase) {
+                                                          const int* __restrict__ bdel, int* nonfinite, int n, int s,
+                                                          int p, int f0, int Sp, int F, uint64_t ldb, uint64_t bslice,
+                                                          int cbase) {
   __shared__ int se[8][33];
   __shared__ double sss[8][33];
+  __shared__ double sl1[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31), w = threadIdx.x >> 5, f = blockIdx.y;
-  const int k = slot_slice(f0 + f, p, cbase);
+  const int k = slot_slice(f0 + f, p, cbase), kf = slot_freq(f0 + f, p);
   const int j0 = blockIdx.z * 256, jend = min(2 * n, j0 + 256);
   int E = kNoExp;
-  double ss = 0.0;
+  double ss = 0.0, l1 = 0.0;
   bool bad = false;
   if (c < s) {
     const double2* base1 = b1 + k * bslice + c;
@@ -743,49 +843,68 @@ __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restr
         }
         const double mx = fmax(ax, ay);
         if (mx == 0.0) continue;
-        const int e = exp_bits(mx);
+        const int j = jb + 8 * u;
+        const int d = bal_delta(bdel, kf, n, j < n ? j : j - n);  // row j of D Y
+        const int e = exp_bits(mx) + d;
         if (e > E) {
-          if (E != kNoExp) ss = scale2(ss, 2 * (E - e));
+          if (E != kNoExp) {
+            ss = scale2(ss, 2 * (E - e));
+            l1 = scale2(l1, E - e);
+          }
           E = e;
         }
-        const double a = scale2(y[u].x, -E), b = scale2(y[u].y, -E);
+        const double a = scale2(y[u].x, d - E), b = scale2(y[u].y, d - E);
         ss = fma(a, a, fma(b, b, ss));
+        l1 += fabs(a) + fabs(b);
       }
     }
   }
   se[w][threadIdx.x & 31] = E;
   sss[w][threadIdx.x & 31] = ss;
+  sl1[w][threadIdx.x & 31] = l1;
   bad = __syncthreads_or(bad);
   if (w == 0) {
     int Eb = kNoExp;
     for (int t = 0; t < 8; ++t) Eb = max(Eb, se[t][threadIdx.x]);
-    double sb = 0.0;
+    double sb = 0.0, lb = 0.0;
     if (Eb != kNoExp)
       for (int t = 0; t < 8; ++t)
-        if (se[t][threadIdx.x] != kNoExp) sb += scale2(sss[t][threadIdx.x], 2 * (se[t][threadIdx.x] - Eb));
+        if (se[t][threadIdx.x] != kNoExp) {
+          sb += scale2(sss[t][threadIdx.x], 2 * (se[t][threadIdx.x] - Eb));
+          lb += scale2(sl1[t][threadIdx.x], se[t][threadIdx.x] - Eb);
+        }
     if (bad && threadIdx.x == 0) atomicExch(nonfinite, 1);
-    part[((size_t)blockIdx.z * F + f) * Sp + c] = ColPart{(c < s && !bad) ? Eb : kNoExp, sb};
+    part[((size_t)blockIdx.z * F + f) * Sp + c] = ColPart{(c < s && !bad) ? Eb : kNoExp, sb, lb};
   }
 }
 
-// B side, pass 1b: combine the row-block partials of each column in order
-__global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* __restrict__ eB, int nz, int F,
-                                        int Sp, int fcur) {
+// B side, pass 1b: combine the row-block partials of each column in order;
+// column exponent e and the L1 norm of the scaled (unrounded) column (guard)
+__global__ void oz_colexp_finish_kernel(const ColPart* __restrict__ part, int* __restrict__ eB,
+                                        double* __restrict__ yl1, int* __restrict__ bmin, int nz, int F, int Sp,
+                                        int fcur) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= fcur * Sp) return;
   const int f = t / Sp, c = t - f * Sp;
   int E = kNoExp;
   for (int z = 0; z < nz; ++z) E = max(E, part[((size_t)z * F + f) * Sp + c].E);
   int e = 0;
+  double l1s = 0.0;
   if (E != kNoExp) {
-    double ss = 0.0;
+    double ss = 0.0, l1 = 0.0;
     for (int z = 0; z < nz; ++z) {
       const ColPart pz = part[((size_t)z * F + f) * Sp + c];
-      if (pz.E != kNoExp) ss += scale2(pz.ss, 2 * (pz.E - E));
+      if (pz.E != kNoExp) {
+        ss += scale2(pz.ss, 2 * (pz.E - E));
+        l1 += scale2(pz.l1, pz.E - E);
+      }
     }
     e = scale_exponent(E, sqrt(ss));
+    l1s = scale2(l1 * (1.0 + 0x1p-40), E + e);
+    atomicMin(bmin + f, e);
   }
   eB[f * Sp + c] = e;
+  yl1[f * Sp + c] = l1s;
 }
 
 // B side, pass 2: one CTA per (slot f, 32 columns, 128-row block of Y); writes
@@ -805,12 +924,13 @@ constexpr size_t res_b_smem(int bc) { return sizeof(double2) * bc * kBStride; }
 template <int BC>
 __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2,
-                                                           const int* __restrict__ eB, uint8_t* __restrict__ out,
-                                                           int n, int s, int p, int f0, int Sp, int F, uint64_t ldb,
-                                                           uint64_t bslice, int cbase, int share_end) {
+                                                           const int* __restrict__ eB, const int* __restrict__ bdel,
+                                                           uint8_t* __restrict__ out, int n, int s, int p, int f0,
+                                                           int Sp, int F, uint64_t ldb, uint64_t bslice, int cbase,
+                                                           int share_end) {
   extern __shared__ double2 tile[];  // [BC][kBStride]
   const int c0 = blockIdx.x * BC, j0 = blockIdx.z * kBRows, f = blockIdx.y;
-  const int k = slot_slice(f0 + f, p, cbase);
+  const int k = slot_slice(f0 + f, p, cbase), kf = slot_freq(f0 + f, p);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   constexpr int RPI = 32 / BC;  // rows per warp load
 #pragma unroll
@@ -830,6 +950,9 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
   const bool yy = shares_x(f0 + f, share_end);
   const bool top = jb < n;  // rows of B1 (else B2); 4 rows never straddle n (n % 32 == 0)
   const int pos = yy ? (top ? jb + n : jb - n) : jb;
+  int dj[4];  // balancing of the lane's 4 rows of D Y
+#pragma unroll
+  for (int t = 0; t < 4; ++t) dj[t] = bal_delta(bdel, kf, n, (top ? jb : jb - n) + t);
   for (int cc = ty; cc < BC; cc += 8) {
     const int c = c0 + cc;
     const int e = eB[f * Sp + c];
@@ -840,8 +963,8 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const double2 y = tile[cc * kBStride + jl + t + ((jl + t) >> 3)];
-      lr[t] = to_limbs(y.x, e);
-      li[t] = to_limbs(y.y, e);
+      lr[t] = to_limbs(y.x, e + dj[t]);
+      li[t] = to_limbs(y.y, e + dj[t]);
     }
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
@@ -879,40 +1002,55 @@ __global__ void __launch_bounds__(256) oz_residue_b_kernel(const double2* __rest
 // fraction (mod 2^96 wraps = mod 1); the weights' rounding (<= 1/2 ulp each)
 // bounds the error by 16*255/2 units of 2^-96, i.e. <= 2^-84 * M = 2^41 in X'Y'
 // (which is ~2^110 for a typical element): far below one fp64 ulp.
-__device__ __forceinline__ double crt_finish(uint64_t acc0, uint64_t acc1, uint64_t acc2, int e) {
+// X'Y' as a double (the signed 96-bit fraction times M), before the 2^e scaling
+__device__ __forceinline__ double crt_value(uint64_t acc0, uint64_t acc1, uint64_t acc2) {
   acc1 += acc0 >> 32;
   acc2 += acc1 >> 32;
-  // signed 96-bit fraction in [-1/2, 1/2), then times M 2^e
+  // signed 96-bit fraction in [-1/2, 1/2), then times M
   const int64_t top = (int64_t)(((uint64_t)(uint32_t)acc2 << 32) | (uint32_t)acc1);
   const double frac = (double)top + (double)(uint32_t)acc0 * 2.3283064365386963e-10;  // (top + s0 2^-32), units 2^-64
-  return scale2(frac * c_mod.M, e - 64);
+  return scale2(frac * c_mod.M, -64);
 }
 
 // one thread per 4 consecutive complex elements of output rows r (slot f, row
 // r of [C1; C2]): 16 x 8-byte residue loads (pointer bumped by one plane per
-// modulus), 3 multiply-adds per residue into 64-bit limb accumulators
+// modulus), 3 multiply-adds per residue into 64-bit limb accumulators.  Each
+// CTA walks several rows and leaves its guard partial (weighted squared error
+// bound and |C|^2) in gpart[f][cta].
 constexpr int kCrtVec = 4;
 __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
-                                                     const int* __restrict__ eB, const int* nonfinite,
-                                                     double2* __restrict__ c1, double2* __restrict__ c2, int m,
-                                                     int s, int p, int f0, int bslot0, int Mp, int Sp, int F,
-                                                     uint64_t ldc, uint64_t cslice, int cbase, int share_end) {
+                                                     const double* __restrict__ xl1, const int* __restrict__ amin,
+                                                     const int* __restrict__ eB, const double* __restrict__ yl1,
+                                                     const int* __restrict__ bmin, const int* nonfinite,
+                                                     GuardAcc* __restrict__ gpart, double2* __restrict__ c1,
+                                                     double2* __restrict__ c2, int m, int n, int s, int p, int f0,
+                                                     int bslot0, int Mp, int Sp, int F, uint64_t ldc, uint64_t cslice,
+                                                     int cbase, int share_end) {
   if (*nonfinite) return;
+  __shared__ double red[8];
   const int cb = (blockIdx.x * blockDim.x + threadIdx.x) * kCrtVec;
   const int f = blockIdx.z;
-  if (cb >= s) return;
-  int eb[kCrtVec];
-#pragma unroll
-  for (int t = 0; t < kCrtVec; ++t) {
-    eb[t] = eB[(bslot0 + f) * Sp + cb + t];
-  }
+  const bool active = cb < s;
   const int k = slot_slice(f0 + f, p, cbase);
   const size_t plane = (size_t)F * Mp * Sp * 2;  // bytes
   // odd slot of a shared-X' pair: R row r < m is -C2[r], R row m + r is C1[r],
   // with the row exponents of the even partner's X'
   const bool sx = shares_x(f0 + f, share_end);
   const int fa = sx ? f - 1 : f;
-  for (int r = blockIdx.y; r < 2 * m; r += gridDim.y) {
+  const int a0 = amin[fa], b0 = bmin[bslot0 + f];
+  int eb[kCrtVec];
+  double yb[kCrtVec], wc[kCrtVec];  // column share of the element bound; column weight (0: exact column)
+  const double kq = 0.25 * (4.0 * n) + 0x1p42;
+#pragma unroll
+  for (int t = 0; t < kCrtVec; ++t) {
+    const int c = active ? min(cb + t, Sp - 1) : 0;
+    eb[t] = eB[(bslot0 + f) * Sp + c];
+    const double l = yl1[(bslot0 + f) * Sp + c];
+    yb[t] = 0.5 * l + kq;
+    wc[t] = (active && cb + t < s && l != 0.0) ? scale2(1.0, -2 * (eb[t] - b0)) : 0.0;
+  }
+  double gsb = 0.0, gsc = 0.0;
+  for (int r = blockIdx.y; r < 2 * m && active; r += gridDim.y) {
     const uint8_t* ptr = R + ((size_t)(f * Mp + r) * Sp + cb) * 2;
     const bool neg = sx && r < m;
     uint64_t acc[kCrtVec][2][3];
@@ -941,14 +1079,55 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
       }
     }
     const int ea = eA[fa * Mp + r];
+    const double xr = xl1[fa * Mp + r];
+    const double xb = 0.5 * xr;
+    const double wr = xr != 0.0 ? scale2(1.0, -2 * (ea - a0)) : 0.0;  // (an all-zero row is exact)
     double2* dst = ((r < m) != sx) ? c1 + k * cslice + (size_t)(sx ? r - m : r) * ldc
                                    : c2 + k * cslice + (size_t)(sx ? r : r - m) * ldc;
 #pragma unroll
     for (int t = 0; t < kCrtVec; ++t) {
       if (cb + t >= s) break;
       const int e = -(ea + eb[t]);
-      dst[cb + t] = make_double2(crt_finish(acc[t][0][0], acc[t][0][1], acc[t][0][2], e),
-                                 crt_finish(acc[t][1][0], acc[t][1][1], acc[t][1][2], e));
+      const double vr = crt_value(acc[t][0][0], acc[t][0][1], acc[t][0][2]);
+      const double vi = crt_value(acc[t][1][0], acc[t][1][1], acc[t][1][2]);
+      dst[cb + t] = make_double2(scale2(vr, e), scale2(vi, e));
+      const double w = wr * wc[t], bnd = xb + yb[t];  // per real part; |err|^2 <= 2 bnd^2
+      gsb = fma(2.0 * bnd * bnd, w, gsb);
+      gsc = fma(fma(vr, vr, vi * vi), w, gsc);
+    }
+  }
+  gsb = block_sum(gsb, red);
+  gsc = block_sum(gsc, red);
+  if (threadIdx.x == 0)
+    gpart[(size_t)f * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = GuardAcc{gsb, gsc};
+}
+
+// Guard decision per slot unit of a batch: combine the CRT partials of the
+// unit's slot(s) in a fixed order and flag the pair for the DMMA recompute
+// unless sum bound^2 <= tol2 * sum |C|^2.
+__global__ void __launch_bounds__(256) oz_guard_kernel(const GuardAcc* __restrict__ gpart, int nper,
+                                                       const int* nonfinite, int* __restrict__ pair_flags, int p,
+                                                       int f0, int fcur, double tol2, int force) {
+  __shared__ double red[8];
+  if (*nonfinite) return;  // everything is recomputed anyway
+  int sa, sb;
+  unit_slots(blockIdx.x, f0, fcur, p, sa, sb);
+  double gsb = 0.0, gsc = 0.0;
+  for (int sl = sa; sl <= sb; ++sl) {
+    const GuardAcc* g = gpart + (size_t)(sl - f0) * nper;
+    for (int i = threadIdx.x; i < nper; i += blockDim.x) {
+      gsb += g[i].sb;
+      gsc += g[i].sc;
+    }
+  }
+  gsb = block_sum(gsb, red);
+  gsc = block_sum(gsc, red);
+  if (threadIdx.x == 0) {
+    const bool ok = !force && gsc > 0.0 && gsc <= kDblMax && gsb <= tol2 * gsc;
+    if (!ok) {
+      const int kf = slot_freq(sa, p);
+      pair_flags[min(kf, p - kf)] = 1;
+      atomicAdd(&g_guard_fallbacks, 1ull);
     }
   }
 }
@@ -1102,9 +1281,27 @@ uint64_t batch_slots(uint64_t p, uint64_t per_slot, uint64_t budget) {
   return std::min<uint64_t>(p, ((p + nb - 1) / nb + 1) & ~uint64_t(1));
 }
 
+bool balance_on() {
+  static const bool on = oz::env_int("QTB_OZAKI_BALANCE", 1) != 0;
+  return on;
+}
+// guard tolerance tol^2 (QTB_OZAKI_GUARD_LOG2 = log2 tol, default -42);
+// QTB_OZAKI_GUARD=force sends every pair to the DMMA kernels (tests)
+double guard_tol2() {
+  static const double t = std::ldexp(1.0, 2 * oz::env_int("QTB_OZAKI_GUARD_LOG2", -42));
+  return t;
+}
+bool guard_force() {
+  static const bool f = [] {
+    const char* v = getenv("QTB_OZAKI_GUARD");
+    return v && strcmp(v, "force") == 0;
+  }();
+  return f;
+}
+
 // B' residues (and column exponents) of slots [f0, f0 + fcur) into buffer slots [bslot0, ...)
-// (parts: kPrepExp = column exponents only, kPrepRes = residues only, from
-// exponents already in B.eB; both by default)
+// (parts: kPrepExp = balancing + column exponents only, kPrepRes = residues
+// only, from exponents already in B.eB; both by default)
 constexpr int kPrepExp = 1, kPrepRes = 2;
 cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint64_t f0, int fcur, int bslot0,
                    int* flag, cudaStream_t stream, int parts = kPrepExp | kPrepRes) {
@@ -1112,16 +1309,26 @@ cudaError_t prep_b(const OzakiB& B, const double2* bh1, const double2* bh2, uint
   const uint64_t Sp = pad_cols(B.s);
   uint8_t* res = B.res + (size_t)bslot0 * 2 * Sp * 4 * B.n;
   int* eB = B.eB + (size_t)bslot0 * Sp;
+  double* yl1 = B.yl1 + (size_t)bslot0 * Sp;
   const int nz = (int)((2 * B.n + 255) / 256);
+  const int* bdel = balance_on() ? B.bdel : nullptr;
   if (parts & kPrepRes && !(parts & kPrepExp)) goto residues;
   {
   ColPart* part = nullptr;
   cudaError_t e = cudaMallocAsync(&part, sizeof(ColPart) * nz * fcur * Sp, stream);
   if (e != cudaSuccess) return e;
   ProfScope ps("k2_int8_colnorms", stream);
+  if (bdel) {
+    const int units = slot_units((int)f0, fcur, (int)B.p);
+    oz_balance_b_kernel<<<dim3((unsigned)((B.n + 7) / 8), (unsigned)units), 256, 0, stream>>>(
+        bh1, bh2, B.bdel, (int)B.n, (int)B.s, (int)B.p, (int)f0, fcur, B.ldb, B.bslice, B.cbase);
+    count_launches(1);
+  }
   oz_colexp_b_kernel<<<dim3((unsigned)(Sp / 32), fcur, (unsigned)nz), 256, 0, stream>>>(
-      bh1, bh2, part, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice, B.cbase);
-  oz_colexp_finish_kernel<<<(unsigned)((fcur * Sp + 255) / 256), 256, 0, stream>>>(part, eB, nz, fcur, (int)Sp, fcur);
+      bh1, bh2, part, bdel, flag, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, fcur, B.ldb, B.bslice, B.cbase);
+  cudaMemsetAsync(B.bmin + bslot0, 0x7f, fcur * sizeof(int), stream);
+  oz_colexp_finish_kernel<<<(unsigned)((fcur * Sp + 255) / 256), 256, 0, stream>>>(part, eB, yl1, B.bmin + bslot0, nz,
+                                                                                    fcur, (int)Sp, fcur);
   ps.stop();
   count_launches(2);
   e = cudaFreeAsync(part, stream);
@@ -1134,38 +1341,24 @@ residues:
   auto kern = bc == 16 ? oz_residue_b_kernel<16> : oz_residue_b_kernel<32>;
   kern<<<dim3((unsigned)(Sp / bc), fcur, (unsigned)((2 * B.n + kBRows - 1) / kBRows)), 256, res_b_smem(bc),
          stream>>>(
-      bh1, bh2, eB, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice, B.cbase,
-      share_end(B.p));
+      bh1, bh2, eB, bdel, res, (int)B.n, (int)B.s, (int)B.p, (int)f0, (int)Sp, (int)B.nslots, B.ldb, B.bslice,
+      B.cbase, share_end(B.p));
   pb.stop();
   count_launches(1);
   return cudaGetLastError();
 }
 
-// X' residues (and row exponents) of every frequency slot of A into A.res
-cudaError_t prep_a(const OzakiA& A, const double2* ah1, const double2* ah2, int* flag, cudaStream_t stream) {
-  using namespace oz;
-  const uint64_t Mp = pad_rows(A.m), Kp = 4 * A.n;
-  cudaError_t e = cudaSuccess;
-  if (Mp > 2 * A.m)
-    e = cudaMemset2DAsync(A.res + 2 * A.m * Kp, Mp * Kp, 0, (Mp - 2 * A.m) * Kp, (size_t)kQ * A.p, stream);
-  if (e != cudaSuccess) return e;
-  ProfScope pr("k2_int8_residues", stream);
-  oz_residue_a_kernel<<<dim3((unsigned)A.m, (unsigned)A.p), 256, 0, stream>>>(
-      ah1, ah2, A.res, A.eA, flag, (int)A.m, (int)A.n, (int)A.p, 0, (int)Mp, (int)A.p, -1, share_end(A.p));
-  pr.stop();
-  count_launches(1);
-  return cudaGetLastError();
-}
-
-// GEMM and CRT for the frequency slots [0, p) against prepared B' slots
-// (B.all: slot f of B' is frequency slot f; else B' is rebuilt per batch) and
-// either prepared X' slots (A != nullptr) or X' built per batch from Â.
-cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1,
-                     const double2* bh2, uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice,
-                     int* flag, cudaStream_t stream) {
+// GEMM and CRT for the frequency slots of B (all p, or B's compact range)
+// against B' (B.all: slot f of B' is frequency slot f; else B' is rebuilt per
+// batch), with X' built per batch from Â; then the guard decision per pair.
+// flag[0]: non-finite inputs (sticky), flag[1 + min(k, p - k)]: pair k is to
+// be recomputed by the DMMA kernels (reset here).
+cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                     uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
+                     cudaStream_t stream) {
   using namespace oz;
   const uint64_t n = B.n, s = B.s, p = B.p, Mp = pad_rows(m), Sp = pad_cols(s), Kp = 4 * n;
-  const uint64_t per_slot = A ? (uint64_t)kQ * Mp * Sp * 2 : a_slot_bytes(m, n, s);
+  const uint64_t per_slot = a_slot_bytes(m, n, s);
   // with B' prepared for every frequency the frequency batches are software-
   // pipelined over two streams: the X' residues of batch i+1 and the CRT of
   // batch i run beside the int8 GEMM of batch i+1 / i (their CTAs fit next to
@@ -1179,16 +1372,28 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   if (pipe && ps >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((ps + 3) / 4 + 1) & ~uint64_t(1)));
   const uint64_t nbatch = (ps + F - 1) / F;
   if (nbuf * F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytesA = A ? 0 : (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
-  const size_t offR = bytesA, offE = offR + nbuf * bytesR, wsbytes = offE + (A ? 0 : nbuf * F * Mp * sizeof(int));
+  // CRT grid: each CTA walks ~2m/256 rows (its guard partial is one block reduction)
+  const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 256),
+                   1);
+  const uint64_t nper = (uint64_t)cgrid.x * cgrid.y;  // guard partials per slot
+  const size_t bytesA = (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
+  const size_t offR = bytesA, offE = offR + nbuf * bytesR, offL = offE + ((nbuf * F * Mp * sizeof(int) + 255) & ~255ull);
+  const size_t offG = offL + nbuf * F * Mp * sizeof(double);
+  const size_t offM = offG + F * nper * sizeof(GuardAcc);
+  const size_t wsbytes = offM + nbuf * F * sizeof(int);
   uint8_t* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, wsbytes, stream);
+  cudaError_t e = cudaMemsetAsync(flag + 1, 0, (p / 2 + 1) * sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  uint8_t* resA = A ? A->res : ws;
-  int* eA = A ? A->eA : reinterpret_cast<int*>(ws + offE);
-  const uint64_t aslots = A ? p : nbuf * F;  // slots in the X' buffer (its plane stride)
+  if ((e = cudaMallocAsync(&ws, wsbytes, stream)) != cudaSuccess) return e;
+  uint8_t* resA = ws;
+  int* eA = reinterpret_cast<int*>(ws + offE);
+  double* xl1 = reinterpret_cast<double*>(ws + offL);
+  GuardAcc* gpart = reinterpret_cast<GuardAcc*>(ws + offG);
+  int* amin = reinterpret_cast<int*>(ws + offM);  // smallest row exponent per X' slot (guard weights)
+  const uint64_t aslots = nbuf * F;  // slots in the X' buffer (its plane stride)
+  const int* bdel = balance_on() ? B.bdel : nullptr;
   // rows [2m, Mp) of every X' slot are padding the residue kernel never writes
-  if (!A && Mp > 2 * m)
+  if (Mp > 2 * m)
     e = cudaMemset2DAsync(resA + 2 * m * Kp, Mp * Kp, 0, (Mp - 2 * m) * Kp, (size_t)kQ * aslots, stream);
   CUtensorMap mapA, mapB;
   if (e == cudaSuccess && (!make_map(&mapA, resA, Kp, aslots * Mp, kQ, BM) ||
@@ -1198,12 +1403,9 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     if ((e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream)) == cudaSuccess) B.ready = true;
   }
   const bool lazyB = B.all && !B.ready;  // B' of each batch built beside the previous batch's GEMM
-  // (experiment switch) the CRT of batch i on the main stream right after its
-  // GEMM instead of on the aux stream beside GEMM i+1: measured equal on config 5
-  const bool crt_main = env_int("QTB_OZAKI_CRT_MAIN", 0) != 0;
-  // the column exponents of every slot first (a streaming read of B̂ that
-  // would crawl beside the GEMM), the B' residues then batch by batch; before
-  // the fork below, so the aux stream's batches see them
+  // the balancing and column exponents of every slot first (a streaming read
+  // of B̂ that would crawl beside the GEMM), the B' residues then batch by
+  // batch; before the fork below, so the aux stream's batches see them
   if (e == cudaSuccess && lazyB) e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream, kPrepExp);
   cudaStream_t aux = stream;
   std::vector<cudaEvent_t> evs;
@@ -1231,15 +1433,13 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     int fcur;
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
-    if (!A) {
-      ProfScope pr("k2_int8_residues", st);
-      oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(ah1, ah2, resA + b * F * Mp * Kp,
-                                                                   eA + b * F * Mp, flag, (int)m, (int)n, (int)p,
-                                                                   (int)f0, (int)Mp, (int)aslots, B.cbase,
-                                                                   share_end(p));
-      pr.stop();
-      count_launches(1);
-    }
+    ProfScope pr("k2_int8_residues", st);
+    cudaMemsetAsync(amin + b * F, 0x7f, F * sizeof(int), st);
+    oz_residue_a_kernel<<<dim3((unsigned)m, fcur), 256, 0, st>>>(
+        ah1, ah2, resA + b * F * Mp * Kp, eA + b * F * Mp, xl1 + b * F * Mp, amin + b * F, bdel, flag, (int)m, (int)n,
+        (int)p, (int)f0, (int)Mp, (int)aslots, B.cbase, share_end(p));
+    pr.stop();
+    count_launches(1);
     if (lazyB) {
       const cudaError_t eb = prep_b(B, B.bh1, B.bh2, f0, fcur, (int)(f0 - B.s0), flag, st, kPrepRes);
       if (eb != cudaSuccess && e == cudaSuccess) e = eb;
@@ -1251,17 +1451,20 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     batch(i, f0, fcur);
     const uint64_t b = i % nbuf;
     const int bslot0 = B.all ? (int)(f0 - B.s0) : 0;
-    const uint64_t aslot0 = A ? f0 : b * F;
-    const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 65535),
-                     (unsigned)fcur);
+    dim3 g = cgrid;
+    g.z = (unsigned)fcur;
     ProfScope pc("k2_int8_crt", st);
-    oz_crt_kernel<<<cgrid, 256, 0, st>>>(ws + offR + b * bytesR, eA + aslot0 * Mp, B.eB, flag, ch1, ch2, (int)m,
-                                         (int)s, (int)p, (int)f0, bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice,
-                                         B.cbase, share_end(p));
+    oz_crt_kernel<<<g, 256, 0, st>>>(ws + offR + b * bytesR, eA + b * F * Mp, xl1 + b * F * Mp, amin + b * F, B.eB,
+                                     B.yl1, B.bmin, flag, gpart, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)f0,
+                                     bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice, B.cbase, share_end(p));
+    oz_guard_kernel<<<(unsigned)slot_units((int)f0, fcur, (int)p), 256, 0, st>>>(
+        gpart, (int)nper, flag, flag + 1, (int)p, (int)f0, fcur, guard_tol2(), guard_force() ? 1 : 0);
     pc.stop();
-    count_launches(1);
+    count_launches(2);
   };
-  if (e == cudaSuccess && (!A || lazyB)) residues(0, stream);
+  // batch 0's X' (and, lazily, its B' residues); without B.all its B' first
+  if (e == cudaSuccess && !B.all) e = prep_b(B, bh1, bh2, B.s0, (int)std::min<uint64_t>(F, ps), 0, flag, stream);
+  if (e == cudaSuccess) residues(0, stream);
   cudaEvent_t res_ready = nullptr, prev_gemm_done = nullptr;
   for (uint64_t i = 0; i < nbatch && e == cudaSuccess; ++i) {
     uint64_t f0;
@@ -1271,14 +1474,16 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
     int bslot0 = (int)(f0 - B.s0);
     if (!B.all) {  // B' for this batch only (sequential schedule)
       bslot0 = 0;
-      if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
-      if (!A && i > 0) residues(i, stream);
+      if (i > 0) {
+        if ((e = prep_b(B, bh1, bh2, f0, fcur, 0, flag, stream)) != cudaSuccess) break;
+        residues(i, stream);
+      }
     }
     // X' of batch i (and, by stream order on aux, the CRT of batch i-2 that used R[b]) ready
     if (res_ready) cudaStreamWaitEvent(stream, res_ready, 0);
     ProfScope pg("k2_int8_gemm", stream);
     GemmParams gp{ws + offR + b * bytesR, kQ, (int)(Mp / BM), (int)Mp, (int)Sp, (int)(Kp / BK), (int)F, bslot0,
-                  (int)(Sp / BNC), fcur, (int)(A ? f0 : b * F), (int)f0, share_end(p)};
+                  (int)(Sp / BNC), fcur, (int)(b * F), (int)f0, share_end(p)};
     if (use_pair()) {
       const uint64_t items = (uint64_t)fcur * kQ * (Mp / 256) * (Sp / BNC);
       const unsigned clusters = (unsigned)std::min<uint64_t>(items, (uint64_t)num_sms() / 2);
@@ -1301,23 +1506,21 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
       cudaEvent_t gemm_done = mkev();
       cudaEventRecord(gemm_done, stream);
       // aux: X' residues of batch i+1 into the other buffer (free once GEMM i-1,
-      // which precedes GEMM i on the main stream, is done), then the CRT of batch i
-      if ((!A || lazyB) && i + 1 < nbatch) {
+      // which precedes GEMM i on the main stream, is done), then the CRT of
+      // batch i — which therefore also precedes residues(i+2) rewriting this
+      // batch's row exponents / norms on the same stream
+      if (i + 1 < nbatch) {
         if (prev_gemm_done) cudaStreamWaitEvent(aux, prev_gemm_done, 0);  // GEMM i-1 read this X' buffer
         residues(i + 1, aux);
       }
       res_ready = mkev();
       cudaEventRecord(res_ready, aux);
-      if (crt_main) {
-        crt(i, stream);
-      } else {
-        cudaStreamWaitEvent(aux, gemm_done, 0);
-        crt(i, aux);
-      }
+      cudaStreamWaitEvent(aux, gemm_done, 0);
+      crt(i, aux);
       prev_gemm_done = gemm_done;
     } else {
       crt(i, stream);
-      if ((!A || lazyB) && B.all && i + 1 < nbatch) residues(i + 1, stream);
+      if (B.all && i + 1 < nbatch) residues(i + 1, stream);
     }
     e = cudaGetLastError();
   }
@@ -1331,6 +1534,22 @@ cudaError_t multiply(const OzakiA* A, OzakiB& B, const double2* ah1, const doubl
   if (aux != stream) cudaStreamDestroy(aux);
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
   return e != cudaSuccess ? e : fe;
+}
+
+// B' storage: residues, column exponents, column norms (guard), balancing
+cudaError_t alloc_b(OzakiB& B, cudaStream_t stream) {
+  const uint64_t Sp = pad_cols(B.s);
+  const size_t bytes = (size_t)oz::kQ * B.nslots * 2 * Sp * 4 * B.n;
+  const size_t offE = bytes, offL = offE + (((size_t)B.nslots * Sp * sizeof(int) + 255) & ~size_t(255));
+  const size_t offD = offL + (size_t)B.nslots * Sp * sizeof(double);
+  const size_t offM = offD + B.p * B.n * sizeof(int);
+  cudaError_t e = cudaMallocAsync(&B.res, offM + B.nslots * sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  B.eB = reinterpret_cast<int*>(B.res + offE);
+  B.yl1 = reinterpret_cast<double*>(B.res + offL);
+  B.bdel = reinterpret_cast<int*>(B.res + offD);
+  B.bmin = reinterpret_cast<int*>(B.res + offM);
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -1357,10 +1576,7 @@ cudaError_t ozaki_prepare_b(const double2* bh1, const double2* bh2, uint64_t m, 
   B.all = require_all || per_b * p <= env_mb("QTB_OZAKI_B_MB", 24576);
   B.nslots = B.all ? (int)p : (int)batch_slots(p, a_slot_bytes(m, n, s) + per_b, env_mb("QTB_OZAKI_WS_MB", 3072));
   if ((uint64_t)B.nslots * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)oz::kQ * B.nslots * 2 * pad_cols(s) * 4 * n;
-  if ((e = cudaMallocAsync(&B.res, bytes + (size_t)B.nslots * pad_cols(s) * sizeof(int), stream)) != cudaSuccess)
-    return e;
-  B.eB = reinterpret_cast<int*>(B.res + bytes);
+  if ((e = alloc_b(B, stream)) != cudaSuccess) return e;
   B.bh1 = bh1;
   B.bh2 = bh2;
   if (B.all && !lazy) e = prep_b(B, bh1, bh2, 0, (int)p, 0, flag, stream);
@@ -1401,9 +1617,9 @@ cudaError_t ozaki_prepare_b_slots(const double2* bh1, const double2* bh2, uint64
   B.all = true;
   B.nslots = ns;
   if ((uint64_t)ns * 2 * pad_cols(s) > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)oz::kQ * ns * 2 * pad_cols(s) * 4 * n;
-  if ((e = cudaMallocAsync(&B.res, bytes + (size_t)ns * pad_cols(s) * sizeof(int), stream)) != cudaSuccess) return e;
-  B.eB = reinterpret_cast<int*>(B.res + bytes);
+  if ((e = alloc_b(B, stream)) != cudaSuccess) return e;
+  B.bh1 = bh1;
+  B.bh2 = bh2;
   if ((e = prep_b(B, bh1, bh2, (uint64_t)s0, ns, 0, flag, stream)) != cudaSuccess) {
     cudaFreeAsync(B.res, stream);
     return e;
@@ -1417,43 +1633,7 @@ cudaError_t ozaki_multiply(OzakiB& B, const double2* ah1, const double2* ah2, co
                            uint64_t m, double2* ch1, double2* ch2, uint64_t ldc, uint64_t cslice, int* flag,
                            cudaStream_t stream) {
   if (m == 0 || B.s == 0) return cudaSuccess;
-  return multiply(nullptr, B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
-}
-
-cudaError_t ozaki_prepare_a(const double2* ah1, const double2* ah2, uint64_t m, uint64_t n, uint64_t p, int* flag,
-                            OzakiA* out, cudaStream_t stream) {
-  *out = OzakiA{};
-  if (n % 32 != 0 || n > 8192 || p == 0 || m == 0) return cudaErrorInvalidValue;
-  cudaError_t e = oz_init();
-  if (e != cudaSuccess) return e;
-  OzakiA A;
-  A.m = m;
-  A.n = n;
-  A.p = p;
-  const uint64_t Mp = pad_rows(m);
-  if (p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
-  const size_t bytes = (size_t)oz::kQ * p * Mp * 4 * n;
-  if ((e = cudaMallocAsync(&A.res, bytes + (size_t)p * Mp * sizeof(int), stream)) != cudaSuccess) return e;
-  A.eA = reinterpret_cast<int*>(A.res + bytes);
-  if ((e = prep_a(A, ah1, ah2, flag, stream)) != cudaSuccess) {
-    cudaFreeAsync(A.res, stream);
-    return e;
-  }
-  *out = A;
-  return cudaSuccess;
-}
-
-cudaError_t ozaki_multiply_prepared(const OzakiA& A, OzakiB& B, double2* ch1, double2* ch2, uint64_t ldc,
-                                    uint64_t cslice, int* flag, cudaStream_t stream) {
-  if (A.m == 0 || B.s == 0) return cudaSuccess;
-  if (A.n != B.n || A.p != B.p || !B.all) return cudaErrorInvalidValue;
-  return multiply(&A, B, nullptr, nullptr, nullptr, nullptr, A.m, ch1, ch2, ldc, cslice, flag, stream);
-}
-
-cudaError_t ozaki_release_a(OzakiA& A, cudaStream_t stream) {
-  cudaError_t e = A.res ? cudaFreeAsync(A.res, stream) : cudaSuccess;
-  A = OzakiA{};
-  return e;
+  return multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
 }
 
 cudaError_t ozaki_release(OzakiB& B, cudaStream_t stream) {
@@ -1467,14 +1647,21 @@ cudaError_t launch_spectral_gemm_ozaki(const double2* ah1, const double2* ah2, c
                                        uint64_t s, uint64_t p, uint64_t ldb, uint64_t ldc, uint64_t bslice,
                                        uint64_t cslice, int* flag, cudaStream_t stream) {
   if (m == 0 || s == 0 || p == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), stream);
-  if (e != cudaSuccess) return e;
   OzakiB B;
-  if ((e = ozaki_prepare_b(bh1, bh2, m, n, s, p, ldb, bslice, flag, false, &B, stream, true)) != cudaSuccess)
-    return e;
+  cudaError_t e = ozaki_prepare_b(bh1, bh2, m, n, s, p, ldb, bslice, flag, false, &B, stream, true);
+  if (e != cudaSuccess) return e;
   e = ozaki_multiply(B, ah1, ah2, bh1, bh2, m, ch1, ch2, ldc, cslice, flag, stream);
   const cudaError_t fe = ozaki_release(B, stream);
   return e != cudaSuccess ? e : fe;
+}
+
+uint64_t int8_guard_fallbacks() {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, oz::g_guard_fallbacks, sizeof(v)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return v;
 }
 
 }  // namespace qtb

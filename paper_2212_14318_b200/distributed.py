@@ -25,324 +25,6 @@ import numpy as np
 from . import _native, shard
 
 
-class RowShardedTProduct:
-    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None,
-                 nchunks: int = 8):
-        import torch
-        self.torch = torch
-        self.m, self.n, self.s, self.p = m, n, s, p
-        self.rank, self.world = rank, world
-        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        self.lo, self.hi = shard.row_slab(m, world, rank)
-        self.rows = self.hi - self.lo
-        plan = shard.column_chunks(s, nchunks, world)  # multiples of the GEMM column tile
-        self.chunks = [(c0, c1) for c0, c1, _ in plan]
-        self.owner = [o for _, _, o in plan]
-        f64 = dict(dtype=torch.float64, device=self.dev)
-        self.a = torch.empty((2, p, self.rows, 2 * n), **f64)
-        self.ah = torch.empty_like(self.a)
-        self.bc = [torch.empty((2, p, n, 2 * (c1 - c0)), **f64) for c0, c1 in self.chunks]
-        self.bh = [torch.empty_like(t) for t in self.bc]
-        self.c = torch.empty((2, p, self.rows, 2 * s), **f64)
-        self.L = _native.lib()
-        # one stage-2 algorithm for every rank and chunk: the full product's
-        # (QT_GEMM_DMMA or QT_GEMM_INT8_EXACT), so the stitched C is bitwise
-        # identical to a single-GPU call
-        self.algo = self.L.qt_gemm_algo(m, n, s, p)
-
-    # ---------------------------------------------------------------- inputs
-    def load_a(self, a1: np.ndarray, a2: np.ndarray) -> None:
-        """Rows of this rank from full host planes (p, m, n) complex128."""
-        for k, src in enumerate((a1, a2)):
-            slab = np.ascontiguousarray(src[:, self.lo:self.hi]).view(np.float64)
-            self.a[k].copy_(self.torch.from_numpy(slab))
-
-    def owned(self, j: int) -> bool:
-        return self.owner[j] == self.rank
-
-    def load_b(self, b1: np.ndarray, b2: np.ndarray, owned_only: bool = True) -> None:
-        """The chunks of B (p, n, s host planes) this rank owns into their
-        buffers (all chunks with owned_only=False: one rank run without peers)."""
-        for j, (t, (c0, c1)) in enumerate(zip(self.bc, self.chunks)):
-            if owned_only and not self.owned(j):
-                continue
-            for k, src in enumerate((b1, b2)):
-                t[k].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, :, c0:c1]).view(np.float64)))
-
-    # ----------------------------------------------------------------- step
-    def step(self, broadcast=None, stream=None) -> None:
-        """One T-product step.  `broadcast(tensor, src)` must enqueue an async
-        broadcast from rank `src` (the chunk's owner) and return an object with
-        .wait() (a torch.distributed Work); None on a single rank."""
-        torch = self.torch
-        st = torch.cuda.current_stream() if stream is None else stream
-        sh = st.cuda_stream
-        L, n, s, p, rows = self.L, self.n, self.s, self.p, self.rows
-        works = [broadcast(t, o) for t, o in zip(self.bc, self.owner)] if broadcast is not None else None
-        if rows:
-            _native.check(L.qt_qfft3_conj_f64_device(self.a[0].data_ptr(), self.a[1].data_ptr(),
-                                                     self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh),
-                          "qfft3_conj(A slab)")
-        plan = None
-        if rows and self.algo == 1:
-            # exact int8 stage 2: the residues of this rank's Â slab are built
-            # once per step and reused by every B̂ chunk
-            h = ctypes.c_void_p()
-            _native.check(L.qt_int8_plan_create(self.ah[0].data_ptr(), self.ah[1].data_ptr(), rows, n, p, sh,
-                                                ctypes.byref(h)), "int8 plan")
-            plan = h
-        for j, (c0, c1) in enumerate(self.chunks):
-            if works is not None:
-                works[j].wait()  # compute stream waits for chunk j only
-            if not rows:
-                continue
-            cols = c1 - c0
-            _native.check(L.qt_qfft3_conj_f64_device(self.bc[j][0].data_ptr(), self.bc[j][1].data_ptr(),
-                                                     self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), n, cols, p,
-                                                     sh), "qfft3_conj(B chunk)")
-            off = 16 * c0  # bytes: column c0 of every row of the C slab
-            if plan is not None:
-                _native.check(L.qt_int8_plan_multiply(
-                    plan, self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(), self.c[0].data_ptr() + off,
-                    self.c[1].data_ptr() + off, cols, cols, s, n * cols, rows * s, sh), "int8 plan multiply")
-            else:
-                _native.check(L.qt_spectral_product_f64_device_ld_algo(
-                    self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[j][0].data_ptr(), self.bh[j][1].data_ptr(),
-                    self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, rows, n, cols, p,
-                    cols, s, n * cols, rows * s, self.algo, sh), "spectral_product(chunk)")
-        if plan is not None:
-            _native.check(L.qt_int8_plan_destroy(plan, sh), "int8 plan destroy")
-        if rows:
-            _native.check(L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
-                                                      self.c[0].data_ptr(), self.c[1].data_ptr(), rows, s, p, sh),
-                          "qifft3_conj(C slab)")
-
-    def result(self):
-        """(c1, c2) of this rank's rows as host complex128 (p, rows, s)."""
-        out = self.c.cpu().numpy().view(np.complex128)
-        return out[0], out[1]
-
-
-class Grid2DTProduct:
-    """One rank's share of the 2-D block-decomposed T-product (gr x gc ranks).
-
-    Rank (i, j) = divmod(rank, gc) computes block (rows of row block i, columns
-    of column block j) of C.  Row i of C needs only row i of A and column j
-    only column j of B, so a block needs A's row block i and
-    B's column block j.  Those arrive inside the step: A's row block is split
-    into gc pieces, piece k owned (resident, uploaded) by rank (i, k) and
-    broadcast over its row group; B's column block into gr pieces, piece k
-    owned by rank (k, j) and broadcast over its column group.  Per rank: K1 of
-    each arriving A piece into the Â block, then the stage-2 residues of Â
-    (int8 path: one plan), then per arriving B piece K1 + stage 2 into its
-    columns of the C block, then K3.  Against row sharding (gc = 1) the
-    replicated work per rank — the transform and residues of ALL of B — drops
-    to those of one column block: config 5 at 8 ranks, (gr, gc) = (4, 2).
-    Every element goes through the same kernels and arithmetic as the
-    single-GPU product (the stage-2 algorithm is the full shape's), so the
-    stitched C is bitwise identical for every grid.
-    """
-
-    def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None, grid=None,
-                 stage_buffer=None):
-        import torch
-        self.torch = torch
-        self.m, self.n, self.s, self.p = m, n, s, p
-        self.rank, self.world = rank, world
-        self.gr, self.gc = grid if grid is not None else shard.grid_shape(world, m, s)
-        assert self.gr * self.gc == world
-        self.i, self.j = divmod(rank, self.gc)
-        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        self.r0, self.r1 = shard.row_slab(m, self.gr, self.i)
-        self.c0, self.c1 = shard.split_range(0, s, self.gc, tile=16)[self.j]
-        self.rows, self.cols = self.r1 - self.r0, self.c1 - self.c0
-        # pieces: (lo, hi, owner rank)
-        self.apieces = [(lo, hi, self.i * self.gc + k)
-                        for k, (lo, hi) in enumerate(shard.split_range(self.r0, self.r1, self.gc))]
-        self.bpieces = [(lo, hi, k * self.gc + self.j)
-                        for k, (lo, hi) in enumerate(shard.split_range(self.c0, self.c1, self.gr, tile=16))]
-        f64 = dict(dtype=torch.float64, device=self.dev)
-        self.a = [torch.empty((2, p, hi - lo, 2 * n), **f64) for lo, hi, _ in self.apieces]
-        self.ah_p = [torch.empty_like(t) for t in self.a]
-        self.b = [torch.empty((2, p, n, 2 * (hi - lo)), **f64) for lo, hi, _ in self.bpieces]
-        # Â block and B̂ pieces: carved out of `stage_buffer` (e.g. symmetric
-        # memory the group's owners store into) or allocated here
-        sizes = self.stage_sizes(m, n, s, p, world, (self.gr, self.gc))[rank]
-        if stage_buffer is None:
-            stage_buffer = torch.empty(sum(sizes), **f64)
-        assert stage_buffer.dtype == torch.float64 and stage_buffer.numel() >= sum(sizes)
-        self.stage_buffer = stage_buffer
-        self.ah = stage_buffer[:sizes[0]].view(2, p, self.rows, 2 * n)
-        self.bh, off = [], sizes[0]
-        for lo, hi, _ in self.bpieces:
-            e = 2 * p * n * 2 * (hi - lo)
-            self.bh.append(stage_buffer[off:off + e].view(2, p, n, 2 * (hi - lo)))
-            off += e
-        self.c = torch.empty((2, p, self.rows, 2 * self.cols), **f64)
-        self.L = _native.lib()
-        self.algo = self.L.qt_gemm_algo(m, n, s, p)
-        self.tables = None
-
-    @staticmethod
-    def stage_sizes(m: int, n: int, s: int, p: int, world: int, grid):
-        """Per rank: float64 elements of (its Â block, all its B̂ pieces)."""
-        gr, gc = grid
-        out = []
-        for r in range(world):
-            i, j = divmod(r, gc)
-            r0, r1 = shard.row_slab(m, gr, i)
-            c0, c1 = shard.split_range(0, s, gc, tile=16)[j]
-            out.append((2 * p * (r1 - r0) * 2 * n, 2 * p * n * 2 * (c1 - c0)))
-        return out
-
-    # ------------------------------------------------ broadcast fused into K1
-    # With every rank's stage buffer addressable (peer_bases, as seen from this
-    # GPU), an owner transforms its piece ONCE and K1's stores put every
-    # frequency row of it straight into the Â block (B̂ piece) of each rank of
-    # its row (column) group — qt_qfft3_conj_f64_device_routed_n, one table per
-    # destination — instead of broadcasting the raw piece for every rank of the
-    # group to transform again.
-    def set_peers(self, peer_bases) -> None:
-        torch, p, n = self.torch, self.p, self.n
-        sizes = self.stage_sizes(self.m, n, self.s, p, self.world, (self.gr, self.gc))
-        self.tables = {}
-        for k, (lo, hi, owner) in enumerate(self.apieces):
-            if owner != self.rank or hi == lo:
-                continue
-            dsts = [self.i * self.gc + jj for jj in range(self.gc)]
-            tab = [[peer_bases[d] + 16 * (((pl * p + r) * self.rows + (lo - self.r0)) * n)
-                    for d in dsts for r in range(p)] for pl in (0, 1)]
-            self.tables[("a", k)] = (torch.tensor(tab, dtype=torch.int64, device=self.dev), len(dsts))
-        for k, (lo, hi, owner) in enumerate(self.bpieces):
-            if owner != self.rank or hi == lo:
-                continue
-            dsts = [ii * self.gc + self.j for ii in range(self.gr)]
-            before = sum(2 * p * n * 2 * (h - l) for l, h, _ in self.bpieces[:k])
-            cols = hi - lo
-            tab = [[peer_bases[d] + 8 * (sizes[d][0] + before) + 16 * ((pl * p + r) * n * cols)
-                    for d in dsts for r in range(p)] for pl in (0, 1)]
-            self.tables[("b", k)] = (torch.tensor(tab, dtype=torch.int64, device=self.dev), len(dsts))
-
-    def k1_fused(self, stream=None) -> None:
-        """K1 of this rank's own pieces, stored into every rank of their groups."""
-        st = self.torch.cuda.current_stream() if stream is None else stream
-        for (kind, k), (tab, nd) in self.tables.items():
-            x = self.a[k] if kind == "a" else self.b[k]
-            lo, hi, _ = (self.apieces if kind == "a" else self.bpieces)[k]
-            rows, width = (hi - lo, self.n) if kind == "a" else (self.n, hi - lo)
-            _native.check(self.L.qt_qfft3_conj_f64_device_routed_n(
-                x[0].data_ptr(), x[1].data_ptr(), tab[0].data_ptr(), tab[1].data_ptr(), nd, rows, width, self.p,
-                st.cuda_stream), f"qfft3_conj routed ({kind} piece)")
-
-    def step_fused(self, barrier, stream=None) -> None:
-        """One step with the piece broadcasts fused into the owners' K1:
-        K1 of own pieces → barrier → stage 2 of every B̂ piece → barrier → K3
-        (the second barrier: no rank still reads the Â/B̂ the next K1 rewrites)."""
-        self.k1_fused(stream)
-        barrier()
-        self._stage2(stream)
-        barrier()
-        self._k3(stream)
-
-    # ---------------------------------------------------------------- inputs
-    def owns_a(self, k: int) -> bool:
-        return self.apieces[k][2] == self.rank
-
-    def owns_b(self, k: int) -> bool:
-        return self.bpieces[k][2] == self.rank
-
-    def load_a(self, a1: np.ndarray, a2: np.ndarray, owned_only: bool = True) -> None:
-        for k, (lo, hi, _) in enumerate(self.apieces):
-            if (owned_only and not self.owns_a(k)) or hi == lo:
-                continue
-            for t, src in enumerate((a1, a2)):
-                self.a[k][t].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, lo:hi]).view(np.float64)))
-
-    def load_b(self, b1: np.ndarray, b2: np.ndarray, owned_only: bool = True) -> None:
-        for k, (lo, hi, _) in enumerate(self.bpieces):
-            if (owned_only and not self.owns_b(k)) or hi == lo:
-                continue
-            for t, src in enumerate((b1, b2)):
-                self.b[k][t].copy_(self.torch.from_numpy(np.ascontiguousarray(src[:, :, lo:hi]).view(np.float64)))
-
-    # ----------------------------------------------------------------- step
-    def step(self, bcast_row=None, bcast_col=None, stream=None) -> None:
-        """One step.  bcast_row(tensor, src) / bcast_col(tensor, src) enqueue
-        an async broadcast from global rank `src` over this rank's row /
-        column group and return a Work (None: no peers in that group)."""
-        torch = self.torch
-        st = torch.cuda.current_stream() if stream is None else stream
-        sh = st.cuda_stream
-        L, n, p = self.L, self.n, self.p
-        wa = [bcast_row(t, o) if hi > lo else None for t, (lo, hi, o) in zip(self.a, self.apieces)] \
-            if bcast_row is not None else None
-        wb = [bcast_col(t, o) if hi > lo else None for t, (lo, hi, o) in zip(self.b, self.bpieces)] \
-            if bcast_col is not None else None
-        for k, (lo, hi, _) in enumerate(self.apieces):
-            if wa is not None and wa[k] is not None:
-                wa[k].wait()
-            if hi == lo:
-                continue
-            one = len(self.apieces) == 1
-            dst = self.ah if one else self.ah_p[k]
-            _native.check(L.qt_qfft3_conj_f64_device(self.a[k][0].data_ptr(), self.a[k][1].data_ptr(),
-                                                     dst[0].data_ptr(), dst[1].data_ptr(), hi - lo, n, p, sh),
-                          "qfft3_conj(A piece)")
-            if not one:
-                self.ah[:, :, lo - self.r0:hi - self.r0].copy_(self.ah_p[k])
-        self._stage2(stream, wb=wb, transform_b=True)
-        self._k3(stream)
-
-    def _stage2(self, stream=None, wb=None, transform_b=False) -> None:
-        """Stage 2 of every B̂ piece into its columns of the C block (after
-        transforming the arrived raw piece when transform_b)."""
-        torch = self.torch
-        st = torch.cuda.current_stream() if stream is None else stream
-        sh = st.cuda_stream
-        L, n, p = self.L, self.n, self.p
-        plan = None
-        if self.rows and self.algo == 1:
-            h = ctypes.c_void_p()
-            _native.check(L.qt_int8_plan_create(self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.rows, n, p, sh,
-                                                ctypes.byref(h)), "int8 plan")
-            plan = h
-        for k, (lo, hi, _) in enumerate(self.bpieces):
-            if wb is not None and wb[k] is not None:
-                wb[k].wait()
-            if hi == lo or not self.rows:
-                continue
-            cols = hi - lo
-            if transform_b:
-                _native.check(L.qt_qfft3_conj_f64_device(self.b[k][0].data_ptr(), self.b[k][1].data_ptr(),
-                                                         self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), n, cols,
-                                                         p, sh), "qfft3_conj(B piece)")
-            off = 16 * (lo - self.c0)
-            if plan is not None:
-                _native.check(L.qt_int8_plan_multiply(
-                    plan, self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(), self.c[0].data_ptr() + off,
-                    self.c[1].data_ptr() + off, cols, cols, self.cols, n * cols, self.rows * self.cols, sh),
-                    "int8 plan multiply")
-            else:
-                _native.check(L.qt_spectral_product_f64_device_ld_algo(
-                    self.ah[0].data_ptr(), self.ah[1].data_ptr(), self.bh[k][0].data_ptr(), self.bh[k][1].data_ptr(),
-                    self.c[0].data_ptr() + off, self.c[1].data_ptr() + off, self.rows, n, cols, p,
-                    cols, self.cols, n * cols, self.rows * self.cols, self.algo, sh), "spectral_product(piece)")
-        if plan is not None:
-            _native.check(L.qt_int8_plan_destroy(plan, sh), "int8 plan destroy")
-
-    def _k3(self, stream=None) -> None:
-        st = self.torch.cuda.current_stream() if stream is None else stream
-        if self.rows and self.cols:
-            _native.check(self.L.qt_qifft3_conj_f64_device(self.c[0].data_ptr(), self.c[1].data_ptr(),
-                                                           self.c[0].data_ptr(), self.c[1].data_ptr(), self.rows,
-                                                           self.cols, self.p, st.cuda_stream), "qifft3_conj(C block)")
-
-    def result(self):
-        """(c1, c2) of this rank's block as host complex128 (p, rows, cols)."""
-        out = self.c.cpu().numpy().view(np.complex128)
-        return out[0], out[1]
-
-
 class FreqParallelTProduct:
     """One rank's share of the frequency-parallel T-product (int8 stage 2).
 
@@ -367,10 +49,12 @@ class FreqParallelTProduct:
     whole row block of A and column block of B.
 
     Every slot is evaluated with the same kernels and arithmetic as the
-    single-GPU int8 product (row and column scalings depend on the slot's
-    own data only), so the stitched C is bitwise identical to it.  Inputs
-    holding inf/NaN are detected (nonfinite()) and rejected by result(): the
-    fp64 DMMA decomposition (Grid2DTProduct) handles those.
+    single-GPU int8 product (row and column scalings and the contraction
+    balancing depend on the slot's own data only), so the stitched C is
+    bitwise identical to it.  Inputs holding inf/NaN, and pairs the int8
+    accuracy guard does not certify, are recomputed by the fp64 DMMA kernels
+    on the compact slot tensors (qt_int8_slots_multiply), as in the
+    single-GPU product; nonfinite() reports the former.
     """
 
     def __init__(self, m: int, n: int, s: int, p: int, rank: int = 0, world: int = 1, device=None,
@@ -610,14 +294,12 @@ class FreqParallelTProduct:
         self.k3(stream)
 
     def nonfinite(self) -> bool:
-        """True if this rank's slots met an inf/NaN (its Ĉ was not written)."""
+        """True if this rank's slots met an inf/NaN (stage 2 of its slots then
+        ran on the fp64 DMMA kernels)."""
         return bool(self.flag.item())
 
     def result(self):
         """(c1, c2) of this rank's rows as host complex128 (p, rows, s)."""
-        if self.nonfinite():
-            raise FloatingPointError("frequency-parallel int8 product: non-finite input values; "
-                                     "use Grid2DTProduct (fp64 DMMA stage 2) for this product")
         out = self.c.cpu().numpy().view(np.complex128)
         return out[0], out[1]
 
@@ -679,40 +361,6 @@ def emulate_freq_parallel_routed(ranks) -> None:
         x.k2_multiply(x.k2_prepare())
     for x in ranks:
         x.k3_routed()
-
-
-def emulate_grid_fused(ranks) -> None:
-    """One step of G Grid2DTProduct instances (rank r = ranks[r]) with the
-    piece broadcasts fused into the owners' K1, in lockstep on one device: the
-    row tables point into the other instances' stage buffers, and lockstep
-    order stands in for the barriers."""
-    bases = [x.stage_buffer.data_ptr() for x in ranks]
-    for x in ranks:
-        if x.tables is None:
-            x.set_peers(bases)
-    for x in ranks:
-        x.k1_fused()
-    for x in ranks:
-        x._stage2()
-    for x in ranks:
-        x._k3()
-
-
-def make_peer_grid_stage(m: int, n: int, s: int, p: int, rank: int, world: int, grid, device, dist_mod,
-                         group=None):
-    """Symmetric-memory stage buffer for Grid2DTProduct, the peers' base
-    addresses and a device barrier (as make_peer_stage)."""
-    import torch
-    import torch.distributed._symmetric_memory as symm_mem
-    numel = max(sum(x) for x in Grid2DTProduct.stage_sizes(m, n, s, p, world, grid))
-    buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
-    hdl = symm_mem.rendezvous(buf, group if group is not None else dist_mod.group.WORLD)
-    bases = [int(x) for x in hdl.buffer_ptrs]
-
-    def barrier():
-        hdl.barrier(channel=0)
-
-    return buf, bases, barrier
 
 
 def emulate_freq_parallel(ranks) -> None:

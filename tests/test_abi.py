@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(L, s), s
         assert s in _native.SIGNATURES, f"{s} has no ctypes signature"
-    assert L.qt_abi_version() == 1
+    assert L.qt_abi_version() == 2
     assert L.qt_last_error() == b""
 
 
@@ -57,6 +57,37 @@ def test_generator_bitwise_equals_reference_generator():
         w1, w2 = O.gen_random_tensor(m, n, p, seed)
         assert np.array_equal(t.t1.view(np.uint64), w1.view(np.uint64))
         assert np.array_equal(t.t2.view(np.uint64), w2.view(np.uint64))
+
+
+def test_generator_distributions_equal_oracle_restatement():
+    """All three BASELINE input distributions (uniform, normal, pure-quaternion
+    RGB): the library's generator equals the oracle's restatement bitwise (the
+    reference arm of bench.py builds its inputs from the latter)."""
+    from paper_2212_14318_b200 import gen_tensor
+    for dist, scale in ((0, 1.0), (1, 1.0), (1, 1.0 / np.sqrt(1920.0)), (2, 1.0)):
+        for (m, n, p, seed) in [(4, 5, 3, 7), (1, 1, 1, 1), (17, 9, 6, 12345)]:
+            t = gen_tensor(m, n, p, seed, dist, scale)
+            w1, w2 = O.gen_tensor(dist, m, n, p, seed, scale)
+            assert np.array_equal(t.t1.view(np.uint64), w1.view(np.uint64)), (dist, m, n, p)
+            assert np.array_equal(t.t2.view(np.uint64), w2.view(np.uint64)), (dist, m, n, p)
+
+
+def test_config_table_is_standalone():
+    """bench.py's reference arm loads configs.py by path, without the product
+    package or its library: the module must not import either."""
+    import importlib.util
+    import subprocess
+    import sys
+    code = ("import importlib.util, sys\n"
+            "spec = importlib.util.spec_from_file_location('cfgs', %r)\n"
+            "m = importlib.util.module_from_spec(spec); sys.modules['cfgs'] = m; spec.loader.exec_module(m)\n"
+            "assert not any(k.startswith('paper_2212_14318_b200') for k in sys.modules)\n"
+            "print([m.CONFIGS[c].seeds() for c in (1, 5)])\n") % os.path.join(ROOT, "paper_2212_14318_b200",
+                                                                                 "configs.py")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    want = [CONFIGS[c].seeds() for c in (1, 5)]
+    assert r.stdout.strip() == str(want)
 
 
 def test_generator_rejects_zero_dims():

@@ -338,43 +338,16 @@ def test_linearity_at_full_size():
     assert O.rel_frob_error(as_pair(lhs), (r1.t1 + r2.t1, r1.t2 + r2.t2)) <= 1e-13
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("m,n,s,p", [(40, 24, 20, 12), (130, 33, 70, 16), (300, 64, 200, 64), (17, 16, 16, 4096),
                                      (64, 256, 512, 4)])
-def test_multi_driver_single_device_matches(m, n, s, p, fused, monkeypatch):
-    """qt_tprod_f64_multi on one device runs the whole pipeline — column chunks
-    of B transformed once by their owner and stored into every device's chunk
-    buffer by K1's routed stores (fused, peer access), or broadcast raw with
-    ncclBroadcast and transformed per device — then strided K2 and K3; it must
-    equal the single-GPU host path bitwise (the last shape takes the int8
-    stage 2 through a reused plan; p = 4096 is never fused)."""
-    monkeypatch.setenv("QTB_MULTI_FUSED", fused)
+def test_multi_driver_single_device_matches(m, n, s, p):
+    """qt_tprod_f64_multi on one device equals the single-GPU host path
+    bitwise (the last shape takes the int8 stage 2)."""
     a = qt.gen_random_tensor(m, n, p, 8)
     b = qt.gen_random_tensor(n, s, p, 9)
     c = qt.tprod_fast(a, b)
     cm = qt.tprod_fast_multi(a, b, [0])
     assert bits_equal(c.t1, cm.t1) and bits_equal(c.t2, cm.t2)
-
-
-@pytest.mark.parametrize("world,nchunks", [(1, 1), (1, 8), (2, 3), (3, 8), (8, 5)])
-def test_chunked_row_sharded_pipeline_bitwise(world, nchunks):
-    """The N > 1 bench/driver pipeline (K1 of the A slab, per-column-chunk K1 of
-    B + strided K2 into the C slab, one K3) run rank by rank on one GPU
-    (B loaded directly instead of broadcast) equals tprod_fast bitwise."""
-    import torch
-    from paper_2212_14318_b200.distributed import RowShardedTProduct
-    m, n, s, p = 150, 40, 70, 12
-    a = qt.gen_random_tensor(m, n, p, 31)
-    b = qt.gen_random_tensor(n, s, p, 32)
-    want = qt.tprod_fast(a, b)
-    for r in range(world):
-        sh = RowShardedTProduct(m, n, s, p, r, world, "cuda:0", nchunks=nchunks)
-        sh.load_a(a.t1, a.t2)
-        sh.load_b(b.t1, b.t2, owned_only=False)  # no peers here: this rank holds every chunk
-        sh.step()
-        torch.cuda.synchronize()
-        c1, c2 = sh.result()
-        assert bits_equal(c1, want.t1[:, sh.lo:sh.hi]) and bits_equal(c2, want.t2[:, sh.lo:sh.hi]), (world, r)
 
 
 def test_long_tube_sharding_bitwise():
@@ -474,60 +447,3 @@ def test_concurrent_host_calls_are_reentrant_and_bitwise():
     assert not errors, errors
     for w, g in zip(want, got):
         assert bits_equal(w.t1, g.t1) and bits_equal(w.t2, g.t2)
-
-
-@pytest.mark.parametrize("m,n,s,p,grid", [(150, 40, 70, 12, (2, 2)), (150, 40, 70, 12, (1, 3)), (97, 33, 50, 5, (3, 2)),
-                                          (150, 256, 520, 6, (4, 2)), (150, 256, 520, 6, (2, 2)),
-                                          (64, 288, 512, 4, (1, 1))])
-def test_grid2d_pipeline_bitwise(m, n, s, p, grid):
-    """The N > 1 bench pipeline (2-D blocks of C over a gr x gc grid: K1 of the A
-    row-block pieces, Â residues / stage 2 per B column-block piece, K3), run
-    rank by rank on one GPU with every piece loaded locally, stitches to
-    tprod_fast bitwise — DMMA and int8 stage 2."""
-    import torch
-    from paper_2212_14318_b200.distributed import Grid2DTProduct
-    a = qt.gen_random_tensor(m, n, p, 61)
-    b = qt.gen_random_tensor(n, s, p, 62)
-    want = qt.tprod_fast(a, b)
-    world = grid[0] * grid[1]
-    covered = np.zeros((m, s), bool)
-    for r in range(world):
-        g = Grid2DTProduct(m, n, s, p, r, world, "cuda:0", grid=grid)
-        g.load_a(a.t1, a.t2, owned_only=False)  # no peers: this rank holds every piece
-        g.load_b(b.t1, b.t2, owned_only=False)
-        g.step()
-        torch.cuda.synchronize()
-        c1, c2 = g.result()
-        assert bits_equal(c1, want.t1[:, g.r0:g.r1, g.c0:g.c1]), (grid, r)
-        assert bits_equal(c2, want.t2[:, g.r0:g.r1, g.c0:g.c1]), (grid, r)
-        covered[g.r0:g.r1, g.c0:g.c1] = True
-    assert covered.all()
-
-
-@pytest.mark.parametrize("m,n,s,p,grid", [(150, 40, 70, 12, (2, 2)), (150, 40, 70, 12, (1, 3)), (97, 33, 50, 5, (3, 2)),
-                                          (150, 256, 520, 6, (4, 2)), (64, 288, 512, 4, (1, 1)),
-                                          (120, 48, 64, 16, (4, 1))])
-def test_grid2d_fused_broadcast_bitwise(m, n, s, p, grid):
-    """The 2-D decomposition with the piece broadcasts fused into the owners'
-    K1 (routed stores into every group member's stage buffer; ranks emulated
-    in lockstep on one GPU): each block equals tprod_fast bitwise, twice
-    (the row tables are reused)."""
-    import torch
-    from paper_2212_14318_b200.distributed import Grid2DTProduct, emulate_grid_fused
-    a = qt.gen_random_tensor(m, n, p, 63)
-    b = qt.gen_random_tensor(n, s, p, 64)
-    want = qt.tprod_fast(a, b)
-    world = grid[0] * grid[1]
-    ranks = [Grid2DTProduct(m, n, s, p, r, world, "cuda:0", grid=grid) for r in range(world)]
-    for g in ranks:
-        g.load_a(a.t1, a.t2)  # owned pieces only: the rest arrives through the fused stores
-        g.load_b(b.t1, b.t2)
-    for _ in range(2):
-        for g in ranks:
-            g.c.fill_(float("nan"))
-        emulate_grid_fused(ranks)
-        torch.cuda.synchronize()
-        for g in ranks:
-            c1, c2 = g.result()
-            assert bits_equal(c1, want.t1[:, g.r0:g.r1, g.c0:g.c1]), (grid, g.rank)
-            assert bits_equal(c2, want.t2[:, g.r0:g.r1, g.c0:g.c1]), (grid, g.rank)

@@ -156,100 +156,6 @@ def test_column_chunk_plan():
     assert shard.column_chunks(0, 8, 2) == []
 
 
-def _worker_grid(rank, world, port, m, n, s, p, grid, out_path):
-    """2-D block decomposition (distributed.Grid2DTProduct's schedule) over gloo:
-    A row-block pieces broadcast over row groups, B column-block pieces over
-    column groups, each from its owner; each rank computes its C block."""
-    import sys
-    sys.path.insert(0, ROOT)
-    import oracle as O
-    from paper_2212_14318_b200 import shard
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    gr, gc = grid
-    i, j = divmod(rank, gc)
-    row_groups = [dist.new_group([ii * gc + k for k in range(gc)]) for ii in range(gr)]
-    col_groups = [dist.new_group([k * gc + jj for k in range(gr)]) for jj in range(gc)]
-    A = O.gen_random_tensor(m, n, p, 31)
-    B = O.gen_random_tensor(n, s, p, 32)
-    r0, r1 = shard.row_slab(m, gr, i)
-    c0, c1 = shard.split_range(0, s, gc, tile=16)[j]
-    apieces = [(lo, hi, i * gc + k) for k, (lo, hi) in enumerate(shard.split_range(r0, r1, gc))]
-    bpieces = [(lo, hi, k * gc + j) for k, (lo, hi) in enumerate(shard.split_range(c0, c1, gr, tile=16))]
-    abuf, bbuf = [], []
-    for lo, hi, own in apieces:
-        t = [np.zeros((p, hi - lo, n), np.complex128) for _ in range(2)]
-        if own == rank:
-            t[0][:] = A[0][:, lo:hi]
-            t[1][:] = A[1][:, lo:hi]
-        abuf.append(t)
-    for lo, hi, own in bpieces:
-        t = [np.zeros((p, n, hi - lo), np.complex128) for _ in range(2)]
-        if own == rank:
-            t[0][:] = B[0][:, :, lo:hi]
-            t[1][:] = B[1][:, :, lo:hi]
-        bbuf.append(t)
-    works = []
-    for (lo, hi, own), t in zip(apieces, abuf):
-        if gc > 1 and hi > lo:
-            works += [dist.broadcast(torch.from_numpy(x.view(np.float64)), own, group=row_groups[i], async_op=True)
-                      for x in t]
-    for (lo, hi, own), t in zip(bpieces, bbuf):
-        if gr > 1 and hi > lo:
-            works += [dist.broadcast(torch.from_numpy(x.view(np.float64)), own, group=col_groups[j], async_op=True)
-                      for x in t]
-    for w in works:
-        w.wait()
-    a_blk = (np.concatenate([t[0] for t in abuf], axis=1), np.concatenate([t[1] for t in abuf], axis=1))
-    b_blk = (np.concatenate([t[0] for t in bbuf], axis=2), np.concatenate([t[1] for t in bbuf], axis=2))
-    assert np.array_equal(a_blk[0], A[0][:, r0:r1]) and np.array_equal(b_blk[1], B[1][:, :, c0:c1])
-    c = O.tprod_fast(a_blk, b_blk)
-    mb = -(-m // gr)
-    sb = shard.split_range(0, s, gc, tile=16)[0][1]
-    buf = np.zeros((2, p, mb, sb), np.complex128)
-    buf[0, :, :r1 - r0, :c1 - c0] = c[0]
-    buf[1, :, :r1 - r0, :c1 - c0] = c[1]
-    tt = torch.from_numpy(buf.view(np.float64))
-    gathered = [torch.zeros_like(tt) for _ in range(world)] if rank == 0 else None
-    dist.gather(tt, gathered, dst=0)
-    if rank == 0:
-        c1o = np.zeros((p, m, s), np.complex128)
-        c2o = np.zeros((p, m, s), np.complex128)
-        for r, g in enumerate(gathered):
-            ii, jj = divmod(r, gc)
-            rr0, rr1 = shard.row_slab(m, gr, ii)
-            cc0, cc1 = shard.split_range(0, s, gc, tile=16)[jj]
-            gg = g.numpy().view(np.complex128)
-            c1o[:, rr0:rr1, cc0:cc1] = gg[0, :, :rr1 - rr0, :cc1 - cc0]
-            c2o[:, rr0:rr1, cc0:cc1] = gg[1, :, :rr1 - rr0, :cc1 - cc0]
-        np.savez(out_path, c1=c1o, c2=c2o)
-    dist.barrier()
-    dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("grid", [(2, 2), (1, 2)])
-def test_grid2d_piece_broadcasts(tmp_path, grid):
-    import oracle as O
-    m, n, s, p = 9, 5, 40, 6
-    world = grid[0] * grid[1]
-    out = str(tmp_path / "c.npz")
-    mp.spawn(_worker_grid, args=(world, _free_port(), m, n, s, p, grid, out), nprocs=world, join=True)
-    got = np.load(out)
-    want = O.tprod_fast(O.gen_random_tensor(m, n, p, 31), O.gen_random_tensor(n, s, p, 32))
-    assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
-    assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
-
-
-def test_grid_shape():
-    from paper_2212_14318_b200 import shard
-    assert shard.grid_shape(1, 2048, 2048) == (1, 1)
-    assert shard.grid_shape(2, 2048, 2048) == (2, 1)
-    assert shard.grid_shape(4, 2048, 2048) == (2, 2)
-    assert shard.grid_shape(8, 2048, 2048) == (4, 2)
-    assert shard.grid_shape(8, 1080, 64) == (8, 1)   # narrow B: plain row sharding
-
-
 def _cpu_freq_class():
     """FreqParallelTProduct with its three stages restated in numpy (the
     oracle's tube transforms; the paired per-frequency product of
@@ -403,44 +309,3 @@ def test_freq_parallel_routing_tables(m, n, s, p, world):
     for x in ranks:
         r0, r1 = shard.row_slab(m, world, x.rank)
         assert np.array_equal(x.c.numpy().view(np.uint64), want[:, :, r0:r1]), x.rank
-
-
-@pytest.mark.parametrize("m,n,s,p,grid", [(9, 5, 40, 6, (2, 2)), (9, 5, 40, 6, (1, 2)), (13, 4, 50, 5, (3, 2)),
-                                          (12, 3, 33, 4, (4, 1)), (7, 6, 20, 3, (1, 1))])
-def test_grid2d_fused_broadcast_tables(m, n, s, p, grid):
-    """The row tables of the 2-D decomposition's fused broadcasts
-    (Grid2DTProduct.set_peers): every owner's transformed piece (the oracle's
-    qfft3_conj), stored row by row to the addresses its tables give (a
-    memmove per destination standing in for the routed K1 stores), leaves in
-    every rank exactly the Â block and B̂ pieces it needs, bitwise."""
-    import ctypes
-    import oracle as O
-    from paper_2212_14318_b200 import distributed
-    A = O.gen_random_tensor(m, n, p, 45)
-    B = O.gen_random_tensor(n, s, p, 46)
-    Ah = O.qfft3_conj(A)
-    Bh = O.qfft3_conj(B)
-    world = grid[0] * grid[1]
-    ranks = [distributed.Grid2DTProduct(m, n, s, p, r, world, device="cpu", grid=grid) for r in range(world)]
-    bases = [x.stage_buffer.data_ptr() for x in ranks]
-    for x in ranks:
-        x.stage_buffer.fill_(float("nan"))
-    for x in ranks:
-        x.set_peers(bases)
-        for (kind, k), (tab, nd) in x.tables.items():
-            lo, hi, _ = (x.apieces if kind == "a" else x.bpieces)[k]
-            src = [np.ascontiguousarray(h[:, lo:hi]) for h in Ah] if kind == "a" else \
-                [np.ascontiguousarray(h[:, :, lo:hi]) for h in Bh]
-            for pl in (0, 1):
-                for d in range(nd):
-                    for f in range(p):
-                        row = src[pl][f]
-                        ctypes.memmove(int(tab[pl][d * p + f]), row.ctypes.data, row.nbytes)
-    for x in ranks:
-        ah = x.ah.numpy().view(np.complex128)
-        for pl in (0, 1):
-            assert np.array_equal(ah[pl].view(np.uint64), Ah[pl][:, x.r0:x.r1].view(np.uint64)), (grid, x.rank)
-        for k, (lo, hi, _) in enumerate(x.bpieces):
-            bh = x.bh[k].numpy().view(np.complex128)
-            for pl in (0, 1):
-                assert np.array_equal(bh[pl].view(np.uint64), Bh[pl][:, :, lo:hi].view(np.uint64)), (grid, x.rank, k)
