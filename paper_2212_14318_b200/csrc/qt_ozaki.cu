@@ -585,7 +585,16 @@ __device__ __forceinline__ int bal_delta(const int* __restrict__ bdel, int k, in
 }
 
 // bdel for the slot units of [f0, f0 + units): one warp per (unit, row j)
-// reads row j of both CD planes at both frequencies of the unit.
+// reads a fixed sample of row j — kBalSample columns at a stride spread over
+// the row (every column when s <= kBalSample) — of both CD planes at both
+// frequencies of the unit.  Any power-of-two D is exact, so a sample only has
+// to see the scale of the row (a row scaling of B, or the inverse of a column
+// scaling of A, shows in every column); whatever it misses costs accuracy
+// only, which the guard below certifies (else that pair goes to fp64).  The
+// sample is a function of the column index alone, so row slabs and compact
+// slot ranges see the same D.  (A 1/32 sample of config 5's B̂: 0.05 ms vs
+// 0.7 ms for every column.)
+constexpr int kBalSample = 64;
 __global__ void __launch_bounds__(256) oz_balance_b_kernel(const double2* __restrict__ b1,
                                                            const double2* __restrict__ b2, int* __restrict__ bdel,
                                                            int n, int s, int p, int f0, int ns, uint64_t ldb,
@@ -597,21 +606,18 @@ __global__ void __launch_bounds__(256) oz_balance_b_kernel(const double2* __rest
   unit_slots(blockIdx.y, f0, ns, p, sa, sb);
   const int ka = slot_freq(sa, p), kb = slot_freq(sb, p);
   const int la = slot_slice(sa, p, cbase), lb = slot_slice(sb, p, cbase);
+  const int stride = s <= kBalSample ? 1 : (s + kBalSample - 1) / kBalSample;
   int E = kNoExp;
+#pragma unroll
   for (int t = 0; t < 4; ++t) {
-    const double2* row = (t & 1 ? b2 : b1) + (size_t)(t < 2 ? la : lb) * bslice + (size_t)j * ldb;
     if (t >= 2 && la == lb) break;
-    constexpr int kU = 4;
-    for (int c0 = lane; c0 < s; c0 += 32 * kU) {
-      double2 y[kU];
+    const double2* row = (t & 1 ? b2 : b1) + (size_t)(t < 2 ? la : lb) * bslice + (size_t)j * ldb;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int c = c0 + 32 * u;
-        y[u] = c < s ? __ldcs(row + c) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const double mx = fmax(fabs(y[u].x), fabs(y[u].y));
+    for (int u = 0; u < kBalSample / 32; ++u) {
+      const int c = (lane + 32 * u) * stride;
+      if (c < s) {
+        const double2 y = __ldcs(row + c);
+        const double mx = fmax(fabs(y.x), fabs(y.y));
         // inf / nan: the colexp pass raises the non-finite flag; any d is fine then
         if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx));
       }
@@ -676,6 +682,8 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   const int i = blockIdx.x, f = blockIdx.y;
   const int slot = f0 + f;
   const int k = slot_freq(slot, p), sk = (p - k) % p;
+  // (no shared memory: this kernel runs beside the int8 GEMM's maximum-carveout CTAs)
+  const int* dk = bdel ? bdel + (size_t)k * n : nullptr;
   const int fpart = (k == sk) ? f : (f ^ 1);
   const int kq = slot_slice(slot, p, cbase), skq = slot_slice((k == sk) ? slot : (slot ^ 1), p, cbase);
   const double2* P = a1 + ((size_t)kq * m + i) * n;
@@ -688,7 +696,7 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
     const double2 x = P[j], y = Qr[j];
     const double mx = fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y)));
     bad |= !(fabs(x.x) + fabs(x.y) + fabs(y.x) + fabs(y.y) <= kDblMax);
-    if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx) - bal_delta(bdel, k, n, j));
+    if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx) - (dk ? __ldg(dk + j) : 0));
   }
   bad = __syncthreads_or(bad);
   E = block_max_int(E, ired);
@@ -704,7 +712,7 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
 #pragma unroll 4
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const double2 x = P[j], y = Qr[j];
-      const int sh = -bal_delta(bdel, k, n, j) - E;
+      const int sh = -(dk ? __ldg(dk + j) : 0) - E;
       const double a = scale2(x.x, sh), b = scale2(x.y, sh), c = scale2(y.x, sh), d = scale2(y.y, sh);
       ss = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ss))));
       l1 += (fabs(a) + fabs(b)) + (fabs(c) + fabs(d));
@@ -739,10 +747,12 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
     const int j0 = (isP ? u : u - nq) * kAVec;
     const double2* src = isP ? P : Qr;
     Limbs re[kAVec], im[kAVec];
+    const int4 d4 = dk ? __ldg(reinterpret_cast<const int4*>(dk + j0)) : make_int4(0, 0, 0, 0);  // (n % 32 == 0)
+    const int dv[kAVec] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
     for (int t = 0; t < kAVec; ++t) {
       const double2 x = src[j0 + t];
-      const int et = e - bal_delta(bdel, k, n, j0 + t);
+      const int et = e - dv[t];
       re[t] = to_limbs(x.x, et);
       im[t] = to_limbs(x.y, et);
     }
@@ -1018,7 +1028,7 @@ __device__ __forceinline__ double crt_value(uint64_t acc0, uint64_t acc1, uint64
 // CTA walks several rows and leaves its guard partial (weighted squared error
 // bound and |C|^2) in gpart[f][cta].
 constexpr int kCrtVec = 4;
-__global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
+__global__ void __launch_bounds__(256, 4) oz_crt_kernel(const uint8_t* __restrict__ R, const int* __restrict__ eA,
                                                      const double* __restrict__ xl1, const int* __restrict__ amin,
                                                      const int* __restrict__ eB, const double* __restrict__ yl1,
                                                      const int* __restrict__ bmin, const int* nonfinite,
@@ -1027,7 +1037,6 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
                                                      int bslot0, int Mp, int Sp, int F, uint64_t ldc, uint64_t cslice,
                                                      int cbase, int share_end) {
   if (*nonfinite) return;
-  __shared__ double red[8];
   const int cb = (blockIdx.x * blockDim.x + threadIdx.x) * kCrtVec;
   const int f = blockIdx.z;
   const bool active = cb < s;
@@ -1037,18 +1046,8 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
   // with the row exponents of the even partner's X'
   const bool sx = shares_x(f0 + f, share_end);
   const int fa = sx ? f - 1 : f;
-  const int a0 = amin[fa], b0 = bmin[bslot0 + f];
-  int eb[kCrtVec];
-  double yb[kCrtVec], wc[kCrtVec];  // column share of the element bound; column weight (0: exact column)
-  const double kq = 0.25 * (4.0 * n) + 0x1p42;
-#pragma unroll
-  for (int t = 0; t < kCrtVec; ++t) {
-    const int c = active ? min(cb + t, Sp - 1) : 0;
-    eb[t] = eB[(bslot0 + f) * Sp + c];
-    const double l = yl1[(bslot0 + f) * Sp + c];
-    yb[t] = 0.5 * l + kq;
-    wc[t] = (active && cb + t < s && l != 0.0) ? scale2(1.0, -2 * (eb[t] - b0)) : 0.0;
-  }
+  const int* ebs = eB + (bslot0 + f) * Sp;
+  const double* ybs = yl1 + (bslot0 + f) * Sp;
   double gsb = 0.0, gsc = 0.0;
   for (int r = blockIdx.y; r < 2 * m && active; r += gridDim.y) {
     const uint8_t* ptr = R + ((size_t)(f * Mp + r) * Sp + cb) * 2;
@@ -1080,48 +1079,74 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const uint8_t* __restrict__
     }
     const int ea = eA[fa * Mp + r];
     const double xr = xl1[fa * Mp + r];
-    const double xb = 0.5 * xr;
-    const double wr = xr != 0.0 ? scale2(1.0, -2 * (ea - a0)) : 0.0;  // (an all-zero row is exact)
+    // guard weight of the row (an all-zero row is exact: weight 0)
+    const double wr = xr != 0.0 ? scale2(1.0, -2 * (ea - amin[fa])) : 0.0;
+    const int b0 = bmin[bslot0 + f];
     double2* dst = ((r < m) != sx) ? c1 + k * cslice + (size_t)(sx ? r - m : r) * ldc
                                    : c2 + k * cslice + (size_t)(sx ? r : r - m) * ldc;
 #pragma unroll
     for (int t = 0; t < kCrtVec; ++t) {
       if (cb + t >= s) break;
-      const int e = -(ea + eb[t]);
+      const int ebt = ebs[cb + t];
+      const int e = -(ea + ebt);
       const double vr = crt_value(acc[t][0][0], acc[t][0][1], acc[t][0][2]);
       const double vi = crt_value(acc[t][1][0], acc[t][1][1], acc[t][1][2]);
       dst[cb + t] = make_double2(scale2(vr, e), scale2(vi, e));
-      const double w = wr * wc[t], bnd = xb + yb[t];  // per real part; |err|^2 <= 2 bnd^2
+      const double yl = ybs[cb + t];
+      const double w = yl != 0.0 ? wr * scale2(1.0, -2 * (ebt - b0)) : 0.0;  // (all-zero column: exact)
+      const double bnd = 0.5 * (xr + yl) + (0.25 * (4.0 * n) + 0x1p42);  // per real part; |err|^2 <= 2 bnd^2
       gsb = fma(2.0 * bnd * bnd, w, gsb);
       gsc = fma(fma(vr, vr, vi * vi), w, gsc);
     }
   }
-  gsb = block_sum(gsb, red);
-  gsc = block_sum(gsc, red);
-  if (threadIdx.x == 0)
-    gpart[(size_t)f * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = GuardAcc{gsb, gsc};
+  // per-warp partials (fixed shuffle tree; no block barrier)
+  for (int o = 16; o > 0; o >>= 1) {
+    gsb += __shfl_xor_sync(0xffffffffu, gsb, o);
+    gsc += __shfl_xor_sync(0xffffffffu, gsc, o);
+  }
+  if ((threadIdx.x & 31) == 0)
+    gpart[(((size_t)f * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8 + (threadIdx.x >> 5)] =
+        GuardAcc{gsb, gsc};
 }
 
-// Guard decision per slot unit of a batch: combine the CRT partials of the
-// unit's slot(s) in a fixed order and flag the pair for the DMMA recompute
-// unless sum bound^2 <= tol2 * sum |C|^2.
-__global__ void __launch_bounds__(256) oz_guard_kernel(const GuardAcc* __restrict__ gpart, int nper,
-                                                       const int* nonfinite, int* __restrict__ pair_flags, int p,
-                                                       int f0, int fcur, double tol2, int force) {
+// Guard decision per slot unit of a batch, in two deterministic passes:
+// oz_guard_sum_kernel reduces chunk c of the unit's CRT partials (both slots)
+// into gsum[unit][c]; oz_guard_kernel combines the kGuardChunks chunk sums in
+// a fixed order and flags the pair for the DMMA recompute unless
+// sum bound^2 <= tol2 * sum |C|^2.
+constexpr int kGuardChunks = 64;
+__global__ void __launch_bounds__(256) oz_guard_sum_kernel(const GuardAcc* __restrict__ gpart, int nper,
+                                                           const int* nonfinite, GuardAcc* __restrict__ gsum, int p,
+                                                           int f0, int fcur) {
+  __shared__ double red[8];
+  if (*nonfinite) return;
+  int sa, sb;
+  unit_slots(blockIdx.x, f0, fcur, p, sa, sb);
+  const int per = (sb - sa + 1) * nper;  // the unit's partials are contiguous (slots sa..sb)
+  const int chunk = (per + kGuardChunks - 1) / kGuardChunks;
+  const int i0 = blockIdx.y * chunk, i1 = min(per, i0 + chunk);
+  const GuardAcc* g = gpart + (size_t)(sa - f0) * nper;
+  double gsb = 0.0, gsc = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const GuardAcc v = g[i];
+    gsb += v.sb;
+    gsc += v.sc;
+  }
+  gsb = block_sum(gsb, red);
+  gsc = block_sum(gsc, red);
+  if (threadIdx.x == 0) gsum[blockIdx.x * kGuardChunks + blockIdx.y] = GuardAcc{gsb, gsc};
+}
+
+__global__ void __launch_bounds__(kGuardChunks) oz_guard_kernel(const GuardAcc* __restrict__ gsum,
+                                                                const int* nonfinite, int* __restrict__ pair_flags,
+                                                                int p, int f0, int fcur, double tol2, int force) {
   __shared__ double red[8];
   if (*nonfinite) return;  // everything is recomputed anyway
   int sa, sb;
   unit_slots(blockIdx.x, f0, fcur, p, sa, sb);
-  double gsb = 0.0, gsc = 0.0;
-  for (int sl = sa; sl <= sb; ++sl) {
-    const GuardAcc* g = gpart + (size_t)(sl - f0) * nper;
-    for (int i = threadIdx.x; i < nper; i += blockDim.x) {
-      gsb += g[i].sb;
-      gsc += g[i].sc;
-    }
-  }
-  gsb = block_sum(gsb, red);
-  gsc = block_sum(gsc, red);
+  const GuardAcc v = gsum[blockIdx.x * kGuardChunks + threadIdx.x];
+  const double gsb = block_sum(v.sb, red);
+  const double gsc = block_sum(v.sc, red);
   if (threadIdx.x == 0) {
     const bool ok = !force && gsc > 0.0 && gsc <= kDblMax && gsb <= tol2 * gsc;
     if (!ok) {
@@ -1372,14 +1397,14 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
   if (pipe && ps >= 8) F = std::min<uint64_t>(F, std::max<uint64_t>(2, ((ps + 3) / 4 + 1) & ~uint64_t(1)));
   const uint64_t nbatch = (ps + F - 1) / F;
   if (nbuf * F * Mp > 0x7fffffffULL || p * Mp > 0x7fffffffULL) return cudaErrorInvalidValue;
-  // CRT grid: each CTA walks ~2m/256 rows (its guard partial is one block reduction)
-  const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 256),
+  const dim3 cgrid((unsigned)((s + 256 * kCrtVec - 1) / (256 * kCrtVec)), (unsigned)std::min<uint64_t>(2 * m, 65535),
                    1);
-  const uint64_t nper = (uint64_t)cgrid.x * cgrid.y;  // guard partials per slot
+  const uint64_t nper = (uint64_t)cgrid.x * cgrid.y * 8;  // guard partials per slot (one per warp)
   const size_t bytesA = (size_t)kQ * nbuf * F * Mp * Kp, bytesR = (size_t)kQ * F * Mp * Sp * 2;
   const size_t offR = bytesA, offE = offR + nbuf * bytesR, offL = offE + ((nbuf * F * Mp * sizeof(int) + 255) & ~255ull);
   const size_t offG = offL + nbuf * F * Mp * sizeof(double);
-  const size_t offM = offG + F * nper * sizeof(GuardAcc);
+  const size_t offS = offG + F * nper * sizeof(GuardAcc);
+  const size_t offM = offS + F * kGuardChunks * sizeof(GuardAcc);
   const size_t wsbytes = offM + nbuf * F * sizeof(int);
   uint8_t* ws = nullptr;
   cudaError_t e = cudaMemsetAsync(flag + 1, 0, (p / 2 + 1) * sizeof(int), stream);
@@ -1389,6 +1414,7 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
   int* eA = reinterpret_cast<int*>(ws + offE);
   double* xl1 = reinterpret_cast<double*>(ws + offL);
   GuardAcc* gpart = reinterpret_cast<GuardAcc*>(ws + offG);
+  GuardAcc* gsum = reinterpret_cast<GuardAcc*>(ws + offS);
   int* amin = reinterpret_cast<int*>(ws + offM);  // smallest row exponent per X' slot (guard weights)
   const uint64_t aslots = nbuf * F;  // slots in the X' buffer (its plane stride)
   const int* bdel = balance_on() ? B.bdel : nullptr;
@@ -1457,10 +1483,13 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
     oz_crt_kernel<<<g, 256, 0, st>>>(ws + offR + b * bytesR, eA + b * F * Mp, xl1 + b * F * Mp, amin + b * F, B.eB,
                                      B.yl1, B.bmin, flag, gpart, ch1, ch2, (int)m, (int)n, (int)s, (int)p, (int)f0,
                                      bslot0, (int)Mp, (int)Sp, (int)F, ldc, cslice, B.cbase, share_end(p));
-    oz_guard_kernel<<<(unsigned)slot_units((int)f0, fcur, (int)p), 256, 0, st>>>(
-        gpart, (int)nper, flag, flag + 1, (int)p, (int)f0, fcur, guard_tol2(), guard_force() ? 1 : 0);
+    const unsigned units = (unsigned)slot_units((int)f0, fcur, (int)p);
+    oz_guard_sum_kernel<<<dim3(units, kGuardChunks), 256, 0, st>>>(gpart, (int)nper, flag, gsum, (int)p, (int)f0,
+                                                                   fcur);
+    oz_guard_kernel<<<units, kGuardChunks, 0, st>>>(gsum, flag, flag + 1, (int)p, (int)f0, fcur, guard_tol2(),
+                                                    guard_force() ? 1 : 0);
     pc.stop();
-    count_launches(2);
+    count_launches(3);
   };
   // batch 0's X' (and, lazily, its B' residues); without B.all its B' first
   if (e == cudaSuccess && !B.all) e = prep_b(B, bh1, bh2, B.s0, (int)std::min<uint64_t>(F, ps), 0, flag, stream);
