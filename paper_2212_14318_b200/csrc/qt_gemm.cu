@@ -241,10 +241,19 @@ __device__ __forceinline__ PairArgs pair_args(const double2* ah1, const double2*
 // (s0 < 0): u = k in [0, p/2], slices are frequencies.  Compact mode: the
 // operands hold the frequency slots [s0, s0 + ns) (slice t = slot s0 + t) and
 // u walks that range's pair / self-paired units (qt_int8_slots_*).
+// noreflect: the negative control of the parity tests ($QTB_DEBUG_NO_REFLECT=1):
+// sigma(k) = k instead of slice_reflect (tproduct.hpp:27-29), i.e. the
+// quaternion product treated as if j commuted with the complex scalars —
+// every frequency then runs as its own "pair" and parity must fail.
 struct PairMap {
   int s0 = -1, ns = 0;
+  int noreflect = 0;
 };
 __device__ __forceinline__ void map_unit(int u, const PairMap& M, int p, int& ka, int& kb, int& key) {
+  if (M.noreflect) {
+    ka = kb = key = u;
+    return;
+  }
   if (M.s0 < 0) {
     ka = u;
     kb = (p - u) % p;
@@ -407,7 +416,8 @@ cudaError_t launch_cfg(const double2* ah1, const double2* ah2, const double2* bh
                                 (int)C::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const uint64_t npairs = map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
+  const uint64_t npairs =
+      map.noreflect ? p : map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
   // a K that fits one stage (e.g. n <= 16 on the small tile) needs one buffer only
   const uint64_t ktiles = (n + C::BK - 1) / C::BK;
@@ -459,7 +469,8 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
   });
   if (attr_err != cudaSuccess) return attr_err;
   const uint64_t tiles = ((m + C::BM - 1) / C::BM) * ((s + C::BN - 1) / C::BN);
-  const uint64_t units = map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
+  const uint64_t units =
+      map.noreflect ? p : map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
   const uint64_t items = units * tiles;
   if (items == 0) return cudaSuccess;
   const uint64_t grid = std::min<uint64_t>(items, (uint64_t)std::max(1, per_sm) * sms);
@@ -500,11 +511,21 @@ static cudaError_t dmma_impl(const double2* ah1, const double2* ah2, const doubl
   return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, map);
 }
 
+static bool debug_noreflect() {
+  static const bool on = [] {
+    const char* e = getenv("QTB_DEBUG_NO_REFLECT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 cudaError_t dmma_spectral_gemm(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
                                double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                uint64_t ldb, uint64_t ldc, uint64_t bslice, uint64_t cslice, cudaStream_t stream,
                                const int* only_if) {
-  return dmma_impl(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, PairMap{});
+  PairMap map;
+  map.noreflect = (only_if == nullptr && debug_noreflect()) ? 1 : 0;
+  return dmma_impl(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, map);
 }
 
 cudaError_t dmma_spectral_gemm_slots(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
