@@ -7,10 +7,13 @@ override with --config {1..5}.  One step = one full T-product C = A *_T B
 (K1 tube FFT of A and B -> K2 paired-frequency GEMM -> K3 inverse tube FFT)
 over inputs already resident in HBM.  K2 runs as the exact int8 tcgen05
 product (Ozaki-II, csrc/qt_ozaki.cu) for wide products (configs 5 and larger)
-and on the fp64 DMMA tensor cores otherwise (qt_gemm_algo).  With N ranks (torchrun) the rows
-of A and C are sharded in slabs of ceil(m/N) and B's column chunks are
-broadcast with NCCL from the ranks that own them inside the timed step
-(strong scaling: total work fixed).
+and on the fp64 DMMA tensor cores otherwise (qt_gemm_algo).  With N ranks
+(torchrun, one process per GPU) the library's per-rank driver (csrc/qt_rank.cu,
+its own NCCL communicator) runs the step: --multi rows = the north_star split
+(rows of A and C in slabs, B broadcast once inside the timed step), --multi
+freq = frequency-parallel (NCCL send/recv of the transformed pieces inside
+the timed step, nothing replicated; the default for int8 products).  Strong
+scaling: total work fixed.
 
 metric value = F_eff / step time, F_eff = 32 m n s p + 10 (mn + ns + ms) p log2 p
 (SURVEY §8(d)).  e2e = the same metric through the host-buffer C-ABI call
@@ -77,17 +80,13 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tile", type=int, default=0, help="reference tile edge (0 = auto)")
-    ap.add_argument("--exchange", choices=["auto", "fused", "p2p"], default="auto",
-                    help="N > 1 exchange: fused = the transfers done by the tube FFTs' own stores/loads into "
-                         "the peers' stage buffers (symmetric memory over NVLink, two device barriers per step) — "
-                         "frequency-parallel: Â/B̂ stored by K1, Ĉ loaded by K3; 2-D grid: each piece transformed "
-                         "once by its owner and stored into its whole row/column group; p2p = NCCL (send/recv "
-                         "groups, piece broadcasts); auto = fused when available")
-    ap.add_argument("--multi", choices=["auto", "freq", "grid"], default="auto",
-                    help="N > 1 decomposition: freq = frequency-parallel (int8 stage 2), grid = 2-D blocks of C; "
-                         "auto = freq when the product takes the int8 stage 2")
+    ap.add_argument("--multi", choices=["auto", "rows", "freq"], default="auto",
+                    help="N > 1 decomposition (csrc/qt_rank.cu): rows = the north_star split (rows of A and C in "
+                         "slabs, B broadcast once with NCCL); freq = frequency-parallel (rows of A/B/C for the "
+                         "tube FFTs, frequency slots for stage 2, NCCL send/recv of the pieces, nothing "
+                         "replicated); auto = freq when the product takes the int8 stage 2, else rows")
     ap.add_argument("--sharded", action="store_true",
-                    help="use the N>1 row-sharded chunked-broadcast pipeline even on one GPU (no broadcast)")
+                    help="run the N > 1 per-rank driver even on one GPU (a one-rank NCCL communicator)")
     return ap.parse_args()
 
 
@@ -325,17 +324,13 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    elif args.sharded and args.exchange == "fused":  # the fused exchange on a one-rank group (exercise it on 1 GPU)
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29531")
-        dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
     L = qt._native.lib()
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
     lo, hi = shard.row_slab(cfg.m, world, rank)
     rows, cols = hi - lo, cfg.s  # this rank's block of C (whole C at N = 1)
-    mode = None
+    mode = "rows"
     k2_shape = None  # (rows, cols, frequencies) of this rank's stage 2, if not (rows, cols, p)
     # N = 1: pinned host inputs (the e2e leg copies from them); N > 1: every
     # rank regenerates A and B (sequential generator) and keeps the pieces it owns
@@ -357,98 +352,29 @@ def run_ours(args, cfg):
                                        dc1.data_ptr(), dc2.data_ptr(), rows, cfg.n, cfg.s, cfg.p, sh)
             qt._native.check(rc, "tprod_fast")
     else:
-        from paper_2212_14318_b200.distributed import FreqParallelTProduct, Grid2DTProduct, make_exchange
+        # one process per GPU: the library's per-rank driver (csrc/qt_rank.cu)
+        # owns the NCCL communicator and every transfer; each rank keeps only
+        # its inputs (its rows of A, and B on the root / its rows of B)
+        from paper_2212_14318_b200 import distributed
         mode = args.multi
         if mode == "auto":
-            mode = "freq" if FreqParallelTProduct.eligible(cfg.m, cfg.n, cfg.s, cfg.p) else "grid"
+            mode = "freq" if L.qt_gemm_algo(cfg.m, cfg.n, cfg.s, cfg.p) == 1 else "rows"
+        comm = distributed.RankComm(rank, world, local, dist if world > 1 else None)
+        cls = distributed.FreqTProduct if mode == "freq" else distributed.RowsTProduct
+        sharded = cls(comm, cfg.m, cfg.n, cfg.s, cfg.p)
+        sharded.load_a(a.t1, a.t2)
+        sharded.load_b(b.t1, b.t2)
         pin_own = []  # (device buffer, pinned host copy) this rank uploads on the e2e leg
-
-        def pin(t):
+        for t in sharded.owned():
             pt = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
             pt.copy_(t)
             pin_own.append((t, pt))
+        rows, cols = sharded.rows, cfg.s
+        if world > 1:
+            dist.barrier()
 
-        if mode == "freq":
-            # frequency-parallel: K1 of this rank's rows of A and B, Â/B̂ pieces
-            # point to point to the owners of their frequency slots, int8 stage 2
-            # of this rank's slots, Ĉ pieces back, K3 of this rank's rows of C
-            peer = None
-            if args.exchange != "p2p" and dist.is_initialized() and FreqParallelTProduct.routable(cfg.p):
-                try:
-                    from paper_2212_14318_b200.distributed import make_peer_stage
-                    peer = make_peer_stage(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev, dist)
-                except Exception as exc:  # no symmetric memory here: NCCL point-to-point instead
-                    if args.exchange == "fused":
-                        raise
-                    print(f"[bench] fused exchange unavailable ({type(exc).__name__}: {exc}); using p2p",
-                          file=sys.stderr)
-            exchange_kind = "fused" if peer is not None else "p2p"
-            sharded = FreqParallelTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev,
-                                           stage_buffer=peer[0] if peer else None)
-            sharded.load_a(a.t1, a.t2)
-            sharded.load_b(b.t1, b.t2)
-            pin(sharded.a)
-            pin(sharded.b)
-            exchange = make_exchange(rank, dist if world > 1 else None)
-            rows, cols = sharded.rows, cfg.s
-            if peer is not None:
-                sharded.set_peers(peer[1])
-            if world > 1:
-                dist.barrier()  # communicator up on every rank before the first point-to-point group
-
-            def step():
-                if peer is not None:
-                    sharded.step_routed(peer[2])
-                else:
-                    sharded.step(exchange)
-        else:
-            # 2-D blocks of C over a gr x gc grid of ranks: A's row block / B's column
-            # block arrive as pieces broadcast (NCCL) from their owners inside the
-            # step, overlapping K1 / stage 2 (paper_2212_14318_b200/distributed.py)
-            peer = None
-            if args.exchange != "p2p" and dist.is_initialized() and FreqParallelTProduct.routable(cfg.p):
-                try:
-                    from paper_2212_14318_b200.distributed import make_peer_grid_stage
-                    peer = make_peer_grid_stage(cfg.m, cfg.n, cfg.s, cfg.p, rank, world,
-                                                shard.grid_shape(world, cfg.m, cfg.s), dev, dist)
-                except Exception as exc:  # no symmetric memory here: NCCL broadcasts instead
-                    if args.exchange == "fused":
-                        raise
-                    print(f"[bench] fused broadcasts unavailable ({type(exc).__name__}: {exc}); using NCCL",
-                          file=sys.stderr)
-            exchange_kind = "fused" if peer is not None else "p2p"
-            sharded = Grid2DTProduct(cfg.m, cfg.n, cfg.s, cfg.p, rank, world, dev,
-                                     stage_buffer=peer[0] if peer else None)
-            gr, gc = sharded.gr, sharded.gc
-            sharded.load_a(a.t1, a.t2)
-            sharded.load_b(b.t1, b.t2)
-            for k, t in enumerate(sharded.a):
-                if sharded.owns_a(k):
-                    pin(t)
-            for k, t in enumerate(sharded.b):
-                if sharded.owns_b(k):
-                    pin(t)
-            rows, cols = sharded.rows, sharded.cols
-            bcast_row = bcast_col = None
-            if world > 1:
-                # every rank creates every group, in the same order
-                row_groups = [dist.new_group([i * gc + k for k in range(gc)]) for i in range(gr)]
-                col_groups = [dist.new_group([k * gc + j for k in range(gr)]) for j in range(gc)]
-                if gc > 1:
-                    bcast_row = lambda t, src: dist.broadcast(t, src, group=row_groups[sharded.i], async_op=True)
-                if gr > 1:
-                    bcast_col = lambda t, src: dist.broadcast(t, src, group=col_groups[sharded.j], async_op=True)
-
-            if peer is not None:
-                sharded.set_peers(peer[1])
-                if world > 1:
-                    dist.barrier()
-
-            def step():
-                if peer is not None:
-                    sharded.step_fused(peer[2])
-                else:
-                    sharded.step(bcast_row=bcast_row, bcast_col=bcast_col)
+        def step():
+            sharded.step()
         del a, b
         # stage-timing operands of this rank's block shape
         da1 = torch.randn((cfg.p, rows, 2 * cfg.n), dtype=torch.float64, device=dev)
@@ -456,8 +382,8 @@ def run_ours(args, cfg):
         db1 = torch.randn((cfg.p, cfg.n, 2 * cols), dtype=torch.float64, device=dev)
         db2 = torch.randn_like(db1)
         dc1, dc2 = sharded.c[0], sharded.c[1]
-        if mode == "freq":  # this rank's stage 2: all m x s of its ns frequency slots
-            k2_shape = (cfg.m, cfg.s, max(1, sharded.ns))
+        if mode == "freq":  # this rank's stage 2: all m x s of its frequency slots
+            k2_shape = (cfg.m, cfg.s, max(1, sharded.slot1 - sharded.slot0))
 
     # clocks are sampled from the first warm-up step through the per-kernel
     # timing loops, so short steps still yield samples under load
@@ -758,8 +684,8 @@ def run_ours(args, cfg):
         e2e = {"value": cfg.flops_eff / e2e_s / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.n) + cfg.bytes_tensor(cfg.n, cfg.s),
                "d2h_bytes_per_step": cfg.bytes_tensor(cfg.m, cfg.s), "ms_per_step": e2e_s * 1e3,
-               "api": "per rank: the pinned A/B pieces it owns H2D, NCCL broadcasts of the pieces over row/column groups, "
-                      "qt_* device pipeline, pinned C slab D2H; max over ranks"}
+               "api": "per rank: its pinned inputs H2D, the per-rank driver step (NCCL inside), its pinned rows "
+                      "of C D2H; max over ranks"}
 
     cpu = None
     if rank == 0 and not sharded_mode and not args.no_cpu_baseline:
@@ -781,12 +707,7 @@ def run_ours(args, cfg):
             "accuracy": accuracy,
             "fp64_dmma_path": dmma_path,
             "config": config_dict(cfg),
-            "parallelism": ((f"freq{world}(frequency slots; rows of A, B, C for the tube FFTs)"
-                             + ("+exchange fused into K1 stores / K3 loads (symmetric memory)"
-                                if exchange_kind == "fused" else "+NCCL point-to-point exchange")
-                             if mode == "freq" else "?")
-                            if sharded_mode else f"rows{world}")
-            + (" (sharded pipeline)" if args.sharded and world == 1 else ""),
+            "parallelism": (f"{mode}{world}" + (" (per-rank driver qt_rank_*, NCCL)" if sharded_mode else "")),
             "l2": "inputs > L2" if big else "L2 flushed (256 MB write) before each timed step",
             "flops_eff_per_step": cfg.flops_eff,
             "roofline": roof,

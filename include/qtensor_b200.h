@@ -243,13 +243,58 @@ int qt_qifft3_conj_f64_host(const double* x1, const double* x2,
 /* ---- single-process multi-GPU driver -----------------------------------
  * Host buffers in, host buffers out.  Rows of A and C are sharded in
  * contiguous slabs of ceil(m/ndev) rows over devices[0..ndev); B is copied
- * to devices[0] once and broadcast to the others with NCCL over NVLink.
- * ndev == 1 runs without NCCL.  Output is bitwise identical for every ndev. */
+ * to devices[0] once and broadcast to the others with NCCL over NVLink, then
+ * every device runs the single-GPU product of its slab (csrc/qt_multi.cu).
+ * ndev == 1 runs without NCCL.  Output is bitwise identical for every ndev;
+ * the caller's current device is restored. */
 int qt_tprod_f64_multi(const double* a1, const double* a2,
                        const double* b1, const double* b2,
                        double* c1, double* c2,
                        uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                        const int* devices, int ndev);
+
+/* ---- one process per GPU (torchrun): per-rank multi-GPU drivers ---------
+ * No reference counterpart (the reference is single-process,
+ * tproduct.cpp:75-111).  The library owns the NCCL communicator (NCCL is
+ * resolved at run time, csrc/qt_nccl.h); the launcher only moves the 128-byte
+ * id: rank 0 calls qt_comm_unique_id, every rank qt_comm_init with it (prints
+ * one "[qtensor_b200] NCCL x.y.z communicator: rank r of G on cuda:d" line).
+ * All device pointers below live on the rank's device, which must be current.
+ *
+ * Row split (the north_star decomposition, csrc/qt_rank.cu): the rank owns
+ * `rows` rows of A and C (a contiguous slab, qt_rank_partition); b1/b2 are
+ * n*s*p complex planes on every rank, holding B on `root` — broadcast in
+ * place (grouped ncclBroadcast per plane on `stream`), then the single-GPU
+ * product of the slab.  Bitwise equal to the rows of the one-GPU product.
+ *
+ * Frequency-parallel split: rank r passes its rows [a0, a1) of A, its rows
+ * [b0, b1) of B and receives its rows [a0, a1) of C (qt_rank_partition's
+ * out6 = {a0, a1, b0, b1, slot0, slot1}); stage 2 of the frequency slots
+ * [slot0, slot1) runs on this rank, the pieces move by NCCL send/recv.
+ * Bitwise equal to the one-GPU product.  qt_rank_freq_emulate runs `world`
+ * ranks in lockstep on the current device (pieces moved by device copies,
+ * same schedule) over whole-tensor device buffers: the single-GPU test of the
+ * decomposition. */
+int qt_comm_unique_id(void* id128);
+int qt_comm_init(const void* id128, int rank, int world, int device, void** comm);
+int qt_comm_destroy(void* comm);
+int qt_rank_partition(uint64_t m, uint64_t n, uint64_t p, int world, int rank, uint64_t* out6);
+/* host only: the frequency-parallel exchange schedule of `rank` for part 0 (Â),
+ * 1 (B̂) or 2 (Ĉ), its sends (send = 1) or receives, in transfer order: per
+ * piece {peer, slot, plane, first row, rows} (rows of the m- or n-row
+ * dimension).  count = number of pieces (out5 = NULL: count only). */
+int qt_rank_freq_schedule(uint64_t m, uint64_t n, uint64_t s, uint64_t p, int world, int rank, int part, int send,
+                          int64_t* out5, uint64_t cap, uint64_t* count);
+int qt_rank_tprod_rows(void* comm, const double* a1, const double* a2, double* b1, double* b2,
+                       double* c1, double* c2, uint64_t rows, uint64_t n, uint64_t s, uint64_t p,
+                       int root, void* stream);
+int qt_rank_freq_create(void* comm, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void** plan);
+int qt_rank_freq_step(void* plan, const double* a1, const double* a2, const double* b1, const double* b2,
+                      double* c1, double* c2, void* stream);
+int qt_rank_freq_nonfinite(void* plan, int* out);
+int qt_rank_freq_destroy(void* plan);
+int qt_rank_freq_emulate(int world, const double* a1, const double* a2, const double* b1, const double* b2,
+                         double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream);
 
 /* ---- QT3 tensor files <-> device planes ---------------------------------
  * The reference's binary format (tensor_io.hpp:16-20): "QT3\0", m, n, p as

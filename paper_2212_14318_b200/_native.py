@@ -52,6 +52,18 @@ SIGNATURES = {
     "qt_qfft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_qifft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_tprod_f64_multi": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
+    "qt_comm_unique_id": (ctypes.c_int, [_vp]),
+    "qt_comm_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "qt_comm_destroy": (ctypes.c_int, [_vp]),
+    "qt_rank_partition": (ctypes.c_int, [_u64, _u64, _u64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_u64)]),
+    "qt_rank_freq_schedule": (ctypes.c_int, [_u64] * 4 + [ctypes.c_int] * 4 + [ctypes.POINTER(ctypes.c_int64), _u64,
+                                                                           ctypes.POINTER(_u64)]),
+    "qt_rank_tprod_rows": (ctypes.c_int, [_vp] + [_dp] * 6 + [_u64] * 4 + [ctypes.c_int, _vp]),
+    "qt_rank_freq_create": (ctypes.c_int, [_vp] + [_u64] * 4 + [ctypes.POINTER(ctypes.c_void_p)]),
+    "qt_rank_freq_step": (ctypes.c_int, [_vp] + [_dp] * 6 + [_vp]),
+    "qt_rank_freq_nonfinite": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
+    "qt_rank_freq_destroy": (ctypes.c_int, [_vp]),
+    "qt_rank_freq_emulate": (ctypes.c_int, [ctypes.c_int] + [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_qt3_probe": (ctypes.c_int, [ctypes.c_char_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3),
     "qt_qt3_read_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),
     "qt_qt3_write_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),

@@ -1,15 +1,14 @@
-"""Row sharding of the T-product over ranks (one process per GPU).
+"""Partition rules of the multi-GPU T-product (one process per GPU).
 
 Row i of C = A *_T B depends only on row i of A and all of B (every slice
 product and every tube transform is row-local), so the rows of A
-and C are split into contiguous slabs of ceil(m / world) rows and B is
-replicated by broadcasts of its column chunks, each from the rank that owns
-(uploaded) it — the only exchange on the path.  The
-slab computation is the single-GPU pipeline unchanged, so the stitched result
-is bitwise identical to the one-GPU result for every world size.
+and C are split into contiguous slabs of ceil(m / world) rows (row split: B
+broadcast); stage 2 is independent per frequency pair, so the frequency-
+parallel split gives each rank a contiguous range of frequency slots.
 
-The same slab rule is used by the C++ single-process driver
-(qt_tprod_f64_multi, csrc/qt_multi.cu).
+These are restatements of the C++ drivers' rules (csrc/qt_rank.cu,
+csrc/qt_multi.cu) for the CPU tests; tests/test_multiproc_gloo.py checks the
+two agree (qt_rank_partition).
 """
 from __future__ import annotations
 
@@ -24,45 +23,6 @@ def row_slab(m: int, world: int, rank: int) -> tuple[int, int]:
     lo = min(m, rank * slab)
     hi = min(m, lo + slab)
     return lo, hi
-
-
-def column_chunks(s: int, nchunks: int, world: int, tile: int = 16) -> list[tuple[int, int, int]]:
-    """B's column chunks as (c0, c1, owner): ~nchunks chunks of a multiple of
-    `tile` columns, owned round-robin.  The owner of chunk j holds (uploads)
-    those columns of B and is the root of their broadcast, so with G ranks each
-    rank moves ~1/G of B over its PCIe link and its NVLink egress instead of
-    rank 0 moving all of it."""
-    q = -(-s // max(1, nchunks))
-    q = min(s, -(-q // tile) * tile) if s else 0
-    if q == 0:
-        return []
-    return [(c0, min(s, c0 + q), j % max(1, world)) for j, c0 in enumerate(range(0, s, q))]
-
-
-def split_range(lo: int, hi: int, parts: int, tile: int = 1) -> list[tuple[int, int]]:
-    """[lo, hi) in `parts` contiguous pieces of ceil(len/parts) rounded up to a
-    multiple of `tile` (trailing pieces may be empty)."""
-    n = hi - lo
-    q = -(-n // max(1, parts))
-    q = -(-q // tile) * tile if q else 0
-    return [(min(hi, lo + k * q), min(hi, lo + (k + 1) * q)) for k in range(parts)]
-
-
-def grid_shape(world: int, m: int, s: int) -> tuple[int, int]:
-    """(gr, gc) with gr * gc = world for the 2-D block decomposition of C.
-    Every rank of row group i needs the residues/transform of A's row block i
-    and every rank of column group j those of B's column block j, so the
-    per-rank replicated work is ~ m/gr + s/gc: minimise it (ties: more row
-    groups).  world = 2 gives (2, 1), i.e. plain row sharding."""
-    best = None
-    for gr in range(1, world + 1):
-        if world % gr:
-            continue
-        gc = world // gr
-        cost = m / gr + s / gc
-        if best is None or cost < best[0] - 1e-12 or (abs(cost - best[0]) <= 1e-12 and gr > best[1]):
-            best = (cost, gr, gc)
-    return best[1], best[2]
 
 
 def slot_freq(p: int, slot: int) -> int:

@@ -372,80 +372,6 @@ def test_int8_slot_ranges_nonfinite_and_rejection():
     assert flag == 0 and bits_equal(c.cpu().numpy()[:, 0], full[:, 3])
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_freq_parallel_emulated_bitwise(world):
-    """distributed.FreqParallelTProduct, `world` ranks emulated on one GPU in
-    lockstep (every exchanged piece moved by a device copy): each rank's rows
-    of C equal tprod_fast bitwise."""
-    import torch
-    from paper_2212_14318_b200.distributed import FreqParallelTProduct, emulate_freq_parallel
-    m, n, s, p = 150, 256, 520, 6
-    assert FreqParallelTProduct.eligible(m, n, s, p)
-    a = qt.gen_random_tensor(m, n, p, 91)
-    b = qt.gen_random_tensor(n, s, p, 92)
-    want = qt.tprod_fast(a, b)
-    ranks = [FreqParallelTProduct(m, n, s, p, r, world, "cuda:0") for r in range(world)]
-    for x in ranks:
-        x.load_a(a.t1, a.t2)
-        x.load_b(b.t1, b.t2)
-    emulate_freq_parallel(ranks)
-    torch.cuda.synchronize()
-    for x in ranks:
-        c1, c2 = x.result()
-        assert bits_equal(c1, want.t1[:, x.a0:x.a1]) and bits_equal(c2, want.t2[:, x.a0:x.a1]), (world, x.rank)
-
-
-@pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_freq_parallel_routed_emulated_bitwise(world):
-    """The frequency-parallel step with the exchange fused into K1/K3 (routed
-    row tables into the other ranks' stage buffers; emulated on one GPU in
-    lockstep): bitwise equal to tprod_fast, and to the point-to-point form."""
-    import torch
-    from paper_2212_14318_b200.distributed import FreqParallelTProduct, emulate_freq_parallel_routed
-    m, n, s, p = 150, 256, 520, 6
-    assert FreqParallelTProduct.routable(p)
-    a = qt.gen_random_tensor(m, n, p, 91)
-    b = qt.gen_random_tensor(n, s, p, 92)
-    want = qt.tprod_fast(a, b)
-    ranks = [FreqParallelTProduct(m, n, s, p, r, world, "cuda:0") for r in range(world)]
-    for x in ranks:
-        x.load_a(a.t1, a.t2)
-        x.load_b(b.t1, b.t2)
-    for _ in range(2):  # the tables are reused across steps
-        emulate_freq_parallel_routed(ranks)
-        torch.cuda.synchronize()
-        for x in ranks:
-            c1, c2 = x.result()
-            assert bits_equal(c1, want.t1[:, x.a0:x.a1]) and bits_equal(c2, want.t2[:, x.a0:x.a1]), (world, x.rank)
-
-
-def test_freq_parallel_single_rank_step_and_nonfinite():
-    import torch
-    from paper_2212_14318_b200.distributed import FreqParallelTProduct
-    m, n, s, p = 140, 256, 512, 5
-    a = qt.gen_random_tensor(m, n, p, 93)
-    b = qt.gen_random_tensor(n, s, p, 94)
-    want = qt.tprod_fast(a, b)
-    x = FreqParallelTProduct(m, n, s, p, 0, 1, "cuda:0")
-    x.load_a(a.t1, a.t2)
-    x.load_b(b.t1, b.t2)
-    x.step()
-    torch.cuda.synchronize()
-    c1, c2 = x.result()
-    assert bits_equal(c1, want.t1) and bits_equal(c2, want.t2)
-    # non-finite input: the slots are recomputed by the fp64 kernels, like the
-    # single-GPU product (same DMMA arithmetic per element)
-    b1 = b.t1.copy()
-    b1[2, 3, 4] = float("inf")
-    x.load_b(b1, b.t2)
-    x.step()
-    torch.cuda.synchronize()
-    assert x.nonfinite()
-    c1, c2 = x.result()
-    want = qt.tprod_fast(a, qt.CdTensor3(n, s, p, b1, b.t2))
-    assert np.array_equal(c1, want.t1, equal_nan=True) and np.array_equal(c2, want.t2, equal_nan=True)
-
-
 @pytest.mark.parametrize("env", [{"QTB_OZAKI_SHAREX": "0"}, {"QTB_RESB_COLS": "32"}, {"QTB_OZAKI_2SM": "0"}])
 def test_implementation_switches_bitwise(tmp_path, env):
     """The int8 stage 2 is the same integer computation whatever the layout

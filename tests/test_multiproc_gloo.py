@@ -79,150 +79,114 @@ def test_row_sharded_world2_equals_single(tmp_path, m, n, s, p):
     assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
 
 
-def _worker_chunks(rank, world, port, m, n, s, p, nchunks, out_path):
-    """B in column chunks owned round-robin (shard.column_chunks): each rank
-    fills only the chunks it owns, every chunk is broadcast from its owner,
-    then each rank computes its C slab — the N > 1 bench pipeline's schedule."""
-    import sys
-    sys.path.insert(0, ROOT)
+def _freq_rank_cpu(m, n, s, p, world, rank, A, B, exchange):
+    """One frequency-parallel rank with the LIBRARY's partition and exchange
+    schedule (qt_rank_partition / qt_rank_freq_schedule, csrc/qt_rank.cu) and
+    its buffers laid out as the C++ driver's, the stages restated on the CPU
+    (the oracle's tube transforms; the paired per-frequency product of SURVEY
+    §8(a) in complex arithmetic).  `exchange(sends, recvs)` moves the pieces
+    (lists of (peer, array view) in transfer order)."""
     import oracle as O
-    from paper_2212_14318_b200 import shard
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    a = O.gen_random_tensor(m, n, p, 21)
-    lo, hi = shard.row_slab(m, world, rank)
-    a_slab = shard.take_rows(a[0], a[1], lo, hi)
-    b_full = O.gen_random_tensor(n, s, p, 22)
-    plan = shard.column_chunks(s, nchunks, world, tile=1)
-    assert len(plan) >= 1 and plan[0][0] == 0 and plan[-1][1] == s
-    bufs = []
-    for (c0, c1, owner) in plan:
-        t1 = np.zeros((p, n, c1 - c0), np.complex128)
-        t2 = np.zeros((p, n, c1 - c0), np.complex128)
-        if owner == rank:  # only the owner holds (uploads) this chunk
-            t1[:] = b_full[0][:, :, c0:c1]
-            t2[:] = b_full[1][:, :, c0:c1]
-        bufs.append((t1, t2, owner))
-    works = []
-    for (t1, t2, owner) in bufs:
-        for t in (t1, t2):
-            works.append(dist.broadcast(torch.from_numpy(t.view(np.float64)), src=owner, async_op=True))
-    for w in works:
-        w.wait()
-    b1 = np.concatenate([t1 for t1, _, _ in bufs], axis=2)
-    b2 = np.concatenate([t2 for _, t2, _ in bufs], axis=2)
-    assert np.array_equal(b1.view(np.uint64), b_full[0].view(np.uint64))
-    assert np.array_equal(b2.view(np.uint64), b_full[1].view(np.uint64))
-    c = O.tprod_fast(a_slab, (b1, b2))
-    slab = -(-m // world)
-    buf = np.zeros((2, p, slab, s), np.complex128)
-    buf[0, :, :hi - lo] = c[0]
-    buf[1, :, :hi - lo] = c[1]
-    t = torch.from_numpy(buf.view(np.float64))
-    gathered = [torch.zeros_like(t) for _ in range(world)] if rank == 0 else None
-    dist.gather(t, gathered, dst=0)
-    if rank == 0:
-        c1 = np.zeros((p, m, s), np.complex128)
-        c2 = np.zeros((p, m, s), np.complex128)
-        for r, g in enumerate(gathered):
-            lo_r, hi_r = shard.row_slab(m, world, r)
-            gg = g.numpy().view(np.complex128)
-            c1[:, lo_r:hi_r] = gg[0, :, :hi_r - lo_r]
-            c2[:, lo_r:hi_r] = gg[1, :, :hi_r - lo_r]
-        np.savez(out_path, c1=c1, c2=c2)
-    dist.barrier()
-    dist.destroy_process_group()
+    from paper_2212_14318_b200 import distributed, shard
+    a0, a1, b0, b1, t0, t1 = distributed.partition(m, n, p, world, rank)
+    ra, rb, ns = a1 - a0, b1 - b0, t1 - t0
+    ah = np.zeros((2, p, ra, n), np.complex128)
+    bh = np.zeros((2, p, rb, s), np.complex128)
+    ac = np.zeros((2, ns, m, n), np.complex128)
+    bc = np.zeros((2, ns, n, s), np.complex128)
+    cc = np.zeros((2, ns, m, s), np.complex128)
+    c = np.zeros((2, p, ra, s), np.complex128)
+    if rb:
+        bh[0], bh[1] = O.qfft3_conj((np.ascontiguousarray(B[0][:, b0:b1]), np.ascontiguousarray(B[1][:, b0:b1])))
+    if ra:
+        ah[0], ah[1] = O.qfft3_conj((np.ascontiguousarray(A[0][:, a0:a1]), np.ascontiguousarray(A[1][:, a0:a1])))
+
+    def views(part, send):
+        out = []
+        for peer, slot, pl, r0, rows in distributed.schedule(m, n, s, p, world, rank, part, send):
+            k = shard.slot_freq(p, slot)
+            if (part == "c") != send:  # this side holds rows of every frequency
+                buf = {"a": ah, "b": bh, "c": c}[part]
+                v = buf[pl, k]
+                assert v.shape[0] == rows
+            else:  # this side owns the slot
+                buf = {"a": ac, "b": bc, "c": cc}[part]
+                v = buf[pl, slot - t0, r0:r0 + rows]
+            out.append((peer, v))
+        return out
+
+    exchange(views("b", True), views("b", False))
+    exchange(views("a", True), views("a", False))
+    for t in range(t0, t1):
+        k = shard.slot_freq(p, t)
+        sk = (p - k) % p
+        part = t if sk == k else t ^ 1
+        i, j = t - t0, part - t0
+        cc[0, i] = ac[0, i] @ bc[0, i] - np.conj(ac[1, j]) @ bc[1, i]
+        cc[1, i] = ac[1, i] @ bc[0, i] + np.conj(ac[0, j]) @ bc[1, i]
+    exchange(views("c", True), views("c", False))
+    if ra:
+        c[0], c[1] = O.qifft3_conj((c[0], c[1]))
+    return a0, a1, c
 
 
-@pytest.mark.parametrize("m,n,s,p,nchunks", [(9, 5, 7, 8, 3), (4, 3, 5, 6, 8)])
-def test_owner_rooted_chunk_broadcast_world2(tmp_path, m, n, s, p, nchunks):
-    import oracle as O
-    out = str(tmp_path / "c.npz")
-    mp.spawn(_worker_chunks, args=(2, _free_port(), m, n, s, p, nchunks, out), nprocs=2, join=True)
-    got = np.load(out)
-    want = O.tprod_fast(O.gen_random_tensor(m, n, p, 21), O.gen_random_tensor(n, s, p, 22))
-    assert np.array_equal(got["c1"].view(np.uint64), want[0].view(np.uint64))
-    assert np.array_equal(got["c2"].view(np.uint64), want[1].view(np.uint64))
-
-
-def test_column_chunk_plan():
-    from paper_2212_14318_b200 import shard
-    plan = shard.column_chunks(2048, 8, 8)
-    assert [o for _, _, o in plan] == list(range(8)) and all(c1 - c0 == 256 for c0, c1, _ in plan)
-    plan = shard.column_chunks(70, 8, 3)
-    assert plan[0][0] == 0 and plan[-1][1] == 70 and all((c1 - c0) % 16 == 0 or c1 == 70 for c0, c1, _ in plan)
-    assert [o for _, _, o in plan] == [j % 3 for j in range(len(plan))]
-    assert shard.column_chunks(0, 8, 2) == []
-
-
-def _cpu_freq_class():
-    """FreqParallelTProduct with its three stages restated in numpy (the
-    oracle's tube transforms; the paired per-frequency product of
-    csrc/qt_ozaki.cu in complex arithmetic) and its exchange schedule as is."""
-    import oracle as O
-    from paper_2212_14318_b200 import distributed
-
-    def cview(t):
-        return t.numpy().view(np.complex128)
-
-    class CpuFreq(distributed.FreqParallelTProduct):
-        def k1(self, stream=None):
-            if self.b1 > self.b0:
-                y = O.qfft3_conj((cview(self.b[0]), cview(self.b[1])))
-                cview(self.bh[0])[:], cview(self.bh[1])[:] = y
-            if self.rows:
-                y = O.qfft3_conj((cview(self.a[0]), cview(self.a[1])))
-                cview(self.ah[0])[:], cview(self.ah[1])[:] = y
-
-        def k2_prepare(self, stream=None):
-            return True if self.ns else None
-
-        def k2_multiply(self, h, stream=None):
-            if h is None:
-                return
-            A1, A2, B1, B2 = cview(self.ac[0]), cview(self.ac[1]), cview(self.bc[0]), cview(self.bc[1])
-            C1, C2 = cview(self.cc[0]), cview(self.cc[1])
-            for t in range(self.s0, self.s1):
-                k = self.freq[t]
-                part = t if (self.p - k) % self.p == k else t ^ 1
-                i, j = t - self.s0, part - self.s0
-                C1[i] = A1[i] @ B1[i] - np.conj(A2[j]) @ B2[i]
-                C2[i] = A2[i] @ B1[i] + np.conj(A1[j]) @ B2[i]
-
-        def k3(self, stream=None):
-            if self.rows:
-                y = O.qifft3_conj((cview(self.c[0]), cview(self.c[1])))
-                cview(self.c[0])[:], cview(self.c[1])[:] = y
-
-    return CpuFreq
+def _local_exchange(rank):
+    def ex(sends, recvs):
+        src = [v for peer, v in sends if peer == rank]
+        dst = [v for peer, v in recvs if peer == rank]
+        assert len(src) == len(dst) == len(sends) == len(recvs)
+        for a, b in zip(src, dst):
+            b[...] = a
+    return ex
 
 
 def _worker_freq(rank, world, port, m, n, s, p, out_path):
-    """distributed.FreqParallelTProduct's exchange over gloo point-to-point
-    ops (make_exchange), stages on the CPU: Â/B̂ row pieces to the slot
-    owners, Ĉ pieces back to the row owners."""
+    """The frequency-parallel schedule of csrc/qt_rank.cu over gloo
+    point-to-point ops (the C++ driver's NCCL send/recv groups), stages on the
+    CPU: Â/B̂ row pieces to the slot owners, Ĉ pieces back to the row owners."""
     import sys
     sys.path.insert(0, ROOT)
     import oracle as O
-    from paper_2212_14318_b200 import distributed, shard
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     A = O.gen_random_tensor(m, n, p, 41)
     B = O.gen_random_tensor(n, s, p, 42)
-    x = _cpu_freq_class()(m, n, s, p, rank, world, device="cpu")
-    x.load_a(*A)
-    x.load_b(*B)
-    x.step(distributed.make_exchange(rank, dist))
-    c = x.c.numpy().view(np.complex128)
+
+    def exchange(sends, recvs):
+        for peer, v in sends:
+            assert v.flags["C_CONTIGUOUS"]
+        local = _local_exchange(rank)
+        ls = [(q, v) for q, v in sends if q == rank]
+        lr = [(q, v) for q, v in recvs if q == rank]
+        local(ls, lr)
+        ops, keep = [], []
+        for q, v in sends:
+            if q != rank:
+                t = torch.from_numpy(v.view(np.float64).reshape(-1))
+                keep.append(t)
+                ops.append(dist.P2POp(dist.isend, t, q))
+        rbufs = []
+        for q, v in recvs:
+            if q != rank:
+                t = torch.empty(v.size * 2, dtype=torch.float64)
+                rbufs.append((t, v))
+                ops.append(dist.P2POp(dist.irecv, t, q))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for t, v in rbufs:
+            v[...] = t.numpy().view(np.complex128).reshape(v.shape)
+
+    a0, a1, c = _freq_rank_cpu(m, n, s, p, world, rank, A, B, exchange)
     mb = -(-m // world)
     buf = np.zeros((2, p, mb, s), np.complex128)
-    buf[:, :, :x.rows] = c
+    buf[:, :, :a1 - a0] = c
     tt = torch.from_numpy(buf.view(np.float64))
     gathered = [torch.zeros_like(tt) for _ in range(world)] if rank == 0 else None
     dist.gather(tt, gathered, dst=0)
     if rank == 0:
+        from paper_2212_14318_b200 import shard
         out = np.zeros((2, p, m, s), np.complex128)
         for r, g in enumerate(gathered):
             r0, r1 = shard.row_slab(m, world, r)
@@ -232,22 +196,52 @@ def _worker_freq(rank, world, port, m, n, s, p, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,n,s,p,world", [(9, 5, 6, 8, 2), (7, 3, 4, 7, 2), (5, 6, 3, 4, 3), (3, 2, 2, 2, 2)])
+@pytest.mark.parametrize("m,n,s,p,world", [(9, 5, 6, 8, 2), (7, 3, 4, 7, 2), (5, 6, 3, 4, 3), (3, 2, 2, 2, 2),
+                                           (11, 4, 5, 6, 4)])
 def test_freq_parallel_exchange(tmp_path, m, n, s, p, world):
+    """The library's frequency-parallel partition + schedule, executed over
+    gloo by `world` processes, stitches to the one-rank result bitwise (every
+    slot is computed identically) and to the reference within 1e-13."""
     import oracle as O
     out = str(tmp_path / "c.npy")
     mp.spawn(_worker_freq, args=(world, _free_port(), m, n, s, p, out), nprocs=world, join=True)
     got = np.load(out)
     A = O.gen_random_tensor(m, n, p, 41)
     B = O.gen_random_tensor(n, s, p, 42)
-    # the same stages on one rank: bitwise (every slot is computed identically)
-    one = _cpu_freq_class()(m, n, s, p, 0, 1, device="cpu")
-    one.load_a(*A)
-    one.load_b(*B)
-    one.step()
-    assert np.array_equal(got.view(np.uint64), one.c.numpy().view(np.uint64))
+    _, _, one = _freq_rank_cpu(m, n, s, p, 1, 0, A, B, _local_exchange(0))
+    assert np.array_equal(got.view(np.uint64), one.view(np.uint64))
     want = O.tprod_fast(A, B)
     assert O.rel_frob_error((got[0], got[1]), want) < 1e-13
+
+
+def test_library_partition_equals_shard_rules():
+    """qt_rank_partition (C++) and shard.row_slab / shard.slot_ranges agree."""
+    from paper_2212_14318_b200 import distributed, shard
+    for m, n, p in [(2048, 2048, 32), (1080, 1920, 64), (16, 16, 4096), (9, 5, 8), (3, 7, 1), (5, 2, 2), (1, 1, 9)]:
+        for world in (1, 2, 3, 4, 5, 8):
+            for r in range(world):
+                a0, a1, b0, b1, t0, t1 = distributed.partition(m, n, p, world, r)
+                assert (a0, a1) == shard.row_slab(m, world, r)
+                assert (b0, b1) == shard.row_slab(n, world, r)
+                assert (t0, t1) == shard.slot_ranges(p, world)[r], (m, n, p, world, r)
+
+
+def test_library_schedule_pairs_every_piece():
+    """Every send of the library's schedule has exactly one matching receive
+    (same peer pair, position and size), for every part and world."""
+    from paper_2212_14318_b200 import distributed
+    for m, n, s, p in [(9, 5, 6, 8), (2, 3, 4, 7), (5, 6, 3, 1), (13, 4, 5, 6)]:
+        for world in (1, 2, 3, 4):
+            for part in "abc":
+                snd = [distributed.schedule(m, n, s, p, world, r, part, True) for r in range(world)]
+                rcv = [distributed.schedule(m, n, s, p, world, r, part, False) for r in range(world)]
+                for src in range(world):
+                    for dst in range(world):
+                        a = [x for x in snd[src] if x[0] == dst]
+                        b = [x for x in rcv[dst] if x[0] == src]
+                        assert len(a) == len(b), (m, n, s, p, world, part, src, dst)
+                        for x, y in zip(a, b):
+                            assert x[1:3] == y[1:3] and x[4] == y[4]
 
 
 def test_slot_ranges_keep_pairs_whole():
@@ -261,51 +255,3 @@ def test_slot_ranges_keep_pairs_whole():
             assert all(not (b & 1 and b < pair_end) for r in rs for b in r)
             sizes = [t1 - t0 for t0, t1 in rs]
             assert max(sizes) - min(sizes) <= 2, (p, world, rs)
-
-
-@pytest.mark.parametrize("m,n,s,p,world", [(9, 5, 6, 8, 2), (7, 3, 4, 7, 3), (5, 6, 3, 4, 3), (11, 4, 5, 6, 4),
-                                           (3, 2, 2, 2, 2), (6, 4, 3, 5, 1)])
-def test_freq_parallel_routing_tables(m, n, s, p, world):
-    """The row tables of the fused exchange (FreqParallelTProduct.set_peers):
-    every rank's frequency rows of Â/B̂, stored to the addresses its tables
-    give (a memmove per row stands in for the routed K1 stores into the
-    peers' stage buffers), and its rows of Ĉ, loaded from the addresses of
-    its K3 table, reproduce the point-to-point exchange — so the stitched C
-    equals the one-rank product bitwise."""
-    import ctypes
-    import oracle as O
-    from paper_2212_14318_b200 import shard
-    A = O.gen_random_tensor(m, n, p, 43)
-    B = O.gen_random_tensor(n, s, p, 44)
-    cls = _cpu_freq_class()
-    ranks = [cls(m, n, s, p, r, world, device="cpu") for r in range(world)]
-    bases = [x.stage_buffer.data_ptr() for x in ranks]
-    for x in ranks:
-        x.load_a(*A)
-        x.load_b(*B)
-        x.set_peers(bases)
-        x.k1()  # into x.ah / x.bh, then "stored" row by row through the tables
-        for key, src in (("a", x.ah), ("b", x.bh)):
-            rowbytes = src[0, 0].numel() * 8
-            if rowbytes == 0:
-                continue
-            for pl in (0, 1):
-                for k in range(p):
-                    ctypes.memmove(int(x.tables[key][pl][k]), src[pl, k].data_ptr(), rowbytes)
-    for x in ranks:
-        x.k2_multiply(x.k2_prepare())
-    for x in ranks:
-        rowbytes = x.c[0, 0].numel() * 8
-        if rowbytes:
-            for pl in (0, 1):
-                for k in range(p):
-                    ctypes.memmove(x.c[pl, k].data_ptr(), int(x.tables["c"][pl][k]), rowbytes)
-        x.k3()
-    one = cls(m, n, s, p, 0, 1, device="cpu")
-    one.load_a(*A)
-    one.load_b(*B)
-    one.step()
-    want = one.c.numpy().view(np.uint64)
-    for x in ranks:
-        r0, r1 = shard.row_slab(m, world, x.rank)
-        assert np.array_equal(x.c.numpy().view(np.uint64), want[:, :, r0:r1]), x.rank

@@ -1,5 +1,6 @@
 // FP64 peak probe for B200 (sm_100a): DMMA (mma.sync f64) and DFMA throughput.
 // Used to fill the P64 roofline denominator (MEASURED_PEAKS.json has no fp64 figure).
+#include <chrono>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -101,5 +102,24 @@ int main() {
   run(dfma_loop<8>, sms * 4, 256, it, 8 * 32 * 2.0, "dfma x8", d);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("clockRate attr = %d kHz\n", clk);
+  // sustained: the best burst shape back to back for ~4 s (clocks settle under the power cap)
+  {
+    const int blocks = sms * 4, threads = 256, iters = 65536;
+    const double fl = (double)blocks * threads / 32 * iters * 8 * 512.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    long launches = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    cudaEventRecord(e0);
+    while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 4.0) {
+      for (int k = 0; k < 4; ++k) dmma_m8n8k4<8><<<blocks, threads>>>(d, iters);
+      launches += 4;
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+    }
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("%-28s sustained launches=%ld  %8.1f ms  %7.2f TFLOP/s\n", "dmma m8n8k4 x8acc", launches, ms,
+           fl * launches / (ms * 1e-3) / 1e12);
+  }
   return 0;
 }
