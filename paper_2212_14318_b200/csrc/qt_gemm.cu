@@ -511,7 +511,7 @@ static cudaError_t dmma_impl(const double2* ah1, const double2* ah2, const doubl
   return launch_cfg<BigCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc, bslice, cslice, stream, only_if, map);
 }
 
-static bool debug_noreflect() {
+bool debug_noreflect() {
   static const bool on = [] {
     const char* e = getenv("QTB_DEBUG_NO_REFLECT");
     return e && e[0] == '1';

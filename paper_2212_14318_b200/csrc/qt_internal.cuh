@@ -180,6 +180,9 @@ cudaError_t dmma_spectral_gemm_slots(const double2* ah1, const double2* ah2, con
                                      double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
                                      int s0, int ns, cudaStream_t stream, const int* only_if);
 
+// $QTB_DEBUG_NO_REFLECT=1: sigma(k) = k in stage 2 (the parity tests' negative control)
+bool debug_noreflect();
+
 // Definitional product C_k = sum_r A_{(k-r) mod p} (.) B_r (qt_naive.cu).
 cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,
                                double2* c1, double2* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
