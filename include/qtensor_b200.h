@@ -227,6 +227,15 @@ int qt_tprod_f64_host(const double* a1, const double* a2,
                       double* c1, double* c2,
                       uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device);
 
+/* tprod_fast that also returns Â, B̂, Ĉ (each m*n / n*s / m*s * p complex per
+ * plane, host buffers): the reference's TProdWorkspace side effect
+ * (tproduct.cpp:80-87, ws.ahat / ws.bhat / ws.chat), used by the drop-in when
+ * $QTB_DROPIN_FILL_WS=1.  C equals qt_tprod_f64_host's. */
+int qt_tprod_f64_host_spectra(const double* a1, const double* a2, const double* b1, const double* b2,
+                              double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device,
+                              double* ahat1, double* ahat2, double* bhat1, double* bhat2,
+                              double* chat1, double* chat2);
+
 int qt_tprod_naive_f64_host(const double* a1, const double* a2,
                             const double* b1, const double* b2,
                             double* c1, double* c2,

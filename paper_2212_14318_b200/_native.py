@@ -49,6 +49,7 @@ SIGNATURES = {
     "qt_tprod_naive_f64_device": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [_vp]),
     "qt_tprod_naive_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),
     "qt_tprod_f64_host": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int]),
+    "qt_tprod_f64_host_spectra": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.c_int] + [_dp] * 6),
     "qt_qfft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_qifft3_conj_f64_host": (ctypes.c_int, [_dp] * 4 + [_u64] * 3 + [ctypes.c_int]),
     "qt_tprod_f64_multi": (ctypes.c_int, [_dp] * 6 + [_u64] * 4 + [ctypes.POINTER(ctypes.c_int), ctypes.c_int]),

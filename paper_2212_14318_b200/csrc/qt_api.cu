@@ -1150,6 +1150,63 @@ int qt_tprod_f64_host(const double* a1, const double* a2, const double* b1, cons
   return tprod_host_impl(a1, a2, b1, b2, c1, c2, m, n, s, p, hc);
 }
 
+// tprod_fast with the reference's workspace side effect (tproduct.cpp:80-87:
+// after a call ws.ahat / ws.bhat / ws.chat hold Â, B̂, Ĉ): the device
+// pipeline with each stage's output also copied back to the caller's host
+// buffers.  The stages are the product's own kernels, so C is the same as
+// qt_tprod_f64_host's (for sizes whose host path does not stream).
+int qt_tprod_f64_host_spectra(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
+                              double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int device, double* ah1,
+                              double* ah2, double* bh1, double* bh2, double* ch1, double* ch2) {
+  t_err.clear();
+  int rc = check_dims(m, n, s, p, "tprod_fast");
+  if (rc) return rc;
+  HostCall hc;
+  if ((rc = hc.begin(device))) return rc;
+  const size_t ab = m * n * p * sizeof(double2), bb = n * s * p * sizeof(double2), cb = m * s * p * sizeof(double2);
+  char* d = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&d, 4 * ab + 4 * bb + 2 * cb + 64, hc.st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(host call)");
+  double* da1 = (double*)d;
+  double* da2 = (double*)(d + ab);
+  double* dh1 = (double*)(d + 2 * ab);
+  double* dh2 = (double*)(d + 3 * ab);
+  double* db1 = (double*)(d + 4 * ab);
+  double* db2 = (double*)(d + 4 * ab + bb);
+  double* dk1 = (double*)(d + 4 * ab + 2 * bb);
+  double* dk2 = (double*)(d + 4 * ab + 3 * bb);
+  double* dc1 = (double*)(d + 4 * ab + 4 * bb);
+  double* dc2 = (double*)(d + 4 * ab + 4 * bb + cb);
+  if (ab) rc = h2d(da1, a1, ab, hc.st);
+  if (!rc && ab) rc = h2d(da2, a2, ab, hc.st);
+  if (!rc && bb) rc = h2d(db1, b1, bb, hc.st);
+  if (!rc && bb) rc = h2d(db2, b2, bb, hc.st);
+  if (!rc && m && n) rc = transform_device_impl(false, da1, da2, dh1, dh2, m, n, p, hc.st);
+  if (!rc && n && s) rc = transform_device_impl(false, db1, db2, dk1, dk2, n, s, p, hc.st);
+  if (!rc && ab) rc = d2h(ah1, dh1, ab, hc.st);
+  if (!rc && ab) rc = d2h(ah2, dh2, ab, hc.st);
+  if (!rc && bb) rc = d2h(bh1, dk1, bb, hc.st);
+  if (!rc && bb) rc = d2h(bh2, dk2, bb, hc.st);
+  if (!rc && cb) {
+    if (n == 0) {
+      if ((e = cudaMemsetAsync(dc1, 0, 2 * cb, hc.st)) != cudaSuccess) rc = cuda_fail(e, "memset");
+    } else if ((e = launch_spectral_gemm((const double2*)dh1, (const double2*)dh2, (const double2*)dk1,
+                                         (const double2*)dk2, (double2*)dc1, (double2*)dc2, m, n, s, p, hc.st)) !=
+               cudaSuccess) {
+      rc = cuda_fail(e, "K2 paired spectral GEMM");
+    }
+  }
+  if (!rc && cb) rc = d2h(ch1, dc1, cb, hc.st);
+  if (!rc && cb) rc = d2h(ch2, dc2, cb, hc.st);
+  if (!rc && cb && n) rc = transform_device_impl(true, dc1, dc2, dc1, dc2, m, s, p, hc.st);  // (n = 0: C = 0, as tprod_fast)
+  if (!rc && cb) rc = d2h(c1, dc1, cb, hc.st);
+  if (!rc && cb) rc = d2h(c2, dc2, cb, hc.st);
+  cudaFreeAsync(d, hc.st);
+  e = cudaStreamSynchronize(hc.st);
+  if (!rc && e != cudaSuccess) rc = cuda_fail(e, "tprod_fast (host) sync");
+  return rc;
+}
+
 int qt_tprod_naive_f64_device(const double* a1, const double* a2, const double* b1, const double* b2, double* c1,
                               double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream) {
   t_err.clear();

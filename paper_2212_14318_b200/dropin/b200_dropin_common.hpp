@@ -16,6 +16,13 @@ inline int device() {
   return env && *env ? std::atoi(env) : 0;
 }
 
+// $QTB_DROPIN_FILL_WS=1: tprod_fast(a, b, ws) leaves Â, B̂, Ĉ in ws as the
+// reference does (tproduct.cpp:80-87); off by default (nothing reads them back)
+inline bool fill_workspace() {
+  const char* env = std::getenv("QTB_DROPIN_FILL_WS");
+  return env && *env == '1';
+}
+
 // QT_EINVAL -> std::invalid_argument (what the reference throws), anything else
 // -> std::runtime_error.  There is no CPU fallback: a missing GPU is an error.
 inline void check(int rc, const char* who) {

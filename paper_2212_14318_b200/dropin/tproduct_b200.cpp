@@ -72,15 +72,28 @@ CdTensor3 tprod_naive(const CdTensor3& a, const CdTensor3& b) {
   return c;
 }
 
-// FFT-domain T-product on the B200 (tproduct.hpp:35-46).  The transformed
-// operands live in stream-ordered device scratch, so `ws` is accepted for
-// signature compatibility and left untouched; repeated calls (with or without
-// a workspace) are bitwise identical, the property test_tproduct.cpp:118-128
-// pins.
+// FFT-domain T-product on the B200 (tproduct.hpp:35-46).  By default the
+// transformed operands live in stream-ordered device scratch and `ws` is left
+// untouched (no caller in the reference reads it back; the copies would cost
+// three extra PCIe transfers); with $QTB_DROPIN_FILL_WS=1 the call leaves Â,
+// B̂ and Ĉ in ws.ahat / ws.bhat / ws.chat exactly as the reference does
+// (tproduct.cpp:80-87), from the product's own kernels
+// (qt_tprod_f64_host_spectra).  Repeated calls (with or without a workspace)
+// are bitwise identical, the property test_tproduct.cpp:118-128 pins.
 CdTensor3 tprod_fast(const CdTensor3& a, const CdTensor3& b, TProdWorkspace& ws) {
-  (void)ws;
   if (a.n != b.m || a.p != b.p) throw std::invalid_argument("tprod_fast: dimension mismatch");
   CdTensor3 c(a.m, b.n, a.p);
+  if (b200::fill_workspace()) {
+    ws.ahat = CdTensor3(a.m, a.n, a.p);
+    ws.bhat = CdTensor3(b.m, b.n, b.p);
+    ws.chat = CdTensor3(a.m, b.n, a.p);
+    b200::check(qt_tprod_f64_host_spectra(b200::dp(a.t1), b200::dp(a.t2), b200::dp(b.t1), b200::dp(b.t2),
+                                          b200::dp(c.t1), b200::dp(c.t2), a.m, a.n, b.n, a.p, b200::device(),
+                                          b200::dp(ws.ahat.t1), b200::dp(ws.ahat.t2), b200::dp(ws.bhat.t1),
+                                          b200::dp(ws.bhat.t2), b200::dp(ws.chat.t1), b200::dp(ws.chat.t2)),
+                "tprod_fast");
+    return c;
+  }
   b200::check(qt_tprod_f64_host(b200::dp(a.t1), b200::dp(a.t2), b200::dp(b.t1), b200::dp(b.t2), b200::dp(c.t1),
                                 b200::dp(c.t2), a.m, a.n, b.n, a.p, b200::device()),
               "tprod_fast");

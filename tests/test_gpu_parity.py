@@ -80,6 +80,32 @@ def test_workspace_reuse_bitwise():  # test_tproduct.cpp:118-128
         assert bits_equal(c1.t1, c2.t1) and bits_equal(c1.t2, c2.t2)
 
 
+@pytest.mark.parametrize("m,n,s,p", [(4, 3, 5, 8), (24, 16, 20, 12), (40, 256, 520, 5), (3, 0, 2, 4)])
+def test_workspace_spectra_like_reference(m, n, s, p):
+    """qt_tprod_f64_host_spectra (the drop-in with $QTB_DROPIN_FILL_WS=1):
+    Â, B̂, Ĉ come back like the reference's ws (tproduct.cpp:80-87) — Â, B̂
+    equal the reference's qfft3_conj within 1e-13, Ĉ inverse-transforms to C
+    — and C is qt_tprod_f64_host's, bitwise (the int8 shape included)."""
+    L = _native.lib()
+    a = qt.gen_random_tensor(m, max(n, 1), p, 5) if n else qt.CdTensor3(m, 0, p)
+    b = qt.gen_random_tensor(max(n, 1), s, p, 6) if n else qt.CdTensor3(0, s, p)
+    c = qt.CdTensor3(m, s, p)
+    ah, bh, ch = qt.CdTensor3(m, n, p), qt.CdTensor3(n, s, p), qt.CdTensor3(m, s, p)
+    ptr = lambda x: x.ctypes.data
+    _native.check(L.qt_tprod_f64_host_spectra(ptr(a.t1), ptr(a.t2), ptr(b.t1), ptr(b.t2), ptr(c.t1), ptr(c.t2), m, n,
+                                              s, p, 0, ptr(ah.t1), ptr(ah.t2), ptr(bh.t1), ptr(bh.t2), ptr(ch.t1),
+                                              ptr(ch.t2)), "tprod spectra")
+    want = qt.tprod_fast(a, b)
+    assert bits_equal(c.t1, want.t1) and bits_equal(c.t2, want.t2)
+    if n:
+        assert O.rel_frob_error((ah.t1, ah.t2), O.qfft3_conj((a.t1, a.t2))) <= 1e-13
+        assert O.rel_frob_error((bh.t1, bh.t2), O.qfft3_conj((b.t1, b.t2))) <= 1e-13
+        back = qt.qifft3_conj(ch)
+        assert bits_equal(back.t1, c.t1) and bits_equal(back.t2, c.t2)
+    else:
+        assert not np.any(ch.t1) and not np.any(c.t1)
+
+
 def test_real_inputs_match_per_slice_spectral_product():  # test_tproduct.cpp:130-166
     rng = RefRng(17)
     m, n, s, p = 3, 2, 4, 6
