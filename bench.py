@@ -95,6 +95,10 @@ def parse_args():
                          "slabs, B broadcast once with NCCL); freq = frequency-parallel (rows of A/B/C for the "
                          "tube FFTs, frequency slots for stage 2, NCCL send/recv of the pieces, nothing "
                          "replicated); auto = freq when the product takes the int8 stage 2, else rows")
+    ap.add_argument("--exchange", choices=["nccl", "fused"], default="nccl",
+                    help="frequency-parallel exchange: nccl = send/recv groups; fused = K1 stores / K3 loads "
+                         "straight into / from the peers' stage buffers (CUDA IPC over NVLink, the library's "
+                         "device barrier; not yet run on more than one GPU)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the N > 1 per-rank driver even on one GPU (a one-rank NCCL communicator)")
     return ap.parse_args()
@@ -380,6 +384,13 @@ def run_ours(args, cfg):
         comm = distributed.RankComm(rank, world, local, dist if world > 1 else None)
         cls = distributed.FreqTProduct if mode == "freq" else distributed.RowsTProduct
         sharded = cls(comm, cfg.m, cfg.n, cfg.s, cfg.p)
+        if mode == "freq" and args.exchange == "fused":
+            handles = [None] * world
+            if world > 1:
+                dist.all_gather_object(handles, sharded.ipc_handle())
+            else:
+                handles = [sharded.ipc_handle()]
+            sharded.set_peers(handles)
         sharded.load_a(a.t1, a.t2)
         sharded.load_b(b.t1, b.t2)
         pin_own = []  # (device buffer, pinned host copy) this rank uploads on the e2e leg
@@ -730,7 +741,10 @@ def run_ours(args, cfg):
             "accuracy": accuracy,
             "fp64_dmma_path": dmma_path,
             "config": config_dict(cfg),
-            "parallelism": (f"{mode}{world}" + (" (per-rank driver qt_rank_*, NCCL)" if sharded_mode else "")),
+            "parallelism": (f"{mode}{world}" + ((" (per-rank driver qt_rank_*, " +
+                                                   ("exchange fused into K1 stores / K3 loads over peer memory)"
+                                                    if mode == "freq" and args.exchange == "fused" else "NCCL)"))
+                                                  if sharded_mode else "")),
             "l2": "inputs > L2" if big else "L2 flushed before each timed step (256 MB write, then a 256 MB read so no "
                                             "dirty line is written back inside the step)",
             "flops_eff_per_step": cfg.flops_eff,

@@ -302,8 +302,25 @@ int qt_rank_freq_step(void* plan, const double* a1, const double* a2, const doub
                       double* c1, double* c2, void* stream);
 int qt_rank_freq_nonfinite(void* plan, int* out);
 int qt_rank_freq_destroy(void* plan);
-int qt_rank_freq_emulate(int world, const double* a1, const double* a2, const double* b1, const double* b2,
-                         double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream);
+int qt_rank_freq_emulate(int world, int fused, const double* a1, const double* a2, const double* b1,
+                         const double* b2, double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                         void* stream);
+/* Fused exchange over peer memory (NVLink): each rank exports its stage
+ * buffer (qt_rank_freq_ipc_handle, 64 bytes), the launcher gathers all of them
+ * in rank order and every rank calls qt_rank_freq_set_peers: from then on a
+ * step's K1 stores each frequency row straight into its slot owner's buffer
+ * and K3 loads its rows straight from the owners (routed transforms), with the
+ * library's own device barrier between the phases — no messages.  Lengths
+ * whose transform is one launch only (qt_fft_routable).  qt_rank_freq_create_ipc
+ * makes a plan without an NCCL communicator (fused exchange only);
+ * qt_rank_freq_phase runs phase 0 (routed K1), 1 (stage 2), 2 (routed K3)
+ * without the device barriers, for callers that order the ranks themselves. */
+int qt_rank_freq_create_ipc(int rank, int world, int device, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                            void** plan);
+int qt_rank_freq_ipc_handle(void* plan, void* handle64);
+int qt_rank_freq_set_peers(void* plan, const void* handles);
+int qt_rank_freq_phase(void* plan, int phase, const double* a1, const double* a2, const double* b1,
+                       const double* b2, double* c1, double* c2, void* stream);
 
 /* ---- QT3 tensor files <-> device planes ---------------------------------
  * The reference's binary format (tensor_io.hpp:16-20): "QT3\0", m, n, p as

@@ -64,7 +64,11 @@ SIGNATURES = {
     "qt_rank_freq_step": (ctypes.c_int, [_vp] + [_dp] * 6 + [_vp]),
     "qt_rank_freq_nonfinite": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
     "qt_rank_freq_destroy": (ctypes.c_int, [_vp]),
-    "qt_rank_freq_emulate": (ctypes.c_int, [ctypes.c_int] + [_dp] * 6 + [_u64] * 4 + [_vp]),
+    "qt_rank_freq_emulate": (ctypes.c_int, [ctypes.c_int, ctypes.c_int] + [_dp] * 6 + [_u64] * 4 + [_vp]),
+    "qt_rank_freq_create_ipc": (ctypes.c_int, [ctypes.c_int] * 3 + [_u64] * 4 + [ctypes.POINTER(ctypes.c_void_p)]),
+    "qt_rank_freq_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "qt_rank_freq_set_peers": (ctypes.c_int, [_vp, _vp]),
+    "qt_rank_freq_phase": (ctypes.c_int, [_vp, ctypes.c_int] + [_dp] * 6 + [_vp]),
     "qt_qt3_probe": (ctypes.c_int, [ctypes.c_char_p] + [ctypes.POINTER(ctypes.c_uint64)] * 3),
     "qt_qt3_read_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),
     "qt_qt3_write_f64_device": (ctypes.c_int, [ctypes.c_char_p, _dp, _dp] + [_u64] * 3 + [_vp]),

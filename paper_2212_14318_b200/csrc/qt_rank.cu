@@ -91,7 +91,15 @@ struct FreqRank {
   double2* bc = nullptr;  // (2, ns, n, s)
   double2* cc = nullptr;  // (2, ns, m, s)
   int* nonfinite = nullptr;
+  uint64_t* sig = nullptr;  // kMaxWorld barrier slots (fused exchange), in buf so peers can address them
   void* buf = nullptr;
+  // fused exchange (qt_rank_freq_set_peers): the peers' buffers mapped here,
+  // device row tables of the routed transforms, the peers' signal slots
+  bool fused = false;
+  std::vector<void*> peer_buf;      // peer j's buffer as seen from this device (own: buf)
+  std::vector<bool> peer_opened;    // opened through cudaIpcOpenMemHandle (closed at destroy)
+  void* tables = nullptr;           // device: [A 2p][B 2p][C 2p] pointers, then world signal pointers
+  uint64_t epoch = 0;
 
   uint64_t ra() const { return a1 - a0; }
   uint64_t rb() const { return b1 - b0; }
@@ -185,27 +193,130 @@ void partition(FreqRank& R, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int 
   R.t1 = R.ranges[rank].second;
 }
 
+constexpr int kMaxWorld = 64;
+
+// Byte offsets of one rank's stage buffer (the same rule on every rank, so a
+// rank can address a peer's compact slot tensors and signal slots).
+struct Layout {
+  size_t ah, bh, ac, bc, cc, nonfinite, sig, total;
+};
+Layout layout(const FreqRank& R) {
+  const size_t cx = sizeof(double2);
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  Layout L;
+  L.ah = 0;
+  L.bh = L.ah + al(2 * R.p * R.ra() * R.n * cx);
+  L.ac = L.bh + al(2 * R.p * R.rb() * R.s * cx);
+  L.bc = L.ac + al(2 * (size_t)R.ns() * R.m * R.n * cx);
+  L.cc = L.bc + al(2 * (size_t)R.ns() * R.n * R.s * cx);
+  L.nonfinite = L.cc + al(2 * (size_t)R.ns() * R.m * R.s * cx);
+  L.sig = L.nonfinite + 256;
+  L.total = L.sig + kMaxWorld * sizeof(uint64_t);
+  return L;
+}
+
 int setup(FreqRank& R, uint64_t m, uint64_t n, uint64_t s, uint64_t p, int rank, int world) {
   partition(R, m, n, s, p, rank, world);
   R.algo = qt_gemm_algo(m, n, s, p);
-  const size_t cx = sizeof(double2);
-  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t bah = al(2 * p * R.ra() * n * cx), bbh = al(2 * p * R.rb() * s * cx);
-  const size_t bac = al(2 * (size_t)R.ns() * m * n * cx), bbc = al(2 * (size_t)R.ns() * n * s * cx);
-  const size_t bcc = al(2 * (size_t)R.ns() * m * s * cx);
-  if (cudaMalloc(&R.buf, bah + bbh + bac + bbc + bcc + 256) != cudaSuccess) {
+  const Layout L = layout(R);
+  if (cudaMalloc(&R.buf, L.total) != cudaSuccess) {  // cudaMalloc: exportable through CUDA IPC
     cudaGetLastError();
     R.buf = nullptr;
     return QT_ENOMEM;
   }
   char* b = (char*)R.buf;
-  R.ah = (double2*)b;
-  R.bh = (double2*)(b + bah);
-  R.ac = (double2*)(b + bah + bbh);
-  R.bc = (double2*)(b + bah + bbh + bac);
-  R.cc = (double2*)(b + bah + bbh + bac + bbc);
-  R.nonfinite = (int*)(b + bah + bbh + bac + bbc + bcc);
-  return cudaMemset(R.nonfinite, 0, sizeof(int)) == cudaSuccess ? QT_OK : QT_ECUDA;
+  R.ah = (double2*)(b + L.ah);
+  R.bh = (double2*)(b + L.bh);
+  R.ac = (double2*)(b + L.ac);
+  R.bc = (double2*)(b + L.bc);
+  R.cc = (double2*)(b + L.cc);
+  R.nonfinite = (int*)(b + L.nonfinite);
+  R.sig = (uint64_t*)(b + L.sig);
+  return cudaMemset(b + L.nonfinite, 0, L.total - L.nonfinite) == cudaSuccess ? QT_OK : QT_ECUDA;
+}
+
+// ------------------------------------------------- fused (peer memory) exchange
+// With every rank's stage buffer mapped (CUDA IPC over NVLink), the exchange
+// needs no messages: K1 stores each frequency row of its rows of Â / B̂
+// straight into the slot owner's compact tensor (qt_qfft3_conj_f64_device_routed:
+// the last Stockham stage's store address comes from a per-(plane, frequency)
+// row table), and K3 loads its rows of every frequency of Ĉ straight from the
+// owners (qt_qifft3_conj_f64_device_routed).  The pieces land exactly where
+// the NCCL exchange puts them, so the result is bitwise the same.  A device
+// barrier (every rank release-stores an epoch into each peer's signal slot
+// for it, then acquire-spins on its own slots) orders the phases: after K1
+// (the pieces are in place) and after stage 2 (every Ĉ is complete and no rank
+// still reads the Â / B̂ the next step's K1 overwrites); the next step's first
+// barrier orders this step's K3 loads before any rank's next stage 2 rewrites
+// its Ĉ.  Only for lengths whose transform is one launch (qt_fft_routable).
+__global__ void peer_barrier_kernel(uint64_t* const* sig, int rank, int world, uint64_t epoch) {
+  const int t = threadIdx.x;
+  __threadfence_system();  // this rank's earlier peer stores before the signal
+  if (t < world) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(sig[t] + rank), "l"(epoch) : "memory");
+  if (t < world) {
+    const uint64_t* mine = sig[rank] + t;
+    uint64_t v = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    } while (v < epoch);
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+// Row tables of rank R for the peers' buffers `bases` (each peer's own layout).
+void build_tables(const FreqRank& R, const std::vector<char*>& bases, std::vector<void*>& tab) {
+  const uint64_t p = R.p;
+  tab.assign(6 * p + R.world, nullptr);
+  std::vector<Layout> Ls(R.world);
+  std::vector<FreqRank> P(R.world);
+  for (int j = 0; j < R.world; ++j) {
+    partition(P[j], R.m, R.n, R.s, R.p, j, R.world);
+    Ls[j] = layout(P[j]);
+  }
+  std::vector<int> owner(p);
+  for (int j = 0; j < R.world; ++j)
+    for (int t = R.ranges[j].first; t < R.ranges[j].second; ++t) owner[t] = j;
+  const size_t cx = sizeof(double2);
+  for (uint64_t t = 0; t < p; ++t) {
+    const uint64_t k = (uint64_t)qtb::slot_frequency((int)t, (int)p);
+    const int j = owner[t];
+    const uint64_t nsj = (uint64_t)P[j].ns(), tl = t - (uint64_t)P[j].t0;
+    for (int pl = 0; pl < 2; ++pl) {
+      tab[pl * p + k] = bases[j] + Ls[j].ac + (((pl * nsj + tl) * R.m + R.a0) * R.n) * cx;          // K1(A) stores
+      tab[2 * p + pl * p + k] = bases[j] + Ls[j].bc + (((pl * nsj + tl) * R.n + R.b0) * R.s) * cx;  // K1(B) stores
+      tab[4 * p + pl * p + k] = bases[j] + Ls[j].cc + (((pl * nsj + tl) * R.m + R.a0) * R.s) * cx;  // K3 loads
+    }
+  }
+  for (int j = 0; j < R.world; ++j) tab[6 * p + j] = bases[j] + Ls[j].sig;
+}
+
+int upload_tables(FreqRank& R, const std::vector<void*>& tab) {
+  if (!R.tables && cudaMalloc(&R.tables, tab.size() * sizeof(void*)) != cudaSuccess) return QT_ENOMEM;
+  return cudaMemcpy(R.tables, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice) == cudaSuccess
+             ? QT_OK
+             : QT_ECUDA;
+}
+
+int k1_routed(FreqRank& R, const double* a1, const double* a2, const double* b1, const double* b2, cudaStream_t st) {
+  double** T = (double**)R.tables;
+  int rc = QT_OK;
+  if (R.rb()) rc = qt_qfft3_conj_f64_device_routed(b1, b2, T + 2 * R.p, T + 3 * R.p, R.rb(), R.s, R.p, st);
+  if (!rc && R.ra()) rc = qt_qfft3_conj_f64_device_routed(a1, a2, T, T + R.p, R.ra(), R.n, R.p, st);
+  return rc;
+}
+
+int k3_routed(FreqRank& R, double* c1, double* c2, cudaStream_t st) {
+  if (!R.ra()) return QT_OK;
+  const double* const* T = (const double* const*)R.tables;
+  return qt_qifft3_conj_f64_device_routed(T + 4 * R.p, T + 5 * R.p, c1, c2, R.ra(), R.s, R.p, st);
+}
+
+int barrier(FreqRank& R, cudaStream_t st) {
+  if (R.world == 1) return QT_OK;
+  ++R.epoch;
+  peer_barrier_kernel<<<1, 64, 0, st>>>((uint64_t* const*)((void**)R.tables + 6 * R.p), R.rank, R.world, R.epoch);
+  return cudaGetLastError() == cudaSuccess ? QT_OK : QT_ECUDA;
 }
 
 int k1(FreqRank& R, const double* a1, const double* a2, const double* b1, const double* b2, cudaStream_t st) {
@@ -392,6 +503,15 @@ int qt_rank_freq_step(void* plan, const double* a1, const double* a2, const doub
   FreqRank* R = (FreqRank*)plan;
   if (!R) return QT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  if (R->fused) {  // the exchange fused into K1's stores / K3's loads over peer memory
+    int rc = k1_routed(*R, a1, a2, b1, b2, st);
+    if (!rc) rc = barrier(*R, st);
+    if (!rc) rc = stage2(*R, st);
+    if (!rc) rc = barrier(*R, st);
+    if (!rc) rc = k3_routed(*R, c1, c2, st);
+    return rc;
+  }
+  if (!R->comm && R->world > 1) return QT_EINVAL;  // an IPC plan before qt_rank_freq_set_peers
   std::vector<Piece> snd, rcv;
   int rc = k1(*R, a1, a2, b1, b2, st);
   if (!rc) {
@@ -414,6 +534,86 @@ int qt_rank_freq_step(void* plan, const double* a1, const double* a2, const doub
   return rc;
 }
 
+// A frequency-parallel plan without an NCCL communicator: its exchange goes
+// through peer memory only (qt_rank_freq_ipc_handle / qt_rank_freq_set_peers).
+int qt_rank_freq_create_ipc(int rank, int world, int device, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                            void** plan) {
+  if (!plan || world <= 0 || world > kMaxWorld || rank < 0 || rank >= world || p == 0 || p > 65534) return QT_EINVAL;
+  *plan = nullptr;
+  qtb::DeviceGuard guard;
+  if (cudaSetDevice(device) != cudaSuccess) return QT_ECUDA;
+  FreqRank* R = new FreqRank;
+  R->device = device;
+  const int rc = setup(*R, m, n, s, p, rank, world);
+  if (rc) {
+    if (R->buf) cudaFree(R->buf);
+    delete R;
+    return rc;
+  }
+  *plan = R;
+  return QT_OK;
+}
+
+int qt_rank_freq_ipc_handle(void* plan, void* out64) {
+  FreqRank* R = (FreqRank*)plan;
+  if (!R || !out64) return QT_EINVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, R->buf) != cudaSuccess) {
+    cudaGetLastError();
+    return QT_ECUDA;
+  }
+  memcpy(out64, &h, sizeof(h));
+  return QT_OK;
+}
+
+// handles: world x 64 bytes (every rank's qt_rank_freq_ipc_handle, in rank
+// order).  Maps the peers' stage buffers, builds the routed transforms' row
+// tables and switches the plan to the fused exchange (lengths whose transform
+// is one launch; others keep the NCCL exchange, or fail for an IPC plan).
+int qt_rank_freq_set_peers(void* plan, const void* handles) {
+  FreqRank* R = (FreqRank*)plan;
+  if (!R || !handles) return QT_EINVAL;
+  if (!qt_fft_routable(R->p)) return R->comm ? QT_OK : QT_EINVAL;
+  qtb::DeviceGuard guard;
+  if (cudaSetDevice(R->device) != cudaSuccess) return QT_ECUDA;
+  R->peer_buf.assign(R->world, nullptr);
+  R->peer_opened.assign(R->world, false);
+  std::vector<char*> bases(R->world);
+  for (int j = 0; j < R->world; ++j) {
+    if (j == R->rank) {
+      R->peer_buf[j] = R->buf;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, (const char*)handles + 64 * (size_t)j, sizeof(h));
+      if (cudaIpcOpenMemHandle(&R->peer_buf[j], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return QT_ECUDA;
+      }
+      R->peer_opened[j] = true;
+    }
+    bases[j] = (char*)R->peer_buf[j];
+  }
+  std::vector<void*> tab;
+  build_tables(*R, bases, tab);
+  const int rc = upload_tables(*R, tab);
+  if (!rc) R->fused = true;
+  return rc;
+}
+
+// One phase of the fused step without the device barriers, for callers that
+// order the ranks themselves (the two-process test on one GPU: no kernel may
+// wait on another process's kernel there): 0 = K1 with routed stores, 1 = stage
+// 2 of the rank's slots, 2 = K3 with routed loads.
+int qt_rank_freq_phase(void* plan, int phase, const double* a1, const double* a2, const double* b1, const double* b2,
+                       double* c1, double* c2, void* stream) {
+  FreqRank* R = (FreqRank*)plan;
+  if (!R || !R->fused || phase < 0 || phase > 2) return QT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (phase == 0) return k1_routed(*R, a1, a2, b1, b2, st);
+  if (phase == 1) return stage2(*R, st);
+  return k3_routed(*R, c1, c2, st);
+}
+
 int qt_rank_freq_nonfinite(void* plan, int* out) {
   FreqRank* R = (FreqRank*)plan;
   if (!R || !out) return QT_EINVAL;
@@ -425,6 +625,9 @@ int qt_rank_freq_destroy(void* plan) {
   if (!R) return QT_OK;
   qtb::DeviceGuard guard;
   cudaSetDevice(R->device);
+  for (size_t j = 0; j < R->peer_opened.size(); ++j)
+    if (R->peer_opened[j]) cudaIpcCloseMemHandle(R->peer_buf[j]);
+  if (R->tables) cudaFree(R->tables);
   const cudaError_t e = R->buf ? cudaFree(R->buf) : cudaSuccess;
   delete R;
   return e == cudaSuccess ? QT_OK : QT_ECUDA;
@@ -435,9 +638,10 @@ int qt_rank_freq_destroy(void* plan) {
 // schedule the NCCL exchange follows): the single-GPU check of the
 // decomposition.  a/b/c: whole device tensors (two planes each, slice-major);
 // each rank reads its rows of A and B and writes its rows of C.
-int qt_rank_freq_emulate(int world, const double* a1, const double* a2, const double* b1, const double* b2,
+int qt_rank_freq_emulate(int world, int fused, const double* a1, const double* a2, const double* b1, const double* b2,
                          double* c1, double* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p, void* stream) {
-  if (world <= 0 || p == 0 || p > 65534) return QT_EINVAL;
+  if (world <= 0 || world > kMaxWorld || p == 0 || p > 65534) return QT_EINVAL;
+  if (fused && !qt_fft_routable(p)) return QT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t cx = sizeof(double2);
   std::vector<FreqRank> R(world);
@@ -492,18 +696,30 @@ int qt_rank_freq_emulate(int world, const double* a1, const double* a2, const do
       }
     return QT_OK;
   };
+  if (fused && !rc) {  // every rank's row tables point into the other emulated ranks' buffers
+    std::vector<char*> bases(world);
+    for (int r = 0; r < world; ++r) bases[r] = (char*)R[r].buf;
+    for (int r = 0; r < world && !rc; ++r) {
+      std::vector<void*> tab;
+      build_tables(R[r], bases, tab);
+      rc = upload_tables(R[r], tab);
+    }
+  }
   for (int r = 0; r < world && !rc; ++r) {
     double2* A = (double2*)abuf[r];
     double2* B = A + 2 * p * R[r].ra() * n;
-    rc = k1(R[r], (double*)A, (double*)(A + p * R[r].ra() * n), (double*)B, (double*)(B + p * R[r].rb() * s), st);
+    const double *A1 = (double*)A, *A2 = (double*)(A + p * R[r].ra() * n);
+    const double *B1 = (double*)B, *B2 = (double*)(B + p * R[r].rb() * s);
+    rc = fused ? k1_routed(R[r], A1, A2, B1, B2, st) : k1(R[r], A1, A2, B1, B2, st);
   }
-  if (!rc) rc = route(Part::B);
-  if (!rc) rc = route(Part::A);
+  if (!rc && !fused) rc = route(Part::B);
+  if (!rc && !fused) rc = route(Part::A);
   for (int r = 0; r < world && !rc; ++r) rc = stage2(R[r], st);
-  if (!rc) rc = route(Part::C);
+  if (!rc && !fused) rc = route(Part::C);
   for (int r = 0; r < world && !rc; ++r) {
     double2* C = (double2*)cbuf[r];
-    rc = k3(R[r], (double*)C, (double*)(C + p * R[r].ra() * s), st);
+    rc = fused ? k3_routed(R[r], (double*)C, (double*)(C + p * R[r].ra() * s), st)
+               : k3(R[r], (double*)C, (double*)(C + p * R[r].ra() * s), st);
     for (int pl = 0; pl < 2 && !rc && R[r].ra(); ++pl)
       if (cudaMemcpy2DAsync((pl ? c2 : c1) + 2 * R[r].a0 * s, m * s * cx, C + pl * p * R[r].ra() * s,
                             R[r].ra() * s * cx, R[r].ra() * s * cx, p, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -511,6 +727,7 @@ int qt_rank_freq_emulate(int world, const double* a1, const double* a2, const do
   }
   cudaStreamSynchronize(st);
   for (int r = 0; r < world; ++r) {
+    if (R[r].tables) cudaFree(R[r].tables);
     if (R[r].buf) cudaFree(R[r].buf);
     if (abuf[r]) cudaFree(abuf[r]);
     if (cbuf[r]) cudaFree(cbuf[r]);

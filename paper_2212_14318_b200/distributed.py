@@ -13,7 +13,10 @@ to the others over whatever torch.distributed group the launcher set up, and
 * FreqTProduct — frequency-parallel: rank r transforms its rows of A and B,
   owns a contiguous range of frequency slots for stage 2 and its rows of C
   for the inverse transform; the pieces move by NCCL send/recv
-  (qt_rank_freq_*).  Nothing is replicated.
+  (qt_rank_freq_*), or — after set_peers() with every rank's CUDA IPC handle —
+  by K1's own stores into the owners' buffers and K3's own loads from them
+  (no messages; the library's device barrier between the phases).  Nothing
+  is replicated.
 Both are bitwise identical to the single-GPU product (tests/test_gpu_rank.py),
 and their schedules are exercised over gloo on CPU
 (tests/test_multiproc_gloo.py).
@@ -132,11 +135,22 @@ class RowsTProduct(_RankBase):
             self._stream(stream)), "qt_rank_tprod_rows")
 
 
+class IpcGroup:
+    """rank / world / device of a frequency-parallel plan whose exchange goes
+    through peer memory only (no NCCL communicator: qt_rank_freq_create_ipc)."""
+
+    def __init__(self, rank: int, world: int, device: int):
+        self.rank, self.world, self.device = rank, world, device
+        self.handle = None
+
+
 class FreqTProduct(_RankBase):
     """Frequency-parallel T-product (qt_rank_freq_*): rows [a0, a1) of A and C,
-    rows [b0, b1) of B, stage 2 of the frequency slots [slot0, slot1)."""
+    rows [b0, b1) of B, stage 2 of the frequency slots [slot0, slot1).  With a
+    RankComm the exchange is NCCL send/recv until set_peers() switches it to the
+    fused peer-memory exchange; with an IpcGroup it is fused only."""
 
-    def __init__(self, comm: RankComm, m: int, n: int, s: int, p: int, device=None):
+    def __init__(self, comm, m: int, n: int, s: int, p: int, device=None):
         super().__init__(comm, m, n, s, p, device)
         self.a0, self.a1, self.b0, self.b1, self.slot0, self.slot1 = partition(m, n, p, self.world, self.rank)
         self.rows = self.a1 - self.a0
@@ -144,8 +158,29 @@ class FreqTProduct(_RankBase):
         self.b = self._planes(self.b1 - self.b0, s)
         self.c = self._planes(self.rows, s)
         h = ctypes.c_void_p()
-        _native.check(self.L.qt_rank_freq_create(comm.handle, m, n, s, p, ctypes.byref(h)), "qt_rank_freq_create")
+        if isinstance(comm, IpcGroup):
+            _native.check(self.L.qt_rank_freq_create_ipc(comm.rank, comm.world, comm.device, m, n, s, p,
+                                                         ctypes.byref(h)), "qt_rank_freq_create_ipc")
+        else:
+            _native.check(self.L.qt_rank_freq_create(comm.handle, m, n, s, p, ctypes.byref(h)), "qt_rank_freq_create")
         self.plan = h
+
+    def ipc_handle(self) -> bytes:
+        """This rank's stage buffer as a 64-byte CUDA IPC handle."""
+        buf = ctypes.create_string_buffer(64)
+        _native.check(self.L.qt_rank_freq_ipc_handle(self.plan, buf), "qt_rank_freq_ipc_handle")
+        return bytes(buf.raw)
+
+    def set_peers(self, handles) -> None:
+        """Every rank's ipc_handle() in rank order: switch to the fused exchange."""
+        blob = ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
+        _native.check(self.L.qt_rank_freq_set_peers(self.plan, blob), "qt_rank_freq_set_peers")
+
+    def phase(self, k: int, stream=None) -> None:
+        """One fused phase without the device barriers (0 routed K1, 1 stage 2, 2 routed K3)."""
+        _native.check(self.L.qt_rank_freq_phase(
+            self.plan, k, self.a[0].data_ptr(), self.a[1].data_ptr(), self.b[0].data_ptr(), self.b[1].data_ptr(),
+            self.c[0].data_ptr(), self.c[1].data_ptr(), self._stream(stream)), "qt_rank_freq_phase")
 
     def load_a(self, a1: np.ndarray, a2: np.ndarray) -> None:
         self._load(self.a, a1, a2, self.a0, self.a1)
@@ -174,13 +209,14 @@ class FreqTProduct(_RankBase):
             self.plan = None
 
 
-def emulate_freq(world: int, a1, a2, b1, b2, c1, c2, m: int, n: int, s: int, p: int, stream=None) -> None:
+def emulate_freq(world: int, a1, a2, b1, b2, c1, c2, m: int, n: int, s: int, p: int, stream=None,
+                 fused: bool = False) -> None:
     """`world` frequency-parallel ranks in lockstep on the current device
     (qt_rank_freq_emulate: the pieces moved by device copies along the same
     schedule): whole device tensors in, C out — the one-GPU check of the
     decomposition."""
     import torch
     sh = (torch.cuda.current_stream() if stream is None else stream).cuda_stream
-    _native.check(_native.lib().qt_rank_freq_emulate(world, a1.data_ptr(), a2.data_ptr(), b1.data_ptr(),
+    _native.check(_native.lib().qt_rank_freq_emulate(world, int(fused), a1.data_ptr(), a2.data_ptr(), b1.data_ptr(),
                                                      b2.data_ptr(), c1.data_ptr(), c2.data_ptr(), m, n, s, p, sh),
                   "qt_rank_freq_emulate")
