@@ -23,6 +23,13 @@ inline bool fill_workspace() {
   return env && *env == '1';
 }
 
+// $QTB_DROPIN_NAIVE=gpu: tprod_naive (the definitional oracle) on the B200;
+// default: the reference's own CPU definition (an independent checker)
+inline bool naive_on_gpu() {
+  const char* env = std::getenv("QTB_DROPIN_NAIVE");
+  return env && std::string(env) == "gpu";
+}
+
 // QT_EINVAL -> std::invalid_argument (what the reference throws), anything else
 // -> std::runtime_error.  There is no CPU fallback: a missing GPU is an error.
 inline void check(int rc, const char* who) {
