@@ -572,7 +572,7 @@ int qt_rank_freq_ipc_handle(void* plan, void* out64) {
 // is one launch; others keep the NCCL exchange, or fail for an IPC plan).
 int qt_rank_freq_set_peers(void* plan, const void* handles) {
   FreqRank* R = (FreqRank*)plan;
-  if (!R || !handles) return QT_EINVAL;
+  if (!R || !handles || R->world > kMaxWorld) return QT_EINVAL;  // (kMaxWorld signal slots per rank)
   if (!qt_fft_routable(R->p)) return R->comm ? QT_OK : QT_EINVAL;
   qtb::DeviceGuard guard;
   if (cudaSetDevice(R->device) != cudaSuccess) return QT_ECUDA;
