@@ -467,3 +467,37 @@ def test_int8_guard_forced_fallback_is_the_dmma_product():
     out = _guard_run({"QTB_OZAKI_GUARD": "force"})
     assert out["forced_bitwise_dmma"] is True
     assert out["plain"]["fallbacks"] > 0 and out["plain"]["err"] <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["col1e8", "one_elem"])
+def test_int8_guard_host_streaming_and_freq_parallel(case):
+    """Badly scaled inputs through the other int8 drivers: the host C-ABI path
+    that streams A in row slabs against resident B' (each slab's pairs
+    certified on their own) against the GPU definitional product, and the
+    frequency-parallel split (4 ranks emulated; each slot certified by its
+    owner over all rows) bitwise against the one-GPU product."""
+    import importlib.util
+    import os
+    import torch
+    from paper_2212_14318_b200 import distributed
+    spec = importlib.util.spec_from_file_location(
+        "guard_check", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                                    "guard_check.py"))
+    gc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gc)
+    m, n, s, p = 512, 512, 256, 16  # >= 128 MB: the host call streams row slabs
+    assert _native.lib().qt_gemm_algo(m, n, s, p) == INT8
+    a, b = gc.scaled_inputs(case, m, n, s, p, seed=9)
+    c = qt.tprod_fast(a, b)
+    naive = qt.tprod_naive(a, b)
+    assert O.rel_frob_error((c.t1, c.t2), (naive.t1, naive.t2)) <= 1e-12
+    m2 = 96
+    a2 = qt.CdTensor3(m2, n, p, np.ascontiguousarray(a.t1[:, :m2]), np.ascontiguousarray(a.t2[:, :m2]))
+    want = qt.tprod_fast(a2, b)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.float64)).cuda()
+    c1 = torch.empty((p, m2, 2 * s), dtype=torch.float64, device="cuda")
+    c2 = torch.empty_like(c1)
+    distributed.emulate_freq(4, dev(a2.t1), dev(a2.t2), dev(b.t1), dev(b.t2), c1, c2, m2, n, s, p)
+    torch.cuda.synchronize()
+    assert bits_equal(c1.cpu().numpy().view(np.complex128), want.t1)
+    assert bits_equal(c2.cpu().numpy().view(np.complex128), want.t2)
