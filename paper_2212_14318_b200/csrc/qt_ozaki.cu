@@ -831,10 +831,46 @@ __global__ void __launch_bounds__(256) oz_colexp_b_kernel(const double2* __restr
   int E = kNoExp;
   double ss = 0.0, l1 = 0.0;
   bool bad = false;
+  constexpr int kU = 8;  // loads in flight per thread
+  const double2* base1 = b1 + k * bslice + c;
+  const double2* base2 = b2 + k * bslice + c;
+  // fast path: plain sums of the balanced values (one exact power-of-two
+  // multiply per element), rescaled once at the end.  That equals the running-
+  // exponent pass below bitwise whenever nothing is subnormal or overflows —
+  // guaranteed here when the column segment's largest value lies in
+  // [2^-400, 2^400] and every d in [-1000, 1000]; otherwise (and for inf / nan)
+  // the segment is recomputed by that pass.
+  bool slow = c >= s;
   if (c < s) {
-    const double2* base1 = b1 + k * bslice + c;
-    const double2* base2 = b2 + k * bslice + c;
-    constexpr int kU = 8;  // loads in flight per thread
+    double mxf = 0.0, ssf = 0.0, l1f = 0.0;
+    for (int jb = j0 + w; jb < jend; jb += 8 * kU) {
+      double2 y[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = jb + 8 * u;
+        y[u] = j < jend ? __ldcs(j < n ? base1 + (size_t)j * ldb : base2 + (size_t)(j - n) * ldb)
+                        : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = jb + 8 * u;
+        const int d = bal_delta(bdel, kf, n, j < n ? j : j - n);
+        slow |= (d < -1000) | (d > 1000);
+        const double sc = __longlong_as_double((long long)(d + 1023) << 52);
+        const double a = y[u].x * sc, b = y[u].y * sc, aa = fabs(a), bb = fabs(b);
+        mxf = fmax(mxf, fmax(aa, bb));
+        ssf = fma(a, a, fma(b, b, ssf));
+        l1f += aa + bb;
+      }
+    }
+    if (!(l1f <= kDblMax) || (mxf != 0.0 && (mxf > 0x1p400 || mxf < 0x1p-400))) slow = true;
+    if (!slow && mxf != 0.0) {
+      E = exp_bits(mxf);
+      ss = scale2(ssf, -2 * E);
+      l1 = scale2(l1f, -E);
+    }
+  }
+  if (c < s && slow) {
     for (int jb = j0 + w; jb < jend; jb += 8 * kU) {
       double2 y[kU];
 #pragma unroll
