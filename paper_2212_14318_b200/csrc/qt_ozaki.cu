@@ -527,6 +527,16 @@ __device__ __forceinline__ uint32_t neg_res(uint32_t r, uint32_t p) { return r ?
 // for p = 256 the packed low byte of 256 - r is -r mod 256.  One operation.
 __device__ __forceinline__ uint32_t neg_op(uint32_t r, uint32_t p) { return p - r; }
 
+__device__ __forceinline__ double block_max_dbl(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+  return v;
+}
 __device__ __forceinline__ int block_max_int(int v, int* red) {
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -688,39 +698,70 @@ __global__ void __launch_bounds__(256, 4) oz_residue_a_kernel(const double2* __r
   const int kq = slot_slice(slot, p, cbase), skq = slot_slice((k == sk) ? slot : (slot ^ 1), p, cbase);
   const double2* P = a1 + ((size_t)kq * m + i) * n;
   const double2* Qr = a2 + ((size_t)skq * m + i) * n;
-  // column j of this row pair multiplies Y rows j and n + j: balanced by 2^-d_j
-  int E = kNoExp;
-  bool bad = false;
+  // column j of this row pair multiplies Y rows j and n + j: balanced by 2^-d_j.
+  // Fast path: one pass of plain max / sum of squares / L1 sums of the
+  // balanced values (one exact power-of-two multiply each), rescaled once —
+  // bitwise the exponent-tracking passes below whenever nothing is subnormal
+  // or overflows (row maximum in [2^-400, 2^400], every |d| <= 1000).
+  bool bad = false, slow = false;
+  double mxf = 0.0, ssf = 0.0, l1f = 0.0;
 #pragma unroll 4
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const double2 x = P[j], y = Qr[j];
-    const double mx = fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y)));
     bad |= !(fabs(x.x) + fabs(x.y) + fabs(y.x) + fabs(y.y) <= kDblMax);
-    if (mx != 0.0 && mx <= kDblMax) E = max(E, exp_bits(mx) - (dk ? __ldg(dk + j) : 0));
+    const int dj = dk ? __ldg(dk + j) : 0;
+    slow |= (dj < -1000) | (dj > 1000);
+    const double sc = __longlong_as_double((long long)(1023 - dj) << 52);
+    const double a = x.x * sc, b = x.y * sc, c = y.x * sc, d = y.y * sc;
+    mxf = fmax(mxf, fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(d))));
+    ssf = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ssf))));
+    l1f += (fabs(a) + fabs(b)) + (fabs(c) + fabs(d));
   }
   bad = __syncthreads_or(bad);
-  E = block_max_int(E, ired);
   if (bad) {
     if (threadIdx.x == 0) atomicExch(nonfinite, 1);
     return;
   }
+  slow = __syncthreads_or(slow);
+  mxf = block_max_dbl(mxf, red);
+  ssf = block_sum(ssf, red);
+  l1f = block_sum(l1f, red);
+  slow = slow || !(l1f <= kDblMax) || (mxf != 0.0 && (mxf > 0x1p400 || mxf < 0x1p-400));
+  int E = kNoExp;
   int e = 0;
   double l1s = 0.0;  // L1 norm of the scaled (unrounded) real-form row
-  if (E != kNoExp) {
-    double ss = 0.0;  // sum of squares of the balanced row scaled by 2^-E (each term <= 1)
-    double l1 = 0.0;
+  if (!slow) {
+    if (mxf != 0.0) {
+      E = exp_bits(mxf);
+      const double ss = scale2(ssf, -2 * E);
+      e = scale_exponent(E, sqrt(ss));
+      l1s = scale2(scale2(l1f, -E) * (1.0 + 0x1p-40), E + e);
+    }
+  } else {
+    // exponent-tracking passes (any magnitudes)
 #pragma unroll 4
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const double2 x = P[j], y = Qr[j];
-      const int sh = -(dk ? __ldg(dk + j) : 0) - E;
-      const double a = scale2(x.x, sh), b = scale2(x.y, sh), c = scale2(y.x, sh), d = scale2(y.y, sh);
-      ss = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ss))));
-      l1 += (fabs(a) + fabs(b)) + (fabs(c) + fabs(d));
+      const double mx = fmax(fmax(fabs(x.x), fabs(x.y)), fmax(fabs(y.x), fabs(y.y)));
+      if (mx != 0.0) E = max(E, exp_bits(mx) - (dk ? __ldg(dk + j) : 0));
     }
-    ss = block_sum(ss, red);
-    l1 = block_sum(l1, red);
-    e = scale_exponent(E, sqrt(ss));
-    l1s = scale2(l1 * (1.0 + 0x1p-40), E + e);
+    E = block_max_int(E, ired);
+    if (E != kNoExp) {
+      double ss = 0.0;  // sum of squares of the balanced row scaled by 2^-E (each term <= 1)
+      double l1 = 0.0;
+#pragma unroll 4
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double2 x = P[j], y = Qr[j];
+        const int sh = -(dk ? __ldg(dk + j) : 0) - E;
+        const double a = scale2(x.x, sh), b = scale2(x.y, sh), c = scale2(y.x, sh), d = scale2(y.y, sh);
+        ss = fma(a, a, fma(b, b, fma(c, c, fma(d, d, ss))));
+        l1 += (fabs(a) + fabs(b)) + (fabs(c) + fabs(d));
+      }
+      ss = block_sum(ss, red);
+      l1 = block_sum(l1, red);
+      e = scale_exponent(E, sqrt(ss));
+      l1s = scale2(l1 * (1.0 + 0x1p-40), E + e);
+    }
   }
   if (threadIdx.x == 0) {
     eA[f * Mp + i] = e;
