@@ -1450,6 +1450,22 @@ residues:
   return cudaGetLastError();
 }
 
+struct AuxObjects {
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+};
+AuxObjects& aux_objects(int device) {
+  thread_local AuxObjects objs[64];
+  static AuxObjects none;
+  if (device < 0 || device >= 64) return none;
+  AuxObjects& o = objs[device];
+  if (!o.stream && cudaStreamCreateWithFlags(&o.stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    o.stream = nullptr;
+  }
+  return o;
+}
+
 // GEMM and CRT for the frequency slots of B (all p, or B's compact range)
 // against B' (B.all: slot f of B' is frequency slot f; else B' is rebuilt per
 // batch), with X' built per batch from Â; then the guard decision per pair.
@@ -1510,22 +1526,28 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
   // of B̂ that would crawl beside the GEMM), the B' residues then batch by
   // batch; before the fork below, so the aux stream's batches see them
   if (e == cudaSuccess && lazyB) e = prep_b(B, B.bh1, B.bh2, (uint64_t)B.s0, (int)ps, 0, flag, stream, kPrepExp);
-  cudaStream_t aux = stream;
-  std::vector<cudaEvent_t> evs;
+  // the second stream and the ordering events are per-thread, per-device
+  // objects reused by every call (creating and destroying them per call cost
+  // more than a mid-size product's batches); re-recording an event is safe:
+  // a stream wait captures the event's state when it is enqueued
+  int dev = 0;
+  cudaGetDevice(&dev);
+  AuxObjects& ao = aux_objects(dev);
+  size_t nev = 0;
   auto mkev = [&]() {
-    cudaEvent_t ev = nullptr;
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) evs.push_back(ev);
-    return ev;
-  };
-  if (e == cudaSuccess && pipe && nbatch > 1) {
-    e = cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
-    if (e == cudaSuccess) {
-      cudaEvent_t fork = mkev();
-      cudaEventRecord(fork, stream);
-      cudaStreamWaitEvent(aux, fork, 0);
-    } else {
-      aux = stream;
+    if (nev == ao.events.size()) {
+      cudaEvent_t ev = nullptr;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return (cudaEvent_t) nullptr;
+      ao.events.push_back(ev);
     }
+    return ao.events[nev++];
+  };
+  cudaStream_t aux = stream;
+  if (e == cudaSuccess && pipe && nbatch > 1 && ao.stream) {
+    aux = ao.stream;
+    cudaEvent_t fork = mkev();
+    cudaEventRecord(fork, stream);
+    cudaStreamWaitEvent(aux, fork, 0);
   }
   auto batch = [&](uint64_t i, uint64_t& f0, int& fcur) {
     f0 = B.s0 + i * F;
@@ -1637,8 +1659,7 @@ cudaError_t multiply(OzakiB& B, const double2* ah1, const double2* ah2, const do
   }
   if (e == cudaSuccess && lazyB) B.ready = true;
   const cudaError_t fe = cudaFreeAsync(ws, stream);
-  if (aux != stream) cudaStreamDestroy(aux);
-  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+
   return e != cudaSuccess ? e : fe;
 }
 
