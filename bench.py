@@ -576,6 +576,8 @@ def run_ours(args, cfg):
                 "peak_source": "measured tcgen05 kind::i8 throughput, sustained (back-to-back 4 s under the "
                                "power cap, 1612 MHz): profiles/r02/peaks.json (tools/microbench/int8_peak.cu)",
                 "peak_burst": peak_i8_burst, "frac_of_burst": ach / peak_i8_burst,
+                "frac_of_2x_measured_bf16_sustained": (ach / (2.0 * peaks["bf16_tflops_sustained"])
+                                                       if "bf16_tflops_sustained" in peaks else None),
                 "algorithmic": "2 * 15 moduli * (2m)(4n)(2s) * p int8 ops per step (= 480 m n s p), "
                                "launched in frequency batches",
                 "algorithm": "exact Ozaki-II: 53-bit scaled integers (norm-bounded), 15 coprime moduli <= 256, CRT (csrc/qt_ozaki.cu)",
