@@ -8,13 +8,13 @@ PKG       := paper_2212_14318_b200
 CSRC      := $(PKG)/csrc
 LIB       := $(PKG)/libqtensor_b200.so
 OBJDIR    := build/obj
-SRCS_CU   := $(CSRC)/qt_fft.cu $(CSRC)/qt_gemm.cu $(CSRC)/qt_ozaki.cu $(CSRC)/qt_naive.cu $(CSRC)/qt_io.cu $(CSRC)/qt_api.cu $(CSRC)/qt_multi.cu $(CSRC)/qt_nccl.cu $(CSRC)/qt_rank.cu
+SRCS_CU   := $(CSRC)/qt_fft.cu $(CSRC)/qt_gemm.cu $(CSRC)/qt_ozaki.cu $(CSRC)/qt_naive.cu $(CSRC)/qt_io.cu $(CSRC)/qt_api.cu $(CSRC)/qt_multi.cu $(CSRC)/qt_nccl.cu $(CSRC)/qt_rank.cu $(CSRC)/qt_small.cu
 SRCS_CPP  := $(CSRC)/qt_rng.cpp
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS_CU)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(SRCS_CPP))
 
 all: $(LIB) oracle
 
-$(OBJDIR)/%.o: $(CSRC)/%.cu $(CSRC)/qt_internal.cuh $(CSRC)/qt_dmma_tile.cuh $(CSRC)/qt_nccl.h include/qtensor_b200.h
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(CSRC)/qt_internal.cuh $(CSRC)/qt_dmma_tile.cuh $(CSRC)/qt_fft_reg.cuh $(CSRC)/qt_nccl.h include/qtensor_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.txt || (cat $(OBJDIR)/$*.ptxas.txt; false)
 

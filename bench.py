@@ -518,7 +518,7 @@ def run_ours(args, cfg):
     def read_prof(steps_done=None):
         steps_done = steps_done or nprof
         out = {}
-        for tag in ("fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_residues_b", "k2_int8_colnorms",
+        for tag in ("small_fused", "fft", "k2_dmma", "k2_int8_gemm", "k2_int8_residues", "k2_int8_residues_b", "k2_int8_colnorms",
                     "k2_int8_crt"):
             t_ms, n_l = ctypes.c_double(0.0), ctypes.c_uint64(0)
             qt._native.check(L.qt_prof_read(tag.encode(), ctypes.byref(t_ms), ctypes.byref(n_l)), "qt_prof_read")
@@ -595,6 +595,25 @@ def run_ours(args, cfg):
                                 "note": "same kernel, batches in order (QTB_OZAKI_PIPE=0), nothing co-running"}
         traffic, traffic_src = ncu_traffic(cfg, "K2_int8_gemm", rows if k2_shape is None else -1)
         roof["algorithmic_bytes"] = None
+    elif "small_fused" in prof:
+        # the whole product is ONE cluster kernel (csrc/qt_small.cu): A and B
+        # read once, C written once, K1 -> K2 -> K3 exchanged through DSMEM
+        k_ms = prof["small_fused"]["ms_per_step"]
+        fused_bytes = cfg.bytes_tensor(rows, cfg.n) + cfg.bytes_tensor(cfg.n, cols) + cfg.bytes_tensor(rows, cols)
+        gb = fused_bytes / (k_ms * 1e-3) / 1e9
+        roof = {"kernel": "one-launch small product small_tprod_kernel (K1 + K2 + K3 in one thread-block-cluster "
+                          "kernel, DSMEM exchanges, DMMA.8x8x4 stage 2)",
+                "bound": "hbm", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"],
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                "algorithmic": "32*(mn+ns+ms)*p bytes per launch (A and B read once, C written once)",
+                "algorithm": algo_txt, "kernel_ms": k_ms, "share_of_step": k_ms / ms,
+                "latency_floor": "an EMPTY kernel timed the same way (after the 256 MB L2 flush, events on the "
+                                 "stream) takes 6.1 us and a CUDA graph of three 1 MB copies 10.2 us on this "
+                                 "B200 (tools/microbench/launch_probe.cu, profiles/r02/launch_probe.txt): the "
+                                 "product is latency-bound, not HBM-bound",
+                "traffic": None}
+        traffic, traffic_src = None, None
+        roof["algorithmic_bytes"] = fused_bytes
     elif gemm_ai >= ridge:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
         ktf = 32.0 * krows * cfg.n * kcols * kp / (k_ms * 1e-3) / 1e12

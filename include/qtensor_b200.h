@@ -167,6 +167,13 @@ int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
 #define QT_GEMM_DMMA 0
 #define QT_GEMM_INT8_EXACT 1
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p);
+/* 1 if qt_tprod_f64_device runs a product of this shape as ONE launch (the
+ * cluster kernel of csrc/qt_small.cu: K1, K2 and K3 exchanging through
+ * distributed shared memory; p in {4, 8, 16}, m, s <= 32, n <= 64, fp64 DMMA
+ * stage 2; $QTB_SMALL=0 turns it off), else 0 (three or more launches).  The
+ * result is bitwise the same either way.  Same role as qt_gemm_algo: an
+ * introspection entry with no reference counterpart. */
+int qt_small_fused(uint64_t m, uint64_t n, uint64_t s, uint64_t p);
 int qt_spectral_product_f64_device_ld_algo(const double* ahat1, const double* ahat2,
                                            const double* bhat1, const double* bhat2,
                                            double* chat1, double* chat2,

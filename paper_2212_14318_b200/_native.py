@@ -40,6 +40,7 @@ SIGNATURES = {
     "qt_spectral_product_f64_device_ld": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [_vp]),
     "qt_spectral_product_f64_device_ld_algo": (ctypes.c_int, [_dp] * 6 + [_u64] * 8 + [ctypes.c_int, _vp]),
     "qt_gemm_algo": (ctypes.c_int, [_u64] * 4),
+    "qt_small_fused": (ctypes.c_int, [_u64] * 4),
     "qt_int8_guard_fallbacks": (_u64, []),
     "qt_slot_frequency": (ctypes.c_int, [_u64, _u64]),
     "qt_int8_slots_create": (ctypes.c_int, [_dp, _dp] + [_u64] * 3 + [ctypes.c_int, ctypes.c_int, _vp, _vp,

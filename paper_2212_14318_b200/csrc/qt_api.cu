@@ -130,6 +130,12 @@ int tprod_device_impl(const double* a1, const double* a2, const double* b1, cons
     if ((e = cudaMemsetAsync(c2, 0, cbytes, st)) != cudaSuccess) return cuda_fail(e, "memset");
     return QT_OK;
   }
+  if (small_fused_eligible(m, n, s, p)) {  // one launch: K1, K2, K3 in one cluster kernel (qt_small.cu)
+    if ((e = launch_small_tprod((const double2*)a1, (const double2*)a2, (const double2*)b1, (const double2*)b2,
+                                (double2*)c1, (double2*)c2, m, n, s, p, st, dev)) != cudaSuccess)
+      return cuda_fail(e, "one-launch small T-product");
+    return QT_OK;
+  }
   const uint64_t an = m * n * p, bn = n * s * p;  // complex counts per plane
   double2* ws = nullptr;
   if ((e = cudaMallocAsync(&ws, (2 * an + 2 * bn) * sizeof(double2), st)) != cudaSuccess)
@@ -1049,6 +1055,10 @@ int qt_int8_slots_destroy(void* handle, void* stream) {
 }
 
 uint64_t qt_int8_guard_fallbacks(void) { return int8_guard_fallbacks(); }
+
+int qt_small_fused(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
+  return small_fused_eligible(m, n, s, p) ? 1 : 0;
+}
 
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
   (void)m;

@@ -485,6 +485,10 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
 
 }  // namespace
 
+// the complex-product algorithm every DMMA tile uses (the one-launch small
+// product, qt_small.cu, must evaluate the same one)
+bool dmma_gauss() { return gauss_enabled(); }
+
 // DMMA (fp64 tensor-core) paired product; with an int8 flag array in only_if
 // a CTA runs only for the pairs the int8 path did not certify (qt_ozaki.cu).
 static cudaError_t dmma_impl(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,

@@ -182,6 +182,12 @@ cudaError_t dmma_spectral_gemm_slots(const double2* ah1, const double2* ah2, con
 
 // $QTB_DEBUG_NO_REFLECT=1: sigma(k) = k in stage 2 (the parity tests' negative control)
 bool debug_noreflect();
+bool dmma_gauss();
+// One-launch T-product for small products (qt_small.cu): eligibility and launch.
+bool small_fused_eligible(uint64_t m, uint64_t n, uint64_t s, uint64_t p);
+cudaError_t launch_small_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,
+                               double2* c1, double2* c2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                               cudaStream_t stream, int device);
 
 // Definitional product C_k = sum_r A_{(k-r) mod p} (.) B_r (qt_naive.cu).
 cudaError_t launch_naive_tprod(const double2* a1, const double2* a2, const double2* b1, const double2* b2,
