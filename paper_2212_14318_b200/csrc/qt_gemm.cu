@@ -483,6 +483,229 @@ cudaError_t launch_small_persistent(const double2* ah1, const double2* ah2, cons
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised persistent variant for tiny slices that are whole tiles
+// (m, s <= 16, n <= 16, contiguous slices: e.g. config 3, 16 x 16 x 16 with
+// p = 4096 -> 2049 pair products of 32 KB operands each).  The cp.async ring
+// of paired_small_persistent_kernel keeps one item in flight per CTA and all
+// 128 threads issue its 2048 16-byte copies; here ONE producer warp streams
+// each item's eight operand slices (four of Â, four of B̂, each one contiguous
+// m*n or n*s block) with bulk copies (cp.async.bulk, mbarrier complete_tx)
+// into a kTinyStages-deep ring, and three groups of four consumer warps take
+// turns on the items, so several items' loads are in flight while up to three
+// are on the DMMA pipe.  Operands sit in shared memory unswizzled (each slice
+// as it is in HBM; padded rows through per-row copies were measured 2.6x
+// slower: 128 small bulk copies per item starve the consumers); out-of-range
+// rows / K / columns read +0, as the zero-filled cp.async tiles.  Every accumulator gets exactly mma_stage_3m's DMMA sequence (sets
+// 0-11, K-steps of 4 over the 16-wide K tile), and the epilogue is
+// store_tile_3m's, so results are bitwise those of the other kernels.
+constexpr int kTinyStages = 6;
+constexpr int kTinySlice = 256;                    // double2 per operand slice (16 x 16 max)
+constexpr int kTinyItem = 8 * kTinySlice;          // 32 KB per item
+constexpr int kTinyGroups = 3;
+constexpr int kTinyConsumers = 4 * kTinyGroups;    // warps 0-11: three groups of four
+constexpr int kTinyThreads = 32 * (kTinyConsumers + 1);  // + warp 8: producer
+constexpr size_t kTinySmem = (size_t)kTinyStages * kTinyItem * sizeof(double2);
+
+__device__ __forceinline__ void tiny_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tiny_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tiny_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tiny_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tiny_bulk_load(double2* dst, const double2* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTinyThreads, 1)
+    paired_tiny_ws_kernel(const double2* __restrict__ ah1, const double2* __restrict__ ah2,
+                          const double2* __restrict__ bh1, const double2* __restrict__ bh2, double2* __restrict__ ch1,
+                          double2* __restrict__ ch2, int m, int n, int s, int p, const int* only_if, PairMap map,
+                          int units) {
+  extern __shared__ double2 smem[];
+  __shared__ __align__(8) uint64_t full[kTinyStages], empty[kTinyStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t amn = (size_t)m * n, bns = (size_t)n * s, cms = (size_t)m * s;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTinyStages; ++st) {
+      tiny_mbar_init(&full[st], 1);
+      tiny_mbar_init(&empty[st], 4);  // the four warps of the consuming group
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  if (warp == kTinyConsumers) {  // ---- producer
+    if (lane == 0) {
+      const uint32_t abytes = (uint32_t)(amn * 16), bbytes = (uint32_t)(bns * 16);
+      for (int i = 0;; ++i) {
+        const int w = blockIdx.x + i * G;
+        if (w >= units) break;
+        const int st = i % kTinyStages;
+        tiny_mbar_wait(&empty[st], ((i / kTinyStages) & 1) ^ 1);
+        int ka, kb, key;
+        map_unit(w, map, p, ka, kb, key);
+        if (skip_unit(only_if, key)) {  // nothing to load: complete the phase empty
+          tiny_mbar_expect_tx(&full[st], 0);
+          continue;
+        }
+        tiny_mbar_expect_tx(&full[st], 4 * abytes + 4 * bbytes);
+        double2* d = smem + (size_t)st * kTinyItem;
+        // A1_k, A2_k, A1_s, A2_s | B1_k, B2_k, B1_s, B2_s  (qt_dmma_tile.cuh PairArgs order)
+        tiny_bulk_load(d + 0 * kTinySlice, ah1 + ka * amn, abytes, &full[st]);
+        tiny_bulk_load(d + 1 * kTinySlice, ah2 + ka * amn, abytes, &full[st]);
+        tiny_bulk_load(d + 2 * kTinySlice, ah1 + kb * amn, abytes, &full[st]);
+        tiny_bulk_load(d + 3 * kTinySlice, ah2 + kb * amn, abytes, &full[st]);
+        tiny_bulk_load(d + 4 * kTinySlice, bh1 + ka * bns, bbytes, &full[st]);
+        tiny_bulk_load(d + 5 * kTinySlice, bh2 + ka * bns, bbytes, &full[st]);
+        tiny_bulk_load(d + 6 * kTinySlice, bh1 + kb * bns, bbytes, &full[st]);
+        tiny_bulk_load(d + 7 * kTinySlice, bh2 + kb * bns, bbytes, &full[st]);
+      }
+    }
+    return;
+  }
+  // ---- consumers: group gr takes the CTA's items gr, gr + 2, ...
+  const int gr = warp >> 2, wq = warp & 3;
+  const int wm = wq & 1, wn = wq >> 1;  // the warp's 8 x 8 block of the 16 x 16 tile
+  const int g = lane >> 2, q = lane & 3;
+  const int i_row = wm * 8 + g, j_col = wn * 8 + g;
+  for (int i = gr;; i += kTinyGroups) {
+    const int w = blockIdx.x + i * G;
+    if (w >= units) break;
+    const int st = i % kTinyStages;
+    tiny_mbar_wait(&full[st], (i / kTinyStages) & 1);
+    int ka, kb, key;
+    map_unit(w, map, p, ka, kb, key);
+    if (!skip_unit(only_if, key)) {
+      const double2* sa = smem + (size_t)st * kTinyItem;
+      const double2* sb = sa + 4 * kTinySlice;
+      double T[12][2];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) T[c][0] = T[c][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {  // K tile of 16 (SmallGaussCfg::BK), zero-padded beyond n
+        const int k = ks * 4 + q;
+        double br[4], bi[4], bp[4];
+        const bool bok = k < n && j_col < s;
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) {
+          const double2 v = bok ? sb[pl * kTinySlice + k * s + j_col] : make_double2(0.0, 0.0);
+          br[pl] = v.x;
+          bi[pl] = v.y;
+          bp[pl] = v.x + v.y;
+        }
+        const double nb2k_r = dneg(br[1]), nb2k_i = dneg(bi[1]), nb2k_p = dneg(bp[1]);
+        const bool aok = k < n && i_row < m;
+        double ar[4], ai[4], ap[4], am[4];
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) {
+          const double2 v = aok ? sa[pl * kTinySlice + i_row * n + k] : make_double2(0.0, 0.0);
+          ar[pl] = v.x;
+          ai[pl] = v.y;
+          ap[pl] = v.x + v.y;
+          am[pl] = v.x - v.y;
+        }
+        // mma_stage_3m's sequence (non-SELF; a self-paired unit has sigma k = k)
+        dmma(T[0], ar[0], br[0]);
+        dmma(T[1], ai[0], bi[0]);
+        dmma(T[2], ap[0], bp[0]);
+        dmma(T[3], ar[2], br[1]);
+        dmma(T[4], ai[2], nb2k_i);
+        dmma(T[5], am[2], bp[1]);
+        dmma(T[6], ar[2], br[2]);
+        dmma(T[7], ai[2], bi[2]);
+        dmma(T[8], ap[2], bp[2]);
+        dmma(T[9], ar[0], br[3]);
+        dmma(T[10], ai[0], dneg(bi[3]));
+        dmma(T[11], am[0], bp[3]);
+        dmma(T[0], ar[3], nb2k_r);
+        dmma(T[1], ai[3], bi[1]);
+        dmma(T[2], am[3], nb2k_p);
+        dmma(T[3], ar[1], br[0]);
+        dmma(T[4], ai[1], bi[0]);
+        dmma(T[5], ap[1], bp[0]);
+        dmma(T[6], ar[1], dneg(br[3]));
+        dmma(T[7], ai[1], bi[3]);
+        dmma(T[8], am[1], dneg(bp[3]));
+        dmma(T[9], ar[3], br[2]);
+        dmma(T[10], ai[3], bi[2]);
+        dmma(T[11], ap[3], bp[2]);
+      }
+      // operands consumed: hand the stage back before the (global) stores
+      __syncwarp();
+      if (lane == 0) tiny_mbar_arrive(&empty[st]);
+      double2* cp[4] = {ch1 + ka * cms, ch2 + ka * cms, ch1 + kb * cms, ch2 + kb * cms};
+      const int row = i_row, col = wn * 8 + 2 * q;
+      if (row < m) {
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          double2* dst = cp[o] + (size_t)row * s + col;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double t1 = T[3 * o][e], t2 = T[3 * o + 1][e], t3 = T[3 * o + 2][e];
+            if (col + e < s) dst[e] = make_double2(t1 - t2, t3 - t1 - t2);
+          }
+        }
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) tiny_mbar_arrive(&empty[st]);
+    }
+  }
+}
+
+bool tiny_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("QTB_TINY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+cudaError_t launch_tiny_ws(const double2* ah1, const double2* ah2, const double2* bh1, const double2* bh2,
+                           double2* ch1, double2* ch2, uint64_t m, uint64_t n, uint64_t s, uint64_t p,
+                           cudaStream_t stream, const int* only_if, PairMap map) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  static int sms = 148;
+  const cudaError_t attr_err = once_per_device(mu, done, [&] {
+    cudaError_t e = cudaFuncSetAttribute(paired_tiny_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kTinySmem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return e;
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const uint64_t units = map.noreflect ? p : map.s0 < 0 ? p / 2 + 1 : (uint64_t)slot_units(map.s0, map.ns, (int)p);
+  if (units == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<uint64_t>(units, (uint64_t)sms);
+  ProfScope ps(only_if ? "k2_dmma_guard" : "k2_dmma", stream);
+  paired_tiny_ws_kernel<<<grid, kTinyThreads, kTinySmem, stream>>>(ah1, ah2, bh1, bh2, ch1, ch2, (int)m, (int)n,
+                                                                   (int)s, (int)p, only_if, map, (int)units);
+  ps.stop();
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 // the complex-product algorithm every DMMA tile uses (the one-launch small
@@ -499,6 +722,10 @@ static cudaError_t dmma_impl(const double2* ah1, const double2* ah2, const doubl
   // and its two-deep K pipeline would be all latency; use the 16 x 16 tile.
   const bool gauss = gauss_enabled();
   if (m <= 32 && s <= 32) {
+    // whole-slice tiles with contiguous slices: the warp-specialised ring
+    if (gauss && tiny_enabled() && m <= 16 && s <= 16 && n <= 16 && ldb == s && ldc == s && bslice == n * s &&
+        cslice == m * s)
+      return launch_tiny_ws(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, stream, only_if, map);
     if (n <= (uint64_t)SmallCfg::BK)
       return gauss ? launch_small_persistent<SmallGaussCfg>(ah1, ah2, bh1, bh2, ch1, ch2, m, n, s, p, ldb, ldc,
                                                             bslice, cslice, stream, only_if, map)

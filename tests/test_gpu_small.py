@@ -118,3 +118,55 @@ def test_device_entry_replay_and_row_slabs():
         sa = qt.CdTensor3(hi - lo, n, p, np.ascontiguousarray(a.t1[:, lo:hi]), np.ascontiguousarray(a.t2[:, lo:hi]))
         c = qt.tprod_fast(sa, b)
         assert np.array_equal(bits(c.t1), bits(want.t1[:, lo:hi])) and np.array_equal(bits(c.t2), bits(want.t2[:, lo:hi]))
+
+
+# ------------------------------------------------------------------------------
+# The warp-specialised stage-2 kernel for whole-slice tiles (qt_gemm.cu
+# paired_tiny_ws_kernel: m, s <= 16, n <= 16; config 3): bitwise the
+# cp.async-ring kernel's result ($QTB_TINY=0), which the parity tests pin to
+# the reference.
+TINY_SHAPES = [(16, 16, 16, 4096), (16, 16, 16, 64), (12, 16, 9, 256), (16, 8, 16, 128), (5, 3, 7, 33),
+               (1, 1, 1, 6), (16, 16, 16, 1)]
+
+_TINY_OFF = """
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import paper_2212_14318_b200 as qt
+from test_gpu_small import TINY_SHAPES, tiny_inputs
+for k, (m, n, s, p) in enumerate(TINY_SHAPES):
+    a, b = tiny_inputs(m, n, s, p, k)
+    c = qt.tprod_fast(qt.CdTensor3(m, n, p, a[0], a[1]), qt.CdTensor3(n, s, p, b[0], b[1]))
+    np.save({path!r} + f"_{{k}}_1.npy", c.t1); np.save({path!r} + f"_{{k}}_2.npy", c.t2)
+print("ok")
+"""
+
+
+def tiny_inputs(m, n, s, p, k):
+    a = O.gen_random_tensor(m, n, p, 700 + 2 * k)
+    b = O.gen_random_tensor(n, s, p, 701 + 2 * k)
+    if k == 3:
+        a[1][2, 1, 0] = -np.inf
+        b[0][p - 2, 0, 3] = complex(1.0, np.nan)
+    return a, b
+
+
+@pytest.fixture(scope="module")
+def tiny_off(tmp_path_factory):
+    path = str(tmp_path_factory.mktemp("tiny") / "c")
+    env = dict(os.environ, QTB_TINY="0")
+    code = _TINY_OFF.format(root=ROOT, tests=os.path.join(ROOT, "tests"), path=path)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+    return path
+
+
+@pytest.mark.parametrize("k", range(len(TINY_SHAPES)))
+def test_tiny_stage2_bitwise_and_parity(tiny_off, k):
+    m, n, s, p = TINY_SHAPES[k]
+    a, b = tiny_inputs(m, n, s, p, k)
+    c = qt.tprod_fast(qt.CdTensor3(m, n, p, a[0], a[1]), qt.CdTensor3(n, s, p, b[0], b[1]))
+    w1 = np.load(tiny_off + f"_{k}_1.npy")
+    w2 = np.load(tiny_off + f"_{k}_2.npy")
+    assert np.array_equal(bits(c.t1), bits(w1)) and np.array_equal(bits(c.t2), bits(w2)), (m, n, s, p)
+    if k != 3 and p <= 256:
+        assert O.rel_frob_error((c.t1, c.t2), O.tprod_fast(a, b)) <= 1e-12

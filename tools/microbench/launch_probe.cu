@@ -107,7 +107,7 @@ int main() {
       {"3 empty kernels, graph+PDL", 3, 0, true, true},
       {"3 x copy 1 MB", 3, 1, false, false},         {"3 x copy 1 MB, PDL", 3, 1, true, false},
       {"3 x copy 1 MB, graph", 3, 1, false, true},   {"3 x copy 1 MB, graph+PDL", 3, 1, true, true},
-      {"5 x copy 64 MB", 5, 2, false, false},        {"5 x copy 64 MB, PDL", 5, 2, true, false},
+      {"5 x copy 64 MB", 5, 2, false, false},        {"5 x copy 64 MB, PDL", 5, 2, true, false},    {"5 x copy 64 MB, graph", 5, 2, false, true},
       {"5 x copy 64 MB, graph+PDL", 5, 2, true, true},
   };
   for (const Variant& v : vs) {
