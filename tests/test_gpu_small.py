@@ -126,7 +126,7 @@ def test_device_entry_replay_and_row_slabs():
 # cp.async-ring kernel's result ($QTB_TINY=0), which the parity tests pin to
 # the reference.
 TINY_SHAPES = [(16, 16, 16, 4096), (16, 16, 16, 64), (12, 16, 9, 256), (16, 8, 16, 128), (5, 3, 7, 33),
-               (1, 1, 1, 6), (16, 16, 16, 1)]
+               (1, 1, 1, 6), (16, 16, 16, 1), (9, 40, 13, 4096), (3, 33, 2, 4096)]
 
 _TINY_OFF = """
 import sys, numpy as np
