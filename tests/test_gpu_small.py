@@ -170,3 +170,30 @@ def test_tiny_stage2_bitwise_and_parity(tiny_off, k):
     assert np.array_equal(bits(c.t1), bits(w1)) and np.array_equal(bits(c.t2), bits(w2)), (m, n, s, p)
     if k != 3 and p <= 256:
         assert O.rel_frob_error((c.t1, c.t2), O.tprod_fast(a, b)) <= 1e-12
+
+
+def test_random_shapes_against_oracle():
+    """Random shapes inside both new kernels' domains (the one-launch cluster
+    kernel: p in {4, 8, 16}, m, s <= 32, n <= 64; the tiny-tile K2: m, s <= 16,
+    n <= 16, any p), checked against the reference restated (<= 1e-12) and the
+    definitional product (<= 1e-11)."""
+    rng = np.random.default_rng(20261020)
+    L = _native.lib()
+    fused = tiny = 0
+    for it in range(40):
+        if it % 2 == 0:
+            m, s = (int(x) for x in rng.integers(1, 33, 2))
+            n = int(rng.integers(1, 65))
+            p = int(rng.choice([4, 8, 16]))
+        else:
+            m, n, s = (int(x) for x in rng.integers(1, 17, 3))
+            p = int(rng.integers(1, 70))
+        fused += L.qt_small_fused(m, n, s, p)
+        tiny += 1 if (m <= 16 and s <= 16 and n <= 16 and not L.qt_small_fused(m, n, s, p)) else 0
+        a = O.gen_random_tensor(m, n, p, 5000 + it)
+        b = O.gen_random_tensor(n, s, p, 6000 + it)
+        c = qt.tprod_fast(qt.CdTensor3(m, n, p, a[0], a[1]), qt.CdTensor3(n, s, p, b[0], b[1]))
+        got = (c.t1, c.t2)
+        assert O.rel_frob_error(got, O.tprod_fast(a, b)) <= 1e-12, (m, n, s, p)
+        assert O.rel_frob_error(got, O.tprod_naive(a, b)) <= 1e-11, (m, n, s, p)
+    assert fused >= 15 and tiny >= 10
