@@ -559,6 +559,9 @@ def run_ours(args, cfg):
         * kp / cfg.p
     gemm_ai = 32.0 * krows * cfg.n * kcols * kp / gemm_bytes
     ridge = PEAK_FP64_DMMA_TFLOPS * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    # the DMMA stage-2 kernel this shape takes (qt_gemm.cu dmma_impl)
+    k2_name = ("K2 paired_tiny_ws_kernel (warp-specialised: bulk-copy producer warp, mbarrier ring; DMMA.8x8x4)"
+               if gauss and krows <= 16 and kcols <= 16 and cfg.n <= 16 else "K2 paired_spectral_gemm (DMMA.8x8x4)")
     algo_txt = ("gauss-3m: each complex product as 3 real DMMA products (24 m n s p executed flops)" if gauss
                 else "4m: each complex product as 4 real DMMA products (32 m n s p executed flops)")
     if algo == 1 and "k2_int8_gemm" in prof:
@@ -617,7 +620,7 @@ def run_ours(args, cfg):
     elif gemm_ai >= ridge:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
         ktf = 32.0 * krows * cfg.n * kcols * kp / (k_ms * 1e-3) / 1e12
-        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "tensor", "achieved": ktf,
+        roof = {"kernel": k2_name, "bound": "tensor", "achieved": ktf,
                 "peak": PEAK_FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ktf / PEAK_FP64_DMMA_TFLOPS,
                 "peak_source": "measured fp64 DMMA (mma.sync.m8n8k4.f64) sustained = burst, profiles/r02/peaks.json "
                                "(tools/microbench/fp64_peak.cu); MEASURED_PEAKS.json has no fp64",
@@ -631,7 +634,7 @@ def run_ours(args, cfg):
     else:
         k_ms = prof.get("k2_dmma", {}).get("ms_per_step", gemm_ms)
         gb = gemm_bytes / (k_ms * 1e-3) / 1e9
-        roof = {"kernel": "K2 paired_spectral_gemm (DMMA.8x8x4)", "bound": "hbm", "achieved": gb,
+        roof = {"kernel": k2_name, "bound": "hbm", "achieved": gb,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"],
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
                 "algorithmic": "32*(mn+ns+ms)*p bytes per launch", "algorithm": algo_txt,
