@@ -169,7 +169,7 @@ int qt_spectral_product_f64_device_ld(const double* ahat1, const double* ahat2,
 int qt_gemm_algo(uint64_t m, uint64_t n, uint64_t s, uint64_t p);
 /* 1 if qt_tprod_f64_device runs a product of this shape as ONE launch (the
  * cluster kernel of csrc/qt_small.cu: K1, K2 and K3 exchanging through
- * distributed shared memory; p in {4, 8, 16}, m, s <= 32, n <= 64, fp64 DMMA
+ * distributed shared memory; p in {2, 4, 8, 16}, m, s <= 32, n <= 64, fp64 DMMA
  * stage 2; $QTB_SMALL=0 turns it off), else 0 (three or more launches).  The
  * result is bitwise the same either way.  Same role as qt_gemm_algo: an
  * introspection entry with no reference counterpart. */

@@ -396,8 +396,8 @@ cudaError_t launch_p(const SmallArgs& a, unsigned nclusters, size_t smem, cudaSt
 
 }  // namespace
 
-// Shapes the one-launch kernel takes: p in {4, 8, 16} (two frequencies per
-// CTA, clusters of 2-8), the small DMMA tiles' region of the three-launch path
+// Shapes the one-launch kernel takes: p in {2, 4, 8, 16} (two frequencies per
+// CTA, clusters of 1-8), the small DMMA tiles' region of the three-launch path
 // (m, s <= 32, qt_gemm.cu) and n <= 64 (operands of both slots in shared
 // memory), fp64 DMMA stage 2 with Gauss 3M and slice_reflect.  $QTB_SMALL=0
 // turns it off (the three-launch path then runs; bitwise the same result).
@@ -407,7 +407,7 @@ bool small_fused_eligible(uint64_t m, uint64_t n, uint64_t s, uint64_t p) {
     return !(v && *v == '0');
   }();
   if (!on || m == 0 || n == 0 || s == 0) return false;
-  if (!(p == 4 || p == 8 || p == 16)) return false;
+  if (!(p == 2 || p == 4 || p == 8 || p == 16)) return false;
   if (m > 32 || s > 32 || n > (uint64_t)kMaxN) return false;
   return choose_gemm_algo(n, s, p) == kAlgoDmma && dmma_gauss() && !debug_noreflect();
 }
@@ -434,7 +434,8 @@ cudaError_t launch_small_tprod(const double2* a1, const double2* a2, const doubl
   const size_t smem = small_smem(n, p);
   ProfScope ps("small_fused", stream);
   cudaError_t e;
-  if (p == 4) e = launch_p<4>(a, nclusters, smem, stream);
+  if (p == 2) e = launch_p<2>(a, nclusters, smem, stream);
+  else if (p == 4) e = launch_p<4>(a, nclusters, smem, stream);
   else if (p == 8) e = launch_p<8>(a, nclusters, smem, stream);
   else e = launch_p<16>(a, nclusters, smem, stream);
   ps.stop();

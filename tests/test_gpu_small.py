@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # config 1; edges of the 8 x 16 cluster block (rows, columns, K padding to 16,
 # n = 1, the largest n) for every supported p
 SHAPES = [(32, 32, 32, 16), (8, 8, 8, 4), (24, 20, 17, 8), (5, 64, 31, 16), (32, 1, 32, 4), (1, 16, 1, 16),
-          (9, 48, 3, 8), (17, 7, 16, 16), (31, 33, 29, 4)]
+          (9, 48, 3, 8), (17, 7, 16, 16), (31, 33, 29, 4), (13, 20, 30, 2)]
 
 
 def bits(x):
@@ -70,7 +70,8 @@ def test_selection():
     assert L.qt_small_fused(32, 64, 32, 8) == 1
     assert L.qt_small_fused(33, 32, 32, 16) == 0  # beyond the small DMMA tiles
     assert L.qt_small_fused(32, 65, 32, 16) == 0  # operands exceed shared memory
-    assert L.qt_small_fused(32, 32, 32, 12) == 0  # p not in {4, 8, 16}
+    assert L.qt_small_fused(32, 32, 32, 12) == 0  # p not in {2, 4, 8, 16}
+    assert L.qt_small_fused(32, 32, 32, 2) == 1
     assert L.qt_small_fused(16, 16, 16, 4096) == 0  # config 3
 
 
@@ -174,7 +175,7 @@ def test_tiny_stage2_bitwise_and_parity(tiny_off, k):
 
 def test_random_shapes_against_oracle():
     """Random shapes inside both new kernels' domains (the one-launch cluster
-    kernel: p in {4, 8, 16}, m, s <= 32, n <= 64; the tiny-tile K2: m, s <= 16,
+    kernel: p in {2, 4, 8, 16}, m, s <= 32, n <= 64; the tiny-tile K2: m, s <= 16,
     n <= 16, any p), checked against the reference restated (<= 1e-12) and the
     definitional product (<= 1e-11)."""
     rng = np.random.default_rng(20261020)
@@ -184,7 +185,7 @@ def test_random_shapes_against_oracle():
         if it % 2 == 0:
             m, s = (int(x) for x in rng.integers(1, 33, 2))
             n = int(rng.integers(1, 65))
-            p = int(rng.choice([4, 8, 16]))
+            p = int(rng.choice([2, 4, 8, 16]))
         else:
             m, n, s = (int(x) for x in rng.integers(1, 17, 3))
             p = int(rng.integers(1, 70))
