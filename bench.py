@@ -591,6 +591,13 @@ def run_ours(args, cfg):
                                "kernels of neighbouring batches run beside this kernel (kernel_ms is its own "
                                "event-timed duration, which includes that sharing)",
                 "traffic": None}
+        # the same rate against the peak at the SM clock this run held (the
+        # power cap sets the clock; the rated burst is 4387 TOPS at 1965 MHz)
+        csum = clk.summary()
+        if csum.get("sm_mhz"):
+            per_clk = peak_i8_burst / 1965.0 * csum["sm_mhz"]
+            roof["frac_at_measured_clock"] = ach / per_clk
+            roof["peak_at_measured_clock"] = per_clk
         if "k2_int8_gemm" in prof_iso:
             iso_ms = prof_iso["k2_int8_gemm"]["ms_per_step"]
             roof["isolated"] = {"kernel_ms": iso_ms, "achieved": ops / (iso_ms * 1e-3) / 1e12,
