@@ -76,7 +76,7 @@ def grid_for(m, s):
 
 
 @needs_ref
-@pytest.mark.parametrize("c", [2, 3, 4])
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
 def test_full_tensor_matches_reference(c):
     cfg = qt.CONFIGS[c]
     a, b = qt.make_inputs(cfg)
