@@ -4,18 +4,22 @@
 //
 // A small product is latency-bound: K1, K2 and K3 are three short kernels
 // whose launch gaps and cold-cache round trips cost more than their work
-// (DESIGN.md §7).  Here a cluster of Q = p/2 CTAs owns an 8 x 8 block
-// of C and does all three stages without touching global memory in
-// between:
+// (DESIGN.md §7).  Here a cluster of Q = p/2 CTAs owns an 8 x 8 block of C
+// and does all three stages without touching global memory in between:
 //   1. forward tube FFTs (K1) of the block's A rows and B columns, spread
 //      over the cluster's CTAs, one tube per thread in registers; every output
-//      frequency is stored straight into the shared memory of the CTA that
-//      owns that frequency (st through a cluster-mapped address);
-//   2. cluster barrier; each CTA runs the paired-frequency product (K2) of its
-//      two frequency slices — a pair (k, p - k), or the two self-paired
-//      frequencies 0 and p/2 — on the FP64 tensor pipe (DMMA m8n8k4) and stores
-//      each Ĉ value into the CTA that inverts that tube;
-//   3. cluster barrier; inverse tube FFTs (K3) and the only global stores.
+//      frequency is st.async'ed straight into the shared memory of the CTA
+//      that owns that frequency, its bytes counted on that CTA's mbarrier;
+//   2. each CTA waits for its own operand bytes only, runs the
+//      paired-frequency product (K2) of its two frequency slices — a pair
+//      (k, p - k), or the two self-paired frequencies 0 and p/2 — on the FP64
+//      tensor pipe (DMMA m8n8k4) and st.async's each Ĉ value into the CTA that
+//      inverts that tube (again counted on an mbarrier: a CTA leaves only
+//      after every byte addressed to it has landed, and what it sends comes
+//      from registers, so no CTA's shared memory is written after it exits);
+//   3. inverse tube FFTs (K3) and the only global stores.
+// One cluster barrier, at entry (every CTA running, its mbarriers
+// initialised and its operands zeroed), split around the first tube loads.
 // Every tube is transformed with the same butterflies and twiddles as
 // qt_fft.cu, and every Ĉ element gets the same DMMA sequence (Gauss 3M, K-steps
 // of 4 in order, zero padding to 16) as qt_gemm.cu's small tiles, so the
